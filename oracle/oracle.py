@@ -1,0 +1,278 @@
+"""ctypes access to the CPU checkers. TEST INFRASTRUCTURE ONLY.
+
+Only tests/, __graft_entry__.smoke() and bench.py (cpu_baseline leg and the
+`--impl reference` arm) may import this module. It never backs the product.
+
+* `Port`      -> oracle/liboracle.so, the plain-C restatement (swr_oracle.c)
+* `Reference` -> oracle/_ref/libwrfref.so (or _nofma), the reference library
+                 compiled from /root/reference sources (oracle/Makefile)
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+import subprocess
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+PORT_SO = os.path.join(HERE, "liboracle.so")
+REF_SO = os.path.join(HERE, "_ref", "libwrfref.so")
+REF_NOFMA_SO = os.path.join(HERE, "_ref", "libwrfref_nofma.so")
+
+_fp = C.POINTER(C.c_float)
+_ip = C.POINTER(C.c_int)
+_dp = C.POINTER(C.c_double)
+
+
+def build(ref: bool = True) -> None:
+    """Compile the checkers (liboracle.so always; _ref only where the reference sources exist)."""
+    targets = ["oracle"] + (["ref"] if ref and os.path.isdir("/root/reference/proj/src") else [])
+    subprocess.run(["make", "-s", "-C", HERE] + targets, check=True)
+
+
+def _f(a):
+    return a.ctypes.data_as(_fp) if a is not None else None
+
+
+def _i(a):
+    return a.ctypes.data_as(_ip) if a is not None else None
+
+
+def _d(a):
+    return a.ctypes.data_as(_dp) if a is not None else None
+
+
+def _c32(a):
+    return np.ascontiguousarray(a, dtype=np.float32)
+
+
+class _SoSet(C.Structure):
+    _fields_ = [("H", C.c_int), ("W", C.c_int), ("n", C.c_int), ("center_raw", _fp),
+                ("cholesky", _fp), ("atten_logit", _fp), ("response", _fp)]
+
+
+class _SoNet(C.Structure):
+    _fields_ = [("width", C.c_int), ("bands_c", C.c_int), ("bands_p", C.c_int),
+                ("w", _fp * 11), ("b", _fp * 11)]
+
+
+def _split_res(res):
+    if res is None:
+        return None, None, None
+    dc, dr, da = res
+    return _c32(dc), _c32(dr), _c32(da)
+
+
+class Port:
+    """The plain-C restatement (swr_oracle.c)."""
+
+    def __init__(self, scene):
+        self.lib = C.CDLL(PORT_SO)
+        L = self.lib
+        L.so_prepare.restype = C.c_int64
+        L.so_pooled.restype = C.c_double
+        self.sc = scene
+        self._keep = [_c32(scene.center_raw), _c32(scene.cholesky), _c32(scene.atten_logit),
+                      _c32(scene.response)]
+        self.set = _SoSet(scene.H, scene.W, scene.n, *[_f(a) for a in self._keep])
+        self._w = [_c32(w) for w in scene.weights]
+        self._b = [_c32(b) for b in scene.biases]
+        if self._w:
+            self.net = _SoNet(scene.width, scene.bands_c, scene.bands_p,
+                              (_fp * 11)(*[_f(w) for w in self._w]), (_fp * 11)(*[_f(b) for b in self._b]))
+
+    def normalize(self, pos_m):
+        out = np.zeros(3, np.float32)
+        bmin = np.array(self.sc.bbox_min, np.float64)
+        bmax = np.array(self.sc.bbox_max, np.float64)
+        self.lib.so_normalize_position(_d(bmin), _d(bmax), _f(_c32(pos_m)), _f(out))
+        return out
+
+    def predict(self, pos01, precise=False):
+        n = self.sc.n
+        dc, dr, da = np.zeros((n, 2), np.float32), np.zeros((n, 2), np.float32), np.zeros(n, np.float32)
+        rc = self.lib.so_predict(C.byref(self.net), C.byref(self.set), _f(_c32(pos01)), int(precise),
+                                 _f(dc), _f(dr), _f(da))
+        if rc:
+            raise RuntimeError(f"so_predict failed ({rc})")
+        return dc, dr, da
+
+    def prepare(self, res=None):
+        sc = self.sc
+        dc, dr, da = _split_res(res)
+        n = sc.n
+        tiles = ((sc.H + sc.tile - 1) // sc.tile) * ((sc.W + sc.tile - 1) // sc.tile)
+        state = np.zeros((n, 11), np.float32)
+        rows = np.zeros((n, 2), np.int32)
+        cols = np.zeros((n, 2), np.int32)
+        off = np.zeros(tiles + 1, np.int32)
+        pairs = self.lib.so_prepare(C.byref(self.set), _f(dc), _f(dr), _f(da), C.c_float(sc.cutoff), sc.tile,
+                                    _f(state), _i(rows), _i(cols), _i(off), None, C.c_int64(0))
+        prims = np.zeros(max(pairs, 1), np.int32)
+        self.lib.so_prepare(C.byref(self.set), _f(dc), _f(dr), _f(da), C.c_float(sc.cutoff), sc.tile,
+                            _f(state), _i(rows), _i(cols), _i(off), _i(prims), C.c_int64(pairs))
+        return dict(state=state, rows=rows, cols=cols, tile_offset=off, tile_prims=prims[:pairs])
+
+    def rasterize(self, res=None, precise=True):
+        sc = self.sc
+        dc, dr, da = _split_res(res)
+        out = np.zeros((sc.H, sc.W, 2), np.float32)
+        self.lib.so_rasterize(C.byref(self.set), _f(dc), _f(dr), _f(da), C.c_float(sc.cutoff), sc.tile,
+                              int(precise), _f(out))
+        return out
+
+    def render(self, pos_m, precise=True):
+        res = self.predict(self.normalize(pos_m), precise=precise)
+        return self.rasterize(res, precise=precise), res
+
+    def aoa(self, spec):
+        H, W = spec.shape[0], spec.shape[1]
+        r, c, el, az = C.c_int(), C.c_int(), C.c_double(), C.c_double()
+        self.lib.so_aoa(_f(_c32(spec)), H, W, C.byref(r), C.byref(c), C.byref(el), C.byref(az))
+        return r.value, c.value, el.value, az.value
+
+    def pooled(self, spec):
+        return self.lib.so_pooled(_f(_c32(spec)), spec.shape[0] * spec.shape[1])
+
+
+class Reference:
+    """The reference library built from /root/reference sources (oracle/_ref)."""
+
+    def __init__(self, scene=None, path=None, nofma=False, handle=None):
+        so = REF_NOFMA_SO if nofma else REF_SO
+        if not os.path.exists(so):
+            raise FileNotFoundError(f"{so} missing: run `make -C oracle ref` where /root/reference exists")
+        self.lib = L = C.CDLL(so)
+        L.wref_ck_load.restype = C.c_void_p
+        L.wref_ck_create.restype = C.c_void_p
+        L.wref_ck_init_random.restype = C.c_void_p
+        L.wref_last_error.restype = C.c_char_p
+        L.wref_pooled.restype = C.c_double
+        L.wref_kernel_weight.restype = C.c_float
+        for fn in ("wref_ck_save", "wref_ck_free", "wref_ck_info", "wref_normalize", "wref_predict",
+                   "wref_rasterize", "wref_render_at", "wref_render_batch", "wref_ck_arrays"):
+            getattr(L, fn).argtypes = None
+        self.sc = scene
+        if handle is not None:
+            self.h = handle
+        elif path is not None:
+            self.h = L.wref_ck_load(path.encode())
+        else:
+            sc = scene
+            self._keep = [_c32(sc.center_raw), _c32(sc.cholesky), _c32(sc.atten_logit), _c32(sc.response)]
+            lw = lb = None
+            if sc.weights:
+                self._w = [_c32(w) for w in sc.weights]
+                self._b = [_c32(b) for b in sc.biases]
+                lw = (_fp * 11)(*[_f(w) for w in self._w])
+                lb = (_fp * 11)(*[_f(b) for b in self._b])
+            bmin = np.array(sc.bbox_min, np.float64)
+            bmax = np.array(sc.bbox_max, np.float64)
+            self.h = L.wref_ck_create(sc.H, sc.W, sc.n, *[_f(a) for a in self._keep], sc.width, sc.bands_c,
+                                      sc.bands_p, lw, lb, C.c_float(sc.cutoff), sc.tile, _d(bmin), _d(bmax))
+        if not self.h:
+            raise RuntimeError(self.lib.wref_last_error().decode())
+        self.h = C.c_void_p(self.h)
+        if self.sc is None:
+            self.sc = self._scene_from_handle()
+
+    def _scene_from_handle(self):
+        from paper_2506_12787_b200.scene import Scene
+        ints = np.zeros(6, np.int32)
+        cut = C.c_float()
+        bbox = np.zeros(6, np.float64)
+        bp = self.lib.wref_ck_info(self.h, _i(ints), C.byref(cut), _d(bbox))
+        H, W, n, width, bc, tile = map(int, ints)
+        sc = Scene(H=H, W=W, center_raw=np.zeros((n, 2), np.float32), cholesky=np.zeros((n, 3), np.float32),
+                   atten_logit=np.zeros(n, np.float32), response=np.zeros((n, 2), np.float32),
+                   width=width, bands_c=bc, bands_p=bp, cutoff=cut.value, tile=tile,
+                   bbox_min=tuple(bbox[:3]), bbox_max=tuple(bbox[3:]))
+        sc.weights = [np.zeros(s, np.float32) for s in sc.layer_shapes()]
+        sc.biases = [np.zeros(s[0], np.float32) for s in sc.layer_shapes()]
+        self.lib.wref_ck_arrays(self.h, _f(sc.center_raw), _f(sc.cholesky), _f(sc.atten_logit),
+                                _f(sc.response), (_fp * 11)(*[_f(w) for w in sc.weights]),
+                                (_fp * 11)(*[_f(b) for b in sc.biases]))
+        return sc
+
+    def __del__(self):
+        try:
+            self.lib.wref_ck_free(self.h)
+        except Exception:
+            pass
+
+    def _check(self, rc):
+        if rc:
+            raise RuntimeError(self.lib.wref_last_error().decode())
+
+    def set_threads(self, n):
+        self.lib.wref_set_threads(int(n))
+
+    def save(self, path):
+        self._check(self.lib.wref_ck_save(self.h, path.encode()))
+
+    def normalize(self, pos_m):
+        out = np.zeros(3, np.float32)
+        self._check(self.lib.wref_normalize(self.h, _f(_c32(pos_m)), _f(out)))
+        return out
+
+    def predict(self, pos01):
+        n = self.sc.n
+        dc, dr, da = np.zeros((n, 2), np.float32), np.zeros((n, 2), np.float32), np.zeros(n, np.float32)
+        self._check(self.lib.wref_predict(self.h, _f(_c32(pos01)), _f(dc), _f(dr), _f(da)))
+        return dc, dr, da
+
+    def rasterize(self, res=None, workspace=False):
+        sc = self.sc
+        n = sc.n
+        dc, dr, da = _split_res(res)
+        tiles = ((sc.H + sc.tile - 1) // sc.tile) * ((sc.W + sc.tile - 1) // sc.tile)
+        out = np.zeros((sc.H, sc.W, 2), np.float32)
+        if not workspace:
+            self._check(self.lib.wref_rasterize(self.h, _f(dc), _f(dr), _f(da), _f(out), None, None, None,
+                                                None, None, C.c_longlong(0), None))
+            return out
+        state = np.zeros((n, 11), np.float32)
+        rows = np.zeros((n, 2), np.int32)
+        cols = np.zeros((n, 2), np.int32)
+        off = np.zeros(tiles + 1, np.int32)
+        npairs = C.c_longlong()
+        self._check(self.lib.wref_rasterize(self.h, _f(dc), _f(dr), _f(da), _f(out), _f(state), _i(rows),
+                                            _i(cols), _i(off), None, C.c_longlong(0), C.byref(npairs)))
+        prims = np.zeros(max(npairs.value, 1), np.int32)
+        self._check(self.lib.wref_rasterize(self.h, _f(dc), _f(dr), _f(da), None, None, None, None, None,
+                                            _i(prims), C.c_longlong(npairs.value), None))
+        return out, dict(state=state, rows=rows, cols=cols, tile_offset=off, tile_prims=prims[:npairs.value])
+
+    def render_at(self, pos_m):
+        out = np.zeros((self.sc.H, self.sc.W, 2), np.float32)
+        self._check(self.lib.wref_render_at(self.h, _f(_c32(pos_m)), _f(out)))
+        return out
+
+    def render_batch(self, pos_m, mode=1, spectra=True):
+        pos = _c32(pos_m).reshape(-1, 3)
+        B = pos.shape[0]
+        sp = np.zeros((B, self.sc.H, self.sc.W, 2), np.float32) if spectra else None
+        pooled = np.zeros(B, np.float64)
+        rc = np.zeros((B, 2), np.int32)
+        ang = np.zeros((B, 2), np.float64)
+        self._check(self.lib.wref_render_batch(self.h, B, _f(pos), _f(sp), _d(pooled), _i(rc), _d(ang), mode))
+        return sp, pooled, rc, ang
+
+    def aoa(self, spec):
+        H, W = spec.shape[0], spec.shape[1]
+        r, c, el, az = C.c_int(), C.c_int(), C.c_double(), C.c_double()
+        self._check(self.lib.wref_aoa(_f(_c32(spec)), H, W, C.byref(r), C.byref(c), C.byref(el), C.byref(az)))
+        return r.value, c.value, el.value, az.value
+
+    def pooled(self, spec):
+        return self.lib.wref_pooled(_f(_c32(spec)), spec.shape[0], spec.shape[1])
+
+    def materialize_center(self, rel, raz, double=False):
+        if double:
+            el, az = C.c_double(), C.c_double()
+            self.lib.wref_materialize_center_d(C.c_double(rel), C.c_double(raz), C.byref(el), C.byref(az))
+        else:
+            el, az = C.c_float(), C.c_float()
+            self.lib.wref_materialize_center_f(C.c_float(rel), C.c_float(raz), C.byref(el), C.byref(az))
+        return el.value, az.value

@@ -1,0 +1,410 @@
+// C entry points into the reference library built from /root/reference sources.
+// TEST INFRASTRUCTURE ONLY (the CPU checker and the `--impl reference` bench arm):
+// nothing in the product links or loads this. Every function forwards to the
+// reference's own public API:
+//   train::load_checkpoint / save_checkpoint   checkpoint.cpp:100-146 / :51-98
+//   train::normalize_position / render_at      training.cpp:178-195
+//   deform::predict_residuals                  deform.hpp:106-109 (restated GEMM, see deform_restated.cpp)
+//   splat::rasterize (workspace exposed)        splat.cpp:312-482, prepare() :159-294
+//   tasks::aoa_extract / pooled_magnitude       tasks.cpp:154-169 / :32-39
+// Exceptions are caught and mapped to status codes (0 ok, 1 invalid_argument,
+// 2 runtime_error, 3 other) with the message kept for wref_last_error().
+
+#include <omp.h>
+
+#include <cstring>
+#include <stdexcept>
+#include <string>
+
+#include "wrfsplat/deform.hpp"
+#include "wrfsplat/splat.hpp"
+#include "wrfsplat/tasks.hpp"
+#include "wrfsplat/training.hpp"
+
+using namespace wrfsplat;
+
+namespace
+{
+thread_local std::string g_err;
+
+template <class F>
+int guarded(F &&f)
+{
+    try
+    {
+        f();
+        return 0;
+    }
+    catch (const std::invalid_argument &e)
+    {
+        g_err = e.what();
+        return 1;
+    }
+    catch (const std::runtime_error &e)
+    {
+        g_err = e.what();
+        return 2;
+    }
+    catch (const std::exception &e)
+    {
+        g_err = e.what();
+        return 3;
+    }
+}
+
+train::Checkpoint *ck_of(void *h) { return static_cast<train::Checkpoint *>(h); }
+
+void fill_spectrum(const Spectrum &s, float *dst)
+{
+    std::memcpy(dst, s.data.data(), s.data.size() * sizeof(float));
+}
+
+Spectrum wrap_spectrum(const float *src, int H, int W)
+{
+    Spectrum s(AngularGrid{H, W});
+    std::memcpy(s.data.data(), src, s.data.size() * sizeof(float));
+    return s;
+}
+} // namespace
+
+extern "C" {
+
+const char *wref_last_error() { return g_err.c_str(); }
+
+void wref_set_threads(int n) { omp_set_num_threads(n); }
+int wref_max_threads() { return omp_get_max_threads(); }
+
+void *wref_ck_load(const char *path)
+{
+    train::Checkpoint *out = nullptr;
+    const int rc = guarded([&] { out = new train::Checkpoint(train::load_checkpoint(path)); });
+    return rc == 0 ? out : nullptr;
+}
+
+// Build a checkpoint from raw arrays. lw/lb hold the 11 layers in WRFD order
+// (8 trunk, center, response, atten head); lw == nullptr leaves the net empty
+// (rasterize-only scenes).
+void *wref_ck_create(int H, int W, int n, const float *center_raw, const float *cholesky,
+                     const float *atten_logit, const float *response, int width, int bands_c,
+                     int bands_p, const float *const *lw, const float *const *lb, float cutoff,
+                     int tile, const double *bbox_min, const double *bbox_max)
+{
+    auto *ck = new train::Checkpoint();
+    const int rc = guarded([&] {
+        ck->set.grid = AngularGrid{H, W};
+        ck->set.resize(n);
+        std::memcpy(ck->set.center_raw.data(), center_raw, sizeof(float) * 2 * std::size_t(n));
+        std::memcpy(ck->set.cholesky.data(), cholesky, sizeof(float) * 3 * std::size_t(n));
+        std::memcpy(ck->set.atten_logit.data(), atten_logit, sizeof(float) * std::size_t(n));
+        std::memcpy(ck->set.response.data(), response, sizeof(float) * 2 * std::size_t(n));
+        ck->config.raster.cutoff_radius = cutoff;
+        ck->config.raster.tile = tile;
+        ck->config.primitives = n;
+        if (lw)
+        {
+            ck->net.width = width;
+            ck->net.enc.bands_center = bands_c;
+            ck->net.enc.bands_position = bands_p;
+            ck->config.width = width;
+            ck->config.enc = ck->net.enc;
+            Rng dummy(0);
+            ck->net.init(dummy); // allocates shapes; every value is overwritten below
+            deform::DeformNet::Layer *ls[11];
+            for (int i = 0; i < 8; i++)
+                ls[i] = &ck->net.trunk[std::size_t(i)];
+            ls[8] = &ck->net.head_center;
+            ls[9] = &ck->net.head_response;
+            ls[10] = &ck->net.head_atten;
+            for (int i = 0; i < 11; i++)
+            {
+                std::memcpy(ls[i]->w.data(), lw[i], sizeof(float) * ls[i]->w.size());
+                std::memcpy(ls[i]->b.data(), lb[i], sizeof(float) * ls[i]->b.size());
+            }
+        }
+        for (int a = 0; a < 3; a++)
+        {
+            ck->bbox_min[std::size_t(a)] = bbox_min ? bbox_min[a] : 0.0;
+            ck->bbox_max[std::size_t(a)] = bbox_max ? bbox_max[a] : 1.0;
+        }
+    });
+    if (rc != 0)
+    {
+        delete ck;
+        return nullptr;
+    }
+    return ck;
+}
+
+int wref_ck_save(void *h, const char *path)
+{
+    return guarded([&] { train::save_checkpoint(path, *ck_of(h)); });
+}
+
+void wref_ck_free(void *h) { delete ck_of(h); }
+
+// grid (H, W), n, net width and bands, raster params, bbox (6 doubles)
+int wref_ck_info(void *h, int *ints6, float *cutoff, double *bbox6)
+{
+    const auto &ck = *ck_of(h);
+    ints6[0] = ck.set.grid.n_elevation;
+    ints6[1] = ck.set.grid.n_azimuth;
+    ints6[2] = ck.set.n;
+    ints6[3] = ck.net.width;
+    ints6[4] = ck.net.enc.bands_center;
+    ints6[5] = ck.config.raster.tile;
+    *cutoff = ck.config.raster.cutoff_radius;
+    for (int a = 0; a < 3; a++)
+    {
+        bbox6[a] = ck.bbox_min[std::size_t(a)];
+        bbox6[3 + a] = ck.bbox_max[std::size_t(a)];
+    }
+    return ck.net.enc.bands_position;
+}
+
+// Copy out the Gaussian set and the 11 layers (caller sizes the buffers)
+int wref_ck_arrays(void *h, float *center_raw, float *cholesky, float *atten, float *response,
+                   float *const *lw, float *const *lb)
+{
+    const auto &ck = *ck_of(h);
+    const auto &s = ck.set;
+    std::memcpy(center_raw, s.center_raw.data(), sizeof(float) * s.center_raw.size());
+    std::memcpy(cholesky, s.cholesky.data(), sizeof(float) * s.cholesky.size());
+    std::memcpy(atten, s.atten_logit.data(), sizeof(float) * s.atten_logit.size());
+    std::memcpy(response, s.response.data(), sizeof(float) * s.response.size());
+    if (lw && ck.net.trunk.size() == 8)
+    {
+        const deform::DeformNet::Layer *ls[11];
+        for (int i = 0; i < 8; i++)
+            ls[i] = &ck.net.trunk[std::size_t(i)];
+        ls[8] = &ck.net.head_center;
+        ls[9] = &ck.net.head_response;
+        ls[10] = &ck.net.head_atten;
+        for (int i = 0; i < 11; i++)
+        {
+            std::memcpy(lw[i], ls[i]->w.data(), sizeof(float) * ls[i]->w.size());
+            std::memcpy(lb[i], ls[i]->b.data(), sizeof(float) * ls[i]->b.size());
+        }
+    }
+    return 0;
+}
+
+int wref_normalize(void *h, const float *pos_m, float *out01)
+{
+    return guarded([&] {
+        const auto p = train::normalize_position(*ck_of(h), {pos_m[0], pos_m[1], pos_m[2]});
+        out01[0] = p[0];
+        out01[1] = p[1];
+        out01[2] = p[2];
+    });
+}
+
+int wref_predict(void *h, const float *pos01, float *d_center, float *d_response, float *d_atten)
+{
+    return guarded([&] {
+        const auto &ck = *ck_of(h);
+        deform::DeformWorkspace ws;
+        splat::Residuals res;
+        deform::predict_residuals(ck.net, ck.set, {pos01[0], pos01[1], pos01[2]}, ws, res);
+        std::memcpy(d_center, res.d_center.data(), sizeof(float) * res.d_center.size());
+        std::memcpy(d_response, res.d_response.data(), sizeof(float) * res.d_response.size());
+        std::memcpy(d_atten, res.d_atten.data(), sizeof(float) * res.d_atten.size());
+    });
+}
+
+// rasterize(set, residuals-or-null, params) and expose the workspace.
+// state: n*11 floats, rows/cols: n*2 ints, tile_offset: tiles+1 ints,
+// tile_prims: up to prims_cap ints (the true pair count lands in *n_pairs).
+int wref_rasterize(void *h, const float *d_center, const float *d_response, const float *d_atten,
+                   float *spectrum, float *state, int *rows, int *cols, int *tile_offset,
+                   int *tile_prims, long long prims_cap, long long *n_pairs)
+{
+    return guarded([&] {
+        const auto &ck = *ck_of(h);
+        splat::Residuals res;
+        const splat::Residuals *rp = nullptr;
+        if (d_center)
+        {
+            res.resize(ck.set.n);
+            std::memcpy(res.d_center.data(), d_center, sizeof(float) * res.d_center.size());
+            std::memcpy(res.d_response.data(), d_response, sizeof(float) * res.d_response.size());
+            std::memcpy(res.d_atten.data(), d_atten, sizeof(float) * res.d_atten.size());
+            rp = &res;
+        }
+        splat::RasterWorkspace ws;
+        Spectrum out;
+        splat::rasterize<float>(ck.set, rp, ck.config.raster, out, ws);
+        if (spectrum)
+            fill_spectrum(out, spectrum);
+        if (state)
+            std::memcpy(state, ws.state.data(), sizeof(float) * ws.state.size());
+        if (rows)
+            std::memcpy(rows, ws.row_range.data(), sizeof(int) * ws.row_range.size());
+        if (cols)
+            std::memcpy(cols, ws.col_range.data(), sizeof(int) * ws.col_range.size());
+        if (tile_offset)
+            std::memcpy(tile_offset, ws.tile_offset.data(), sizeof(int) * ws.tile_offset.size());
+        if (n_pairs)
+            *n_pairs = (long long)ws.tile_prims.size();
+        if (tile_prims)
+        {
+            const std::size_t m = std::min<std::size_t>(ws.tile_prims.size(), std::size_t(prims_cap));
+            std::memcpy(tile_prims, ws.tile_prims.data(), sizeof(int) * m);
+        }
+    });
+}
+
+int wref_render_at(void *h, const float *pos_m, float *spectrum)
+{
+    return guarded([&] {
+        const auto s = train::render_at(*ck_of(h), {pos_m[0], pos_m[1], pos_m[2]});
+        fill_spectrum(s, spectrum);
+    });
+}
+
+// Batched consumer loop over render_at (the CPU baseline).
+// mode 0: reference as shipped — positions in sequence, OpenMP inside each render.
+// mode 1: position-parallel — one position per thread, nested regions serial.
+// Any output pointer may be null. aoa_rc = [B][2] ints, aoa_ang = [B][2] (el, az).
+int wref_render_batch(void *h, int B, const float *pos_m, float *spectra, double *pooled,
+                      int *aoa_rc, double *aoa_ang, int mode)
+{
+    return guarded([&] {
+        const auto &ck = *ck_of(h);
+        const std::size_t per = std::size_t(2) * ck.set.grid.cells();
+        auto one = [&](int b) {
+            const Spectrum s = train::render_at(ck, {pos_m[3 * b], pos_m[3 * b + 1], pos_m[3 * b + 2]});
+            if (spectra)
+                std::memcpy(spectra + per * std::size_t(b), s.data.data(), per * sizeof(float));
+            if (pooled)
+                pooled[b] = tasks::pooled_magnitude(s);
+            if (aoa_rc || aoa_ang)
+            {
+                const auto e = tasks::aoa_extract(s);
+                if (aoa_rc)
+                {
+                    aoa_rc[2 * b] = e.row;
+                    aoa_rc[2 * b + 1] = e.col;
+                }
+                if (aoa_ang)
+                {
+                    aoa_ang[2 * b] = e.elevation;
+                    aoa_ang[2 * b + 1] = e.azimuth;
+                }
+            }
+        };
+        if (mode == 0)
+        {
+            for (int b = 0; b < B; b++)
+                one(b);
+        }
+        else
+        {
+            const int keep = omp_get_max_active_levels();
+            omp_set_max_active_levels(1);
+            std::string first_err;
+#pragma omp parallel for schedule(dynamic, 1)
+            for (int b = 0; b < B; b++)
+            {
+                try
+                {
+                    one(b);
+                }
+                catch (const std::exception &e)
+                {
+#pragma omp critical
+                    first_err = e.what();
+                }
+            }
+            omp_set_max_active_levels(keep);
+            if (!first_err.empty())
+                throw std::runtime_error(first_err);
+        }
+    });
+}
+
+int wref_aoa(const float *spectrum, int H, int W, int *row, int *col, double *el, double *az)
+{
+    return guarded([&] {
+        const auto e = tasks::aoa_extract(wrap_spectrum(spectrum, H, W));
+        *row = e.row;
+        *col = e.col;
+        *el = e.elevation;
+        *az = e.azimuth;
+    });
+}
+
+double wref_pooled(const float *spectrum, int H, int W)
+{
+    return tasks::pooled_magnitude(wrap_spectrum(spectrum, H, W));
+}
+
+int wref_magnitude(const float *spectrum, int H, int W, float *out)
+{
+    const auto m = magnitude(wrap_spectrum(spectrum, H, W));
+    std::memcpy(out, m.data(), sizeof(float) * m.size());
+    return 0;
+}
+
+void wref_materialize_center_f(float rel, float raz, float *el, float *az)
+{
+    const auto c = splat::materialize_center<float>(rel, raz);
+    *el = c.elevation;
+    *az = c.azimuth;
+}
+
+void wref_materialize_center_d(double rel, double raz, double *el, double *az)
+{
+    const auto c = splat::materialize_center<double>(rel, raz);
+    *el = c.elevation;
+    *az = c.azimuth;
+}
+
+int wref_encode_f(const float *values, int count, int bands, float *out)
+{
+    deform::encode<float>(values, count, bands, out);
+    return 0;
+}
+
+float wref_kernel_weight(void *h, int idx, float az, float el, const float *d_center,
+                         const float *d_response, const float *d_atten)
+{
+    float out = -1.0f;
+    guarded([&] {
+        const auto &ck = *ck_of(h);
+        splat::Residuals res;
+        const splat::Residuals *rp = nullptr;
+        if (d_center)
+        {
+            res.resize(ck.set.n);
+            std::memcpy(res.d_center.data(), d_center, sizeof(float) * res.d_center.size());
+            std::memcpy(res.d_response.data(), d_response, sizeof(float) * res.d_response.size());
+            std::memcpy(res.d_atten.data(), d_atten, sizeof(float) * res.d_atten.size());
+            rp = &res;
+        }
+        out = splat::kernel_weight<float>(ck.set, idx, az, el, rp);
+    });
+    return out;
+}
+
+// The reference's init_random + DeformNet::init for seeded parity scenes
+// (splat.cpp:681-709, deform.cpp:72-102; draw order: set, then net).
+void *wref_ck_init_random(int H, int W, int n, unsigned long long seed)
+{
+    auto *ck = new train::Checkpoint();
+    const int rc = guarded([&] {
+        Rng rng(seed);
+        ck->set = splat::init_random(AngularGrid{H, W}, n, rng);
+        ck->net.init(rng);
+        ck->config.primitives = n;
+        ck->bbox_min = {0, 0, 0};
+        ck->bbox_max = {1, 1, 1};
+    });
+    if (rc != 0)
+    {
+        delete ck;
+        return nullptr;
+    }
+    return ck;
+}
+
+} // extern "C"
