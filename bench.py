@@ -1,0 +1,347 @@
+#!/usr/bin/env python
+"""Benchmark: batched SwiftWRF spectrum rendering on B200 (BASELINE.json metric
+"spectra/sec at 1/2/4/8 B200 vs CPU ref on host cores; % roofline").
+
+One step = one pass of the hot path (position prep -> deformation MLP -> setup
+-> tile binning -> tile raster -> heads) over one batch of TX positions of
+BASELINE config 2: 50k Gaussians, 1024 positions per GPU, outputs spectra +
+pooled magnitude + RSSI, 90x360 grid, deformation MLP width 156. Synthetic,
+seeded scene (paper_2506_12787_b200.scene.make_scene) and positions.
+
+    python bench.py [--steps K] [--warmup W]                       # 1 GPU
+    torchrun --nproc-per-node N bench.py --gpus N ...              # N GPUs, positions sharded
+    python bench.py --impl reference                               # reference CPU renderer on host cores
+
+Prints ONE JSON line (rank 0).
+"""
+from __future__ import annotations
+
+import argparse
+import ctypes as C
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+sys.path.insert(0, os.path.join(ROOT, "oracle"))
+
+MLP_FLOP_PER_ROW_MIN = None  # set from width in main()
+
+
+def mlp_flops_per_row(width, d_in):
+    """Algorithmic FLOPs per (Gaussian, position) row. Minimal (factored encoding
+    terms): 7 hidden->hidden products + 5 head outputs; literal:
+    the reference's unfactored layer shapes."""
+    minimal = 2 * (7 * width * width + 5 * width)
+    literal = 2 * (width * d_in + 4 * width * width + 3 * width * (width + d_in) + 5 * width)
+    return minimal, literal
+
+
+def load_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as fh:
+            return json.load(fh), "measured"
+    return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0, "sm_max_mhz": 1965.0}, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons during the timed region."""
+
+    def __init__(self, index=0):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.index}",
+                 "--query-gpu=clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+                 "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+                 "clocks_event_reasons.sw_power_cap", "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [x.strip() for x in ln.split(",")]
+            if len(parts) < 7:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx = float(parts[1])
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[3:7]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def cpu_reference_rate(scene, positions, threads=None):
+    """The reference library (oracle/_ref, built from the reference sources) on
+    this host's cores, position-parallel (one render_at per thread)."""
+    import oracle as O
+    kind = "reference"
+    try:
+        ref = O.Reference(scene=scene)
+    except FileNotFoundError:
+        return None
+    cores = threads or os.cpu_count()
+    ref.set_threads(cores)
+    ref.render_batch(positions[:1], mode=1, spectra=False)  # warm
+    t0 = time.perf_counter()
+    ref.render_batch(positions, mode=1, spectra=False)
+    dt = time.perf_counter() - t0
+    return {"value": len(positions) / dt, "unit": "spectra/s", "cores": cores, "kind": kind,
+            "sample": f"{len(positions)} positions of the same scene (N={scene.n}), render_at + pooled + AoA, "
+                      f"position-parallel OpenMP, {dt:.1f} s"}
+
+
+def run_reference_arm(args, scene, rank):
+    if rank != 0:
+        return None
+    cores = os.cpu_count()
+    rng_pos = __import__("paper_2506_12787_b200.scene", fromlist=["random_positions"]).random_positions
+    per_step = max(cores, 4)
+    pos = rng_pos(per_step, seed=99)
+    res = None
+    times = []
+    for i in range(args.warmup + args.steps):
+        r = cpu_reference_rate(scene, pos, cores)
+        if r is None:
+            return {"impl": "reference", "unavailable": "oracle/_ref/libwrfref.so not built"}
+        if i >= args.warmup:
+            times.append(per_step / r["value"])
+            res = r
+    total = sum(times)
+    value = per_step * args.steps / total
+    return {"metric": "spectra/sec", "value": value, "unit": "spectra/s", "n_gpus": args.gpus, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": 1e3 * total / args.steps, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "impl": "reference",
+            "config": config_dict(args, scene),
+            "cpu_baseline": {"value": value, "unit": "spectra/s", "cores": cores, "kind": "reference",
+                             "sample": f"{per_step} positions per step (bounded sample of the workload), "
+                                       f"position-parallel render_at"},
+            "e2e": {"value": value, "unit": "spectra/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+
+
+def config_dict(args, scene):
+    return {"workload": f"BASELINE config 2: batched render of {args.batch} TX positions per GPU, "
+                        f"{scene.n} Gaussians, 90x360 grid, spectra + RSSI",
+            "gaussians": scene.n, "positions_per_gpu": args.batch, "grid": [scene.H, scene.W],
+            "mlp_width": scene.width, "mlp_precision": args.precision, "parallelism": f"positions sharded x{args.gpus}",
+            "l2": "per-step working set (spectra 265 MB + bins ~1 GB) exceeds the 126 MB L2"}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="native", choices=["native", "reference"])
+    ap.add_argument("--n", type=int, default=50000)
+    ap.add_argument("--batch", type=int, default=1024)
+    ap.add_argument("--precision", default=os.environ.get("SWR_BENCH_PRECISION", "fp32"),
+                    choices=["fp32", "bf16x3", "bf16"])
+    ap.add_argument("--chunk", type=int, default=256)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    args.gpus = world if world > 1 else args.gpus
+
+    from paper_2506_12787_b200.scene import make_scene, random_positions
+    scene = make_scene(args.n, seed=0)
+
+    if args.impl == "reference":
+        out = run_reference_arm(args, scene, rank)
+        if out is not None:
+            print(json.dumps(out), flush=True)
+        return
+
+    import torch
+    torch.cuda.set_device(local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    from paper_2506_12787_b200 import swr
+
+    ck = swr.Checkpoint.from_scene(scene, device=local)
+    ck.set_option("mlp_precision", {"fp32": 0, "bf16x3": 1, "bf16": 2}[args.precision])
+    ck.set_option("chunk", args.chunk)
+    B = args.batch
+    H, W = scene.H, scene.W
+    pos_all = random_positions(B * world, seed=1)
+    pos = np.ascontiguousarray(pos_all[rank * B:(rank + 1) * B])
+    stream = torch.cuda.Stream()
+    sptr = stream.cuda_stream
+    d_pos = torch.from_numpy(pos).cuda()
+    d_spec = torch.empty((B, H, W, 2), dtype=torch.float32, device="cuda")
+    d_pooled = torch.empty(B, dtype=torch.float64, device="cuda")
+    d_rssi = torch.empty(B, dtype=torch.float64, device="cuda")
+    flags = swr.OUT_SPECTRA | swr.OUT_POOLED | swr.OUT_RSSI
+    gather = None
+    if world > 1 and rank == 0:
+        gather = [torch.empty_like(d_spec) for _ in range(world)]
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device="cuda")
+
+    def step(timed_events=None):
+        with torch.cuda.stream(stream):
+            swr.render_device(ck, d_pos.data_ptr(), B, flags, d_spec.data_ptr(), d_pooled.data_ptr(),
+                              d_rssi.data_ptr(), 0, 0, sptr)
+            if world > 1:
+                dist.gather(d_spec, gather_list=gather, dst=0)
+                dist.gather(d_rssi, gather_list=[torch.empty_like(d_rssi) for _ in range(world)] if rank == 0 else None,
+                            dst=0)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+
+    # ---------------- device-timed region: K steps, L2 flushed between steps (untimed)
+    l0 = ck.launch_count()
+    ms = []
+    with ClockSampler(local) as clk:
+        if dist:
+            dist.barrier()
+        torch.cuda.synchronize()
+        for _ in range(args.steps):
+            with torch.cuda.stream(stream):
+                flush.fill_(1.0)
+                e0 = torch.cuda.Event(enable_timing=True)
+                e1 = torch.cuda.Event(enable_timing=True)
+                e0.record(stream)
+            step()
+            with torch.cuda.stream(stream):
+                e1.record(stream)
+            e1.synchronize()
+            ms.append(e0.elapsed_time(e1))
+        torch.cuda.synchronize()
+        if dist:
+            dist.barrier()
+    launches = ck.launch_count() - l0
+    total_ms = float(sum(ms))
+    if dist:
+        t = torch.tensor([total_ms], device="cuda", dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        total_ms = float(t.item())
+    value = world * B * args.steps / (total_ms / 1e3)
+
+    # ---------------- stage split + dominant kernel timing (separate pass, events per stage)
+    ck.set_option("stage_timing", 1)
+    step()
+    torch.cuda.synchronize()
+    stages = ck.stage_times()
+    ck.set_option("stage_timing", 0)
+
+    # ---------------- end to end through the host C ABI (pinned host buffers)
+    h_pos = torch.from_numpy(pos).pin_memory()
+    h_spec = torch.empty((B, H, W, 2), dtype=torch.float32).pin_memory()
+    h_pooled = torch.empty(B, dtype=torch.float64).pin_memory()
+    h_rssi = torch.empty(B, dtype=torch.float64).pin_memory()
+    L = swr.lib()
+
+    def host_step():
+        swr._check(L.swr_render(ck.handle, h_pos.data_ptr(), B, flags, h_spec.data_ptr(), h_pooled.data_ptr(),
+                                h_rssi.data_ptr(), None, None))
+
+    host_step()
+    torch.cuda.synchronize()
+    if dist:
+        dist.barrier()
+    t0 = time.perf_counter()
+    for _ in range(max(1, args.steps)):
+        host_step()
+    e2e_s = time.perf_counter() - t0
+    if dist:
+        t = torch.tensor([e2e_s], device="cuda", dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_s = float(t.item())
+    e2e_value = world * B * max(1, args.steps) / e2e_s
+
+    if rank != 0:
+        if dist:
+            dist.destroy_process_group()
+        return
+
+    peaks, peak_src = load_peaks()
+    d_in = 2 * (2 * scene.bands_c + 1) + 3 * (2 * scene.bands_p + 1)
+    fmin, flit = mlp_flops_per_row(scene.width, d_in)
+    mlp_ms = stages[1]
+    rows = scene.n * B
+    if args.precision == "fp32":
+        peak = 148 * 128 * 2 * (peaks.get("sm_max_mhz", 1965.0) * 1e6) / 1e12
+        bound, peak_note = "fp32", "FP32 CUDA-core peak 148 SM x 128 FMA x 2 x 1965 MHz (derived, not measured)"
+    else:
+        peak = peaks["bf16_tflops"]
+        bound, peak_note = "tensor", f"bf16 dense {peak_src} burst"
+    achieved = fmin * rows / (mlp_ms / 1e3) / 1e12 if mlp_ms > 0 else None
+    traffic = None
+    prof = os.path.join(ROOT, "profiles", "ncu_mlp_traffic.json")
+    if os.path.exists(prof):
+        try:
+            traffic = json.load(open(prof)).get(args.precision)
+        except Exception:
+            traffic = None
+
+    cpu = None
+    if not args.no_cpu_baseline:
+        cores = os.cpu_count()
+        cpu = cpu_reference_rate(scene, random_positions(max(cores, 4), seed=99), cores)
+
+    out = {
+        "metric": "spectra/sec", "value": value, "unit": "spectra/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f32" if args.precision == "fp32" else f"f32 ({args.precision} MLP)",
+        "data": "synthetic (seeded scene + TX positions)",
+        "config": config_dict(args, scene),
+        "roofline": {"bound": bound, "kernel": "deform MLP", "achieved": achieved, "peak": peak,
+                     "unit": "TFLOP/s", "frac": (achieved / peak) if achieved else None, "traffic": traffic,
+                     "peak_source": peak_note,
+                     "flop_per_row": fmin, "flop_per_row_literal": flit, "rows_per_launch": rows},
+        "stage_ms": {k: round(float(v), 3) for k, v in zip(["pos_prep", "mlp", "setup", "bin", "raster", "heads"], stages)},
+        "cpu_baseline": cpu,
+        "e2e": {"value": e2e_value, "unit": "spectra/s", "h2d_bytes_per_step": int(pos.nbytes),
+                "d2h_bytes_per_step": int(B * H * W * 2 * 4 + 2 * B * 8)},
+        "gpu_launches": int(launches),
+        "clocks": clk.summary(),
+    }
+    print(json.dumps(out), flush=True)
+    if dist:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,140 @@
+/* swr.h — C ABI of the B200-native SwiftWRF spectrum renderer (libswr.so).
+ *
+ * This is the drop-in boundary for the reference's render path. The reference
+ * (/root/reference/proj) is a statically linked C++ library with no FFI; each
+ * entry point below replaces the C++ call named beside it, batched over TX
+ * positions. Plain C types only (no torch, no C++); every call returns a
+ * swr_status and keeps a per-thread message for swr_last_error(). The C++
+ * wrapper include/swr.hpp rethrows them with the reference's exception types
+ * (std::invalid_argument / std::runtime_error).
+ *
+ * Threading: one context per host thread, or external serialisation. A
+ * context owns its device memory; host buffers are owned by the caller.
+ * Layouts follow the reference: positions [B][3] metres (x, y, z); spectra
+ * [B][H][W][2] interleaved (re, im), elevation the slow axis
+ * (spectrum.hpp:47-60); residuals planar per field (see swr_predict_residuals).
+ */
+#ifndef SWR_H
+#define SWR_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct swr_ctx swr_ctx;
+
+enum swr_status
+{
+    SWR_OK = 0,
+    SWR_EINVAL = 1,   /* std::invalid_argument in the reference (size / grid mismatch) */
+    SWR_ERUNTIME = 2, /* std::runtime_error (I/O, magic, version) */
+    SWR_ECUDA = 3,    /* device error (no sm_100 device, launch failure, OOM) */
+};
+
+/* render flags (swr_render / swr_render_device) */
+#define SWR_OUT_SPECTRA 1u /* write spectra [B][H][W][2] */
+#define SWR_OUT_POOLED 2u  /* pooled magnitude per position (tasks.cpp:32-39) */
+#define SWR_OUT_RSSI 4u    /* slope * pooled + intercept (tasks.cpp:109) */
+#define SWR_OUT_AOA 8u     /* argmax cell (row, col) + cell-centre angles (tasks.cpp:154-169) */
+#define SWR_NO_RESIDUALS 16u /* canonical render: skip the deformation net (rasterize(set, nullptr)) */
+
+/* MLP arithmetic (swr_set_option "mlp_precision") */
+#define SWR_MLP_FP32 0   /* FP32 FMA on the CUDA cores */
+#define SWR_MLP_BF16X3 1 /* tcgen05 split-precision (hi/lo bf16, 3 products, fp32 accumulate) */
+#define SWR_MLP_BF16 2   /* tcgen05 single bf16 product (fast, ~1e-3 relative residual error) */
+
+typedef struct
+{
+    int n_elevation, n_azimuth; /* grid (spectrum.hpp:30-42) */
+    int n;                      /* Gaussians */
+    int width, bands_center, bands_position;
+    float cutoff_radius;        /* RasterParams (splat.hpp:107-116) */
+    int tile;
+    double bbox_min[3], bbox_max[3];
+    int64_t pairs_last;         /* tile/primitive pairs binned by the last render chunk */
+} swr_scene_info;
+
+/* Scene + weights load. Replaces train::load_checkpoint (training.hpp:133,
+ * checkpoint.cpp:100-146). device < 0 selects the current CUDA device. */
+int swr_scene_create_wrfc(const char *path, int device, swr_ctx **out);
+
+/* Same from raw arrays in the reference layouts (GaussianSetT, splat.hpp:43-56;
+ * DeformNetT layers in WRFD order: 8 trunk, head centre/response/atten,
+ * row-major [rows x cols], deform.hpp:57-83). layer_w/layer_b may be NULL for
+ * a rasterize-only scene. */
+int swr_scene_create(int n_elevation, int n_azimuth, int n, const float *center_raw,
+                     const float *cholesky, const float *atten_logit, const float *response,
+                     int width, int bands_center, int bands_position, const float *const *layer_w,
+                     const float *const *layer_b, float cutoff_radius, int tile,
+                     const double *bbox_min, const double *bbox_max, int device, swr_ctx **out);
+
+void swr_scene_destroy(swr_ctx *ctx);
+int swr_scene_get_info(swr_ctx *ctx, swr_scene_info *info);
+
+/* Options: "mlp_precision" (SWR_MLP_*), "chunk" (positions per device chunk),
+ * "rssi_slope" / "rssi_intercept" (affine RSSI calibration, tasks.cpp:60-94). */
+int swr_set_option(swr_ctx *ctx, const char *key, double value);
+
+/* Batched render_at (training.cpp:189-195) + heads, host buffers, synchronous.
+ * pos_m: [B][3] metres. Any output may be NULL when its flag is off.
+ * aoa_rc: [B][2] (row, col); aoa_ang: [B][2] (elevation, azimuth) radians. */
+int swr_render(swr_ctx *ctx, const float *pos_m, int64_t B, uint32_t flags, float *spectra,
+               double *pooled, double *rssi_dbm, int32_t *aoa_rc, double *aoa_ang);
+
+/* Same with device pointers, stream-ordered on `stream` (a cudaStream_t;
+ * NULL = the context's stream). No host synchronisation except one 8-byte
+ * read of the pair count per chunk. */
+int swr_render_device(swr_ctx *ctx, const float *d_pos_m, int64_t B, uint32_t flags,
+                      float *d_spectra, double *d_pooled, double *d_rssi, int32_t *d_aoa_rc,
+                      double *d_aoa_ang, void *stream);
+
+/* ---- per-stage parity hooks (host buffers, synchronous) ---------------- */
+
+/* normalize_position (training.cpp:178-187): pos01 [B][3] */
+int swr_normalize_positions(swr_ctx *ctx, const float *pos_m, int64_t B, float *pos01);
+
+/* deform::predict_residuals (deform.cpp:140-207) for B normalized positions.
+ * Outputs in the reference ResidualsT layouts, one block per position:
+ * d_center [B][n][2], d_response [B][n][2], d_atten [B][n]. */
+int swr_predict_residuals(swr_ctx *ctx, const float *pos01, int64_t B, float *d_center,
+                          float *d_response, float *d_atten);
+
+/* prepare() per-primitive setup (splat.cpp:159-249) with caller residuals
+ * (NULL = zero residuals, i.e. rasterize(set, nullptr)). state [B][n][11] in
+ * the order of splat.cpp:133-147; rows/cols [B][n][2]; tile_count [B][n]. */
+int swr_setup(swr_ctx *ctx, const float *d_center, const float *d_response, const float *d_atten,
+              int64_t B, float *state, int32_t *rows, int32_t *cols, int32_t *tile_count);
+
+/* CSR tile bins (splat.cpp:251-292) per position: tile_offset [B][tiles+1]
+ * (relative to the position's first pair), tile_prims concatenated over
+ * positions (capacity cap entries), total in *n_pairs. */
+int swr_bin(swr_ctx *ctx, const float *d_center, const float *d_response, const float *d_atten,
+            int64_t B, int32_t *tile_offset, int32_t *tile_prims, int64_t cap, int64_t *n_pairs);
+
+/* splat::rasterize (splat.cpp:312-482) with caller residuals (NULL = none):
+ * spectra [B][H][W][2]. */
+int swr_rasterize(swr_ctx *ctx, const float *d_center, const float *d_response,
+                  const float *d_atten, int64_t B, float *spectra);
+
+/* Heads on caller spectra [B][H][W][2] (tasks.cpp:32-39, 154-169). */
+int swr_heads(swr_ctx *ctx, const float *spectra, int64_t B, double *pooled, int32_t *aoa_rc,
+              double *aoa_ang);
+
+/* Kernel launches issued by this context since creation (for the bench). */
+int64_t swr_launch_count(swr_ctx *ctx);
+
+/* Device time (ms) of the last render's stages, accumulated per chunk:
+ * [0] position prep, [1] MLP, [2] setup, [3] bin (scan+emit+sort), [4] raster, [5] heads.
+ * Only filled when option "stage_timing" is 1. */
+int swr_stage_times(swr_ctx *ctx, double *ms6);
+
+const char *swr_last_error(void);
+int swr_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

@@ -1,0 +1,88 @@
+"""Build libswr.so in-tree (nvcc, sm_100a only).
+
+    python -m paper_2506_12787_b200.build          # or __graft_entry__.build()
+
+Every .cu/.cpp under csrc/ is compiled with
+`-gencode arch=compute_100a,code=sm_100a -lineinfo -O3` (host code with
+-ffp-contract=off) and linked into paper_2506_12787_b200/libswr.so, which is
+what the Python host (swr.py), the C++ wrapper (include/swr.hpp) and the
+bench load. Objects go to paper_2506_12787_b200/_build/.
+"""
+from __future__ import annotations
+
+import concurrent.futures as cf
+import glob
+import hashlib
+import os
+import subprocess
+import sys
+
+PKG = os.path.dirname(os.path.abspath(__file__))
+ROOT = os.path.dirname(PKG)
+CSRC = os.path.join(PKG, "csrc")
+OUT = os.path.join(PKG, "libswr.so")
+BUILD = os.path.join(PKG, "_build")
+NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
+JSON_INC = os.environ.get(
+    "SWR_JSON_INC",
+    "/opt/prime-rl/.venv/lib/python3.12/site-packages/include/cudnn_frontend/thirdparty/nlohmann")
+ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
+HOST_CXX = "/usr/bin/g++"
+
+
+def _flags():
+    return ARCH + ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-ffp-contract=off,-O3",
+                   "-ccbin", HOST_CXX, "-I", os.path.join(ROOT, "include"), "-I", CSRC, "-I", JSON_INC,
+                   "-Xptxas", "-v" if os.environ.get("SWR_PTXAS_V") else "-O3"]
+
+
+def _sources():
+    return sorted(glob.glob(os.path.join(CSRC, "*.cu")) + glob.glob(os.path.join(CSRC, "*.cpp")))
+
+
+def _digest(path: str, flags) -> str:
+    h = hashlib.sha1(" ".join(flags).encode())
+    for f in [path] + sorted(glob.glob(os.path.join(CSRC, "*.h")) + glob.glob(os.path.join(ROOT, "include", "*.h"))):
+        with open(f, "rb") as fh:
+            h.update(fh.read())
+    return h.hexdigest()[:16]
+
+
+def _compile(src: str, flags) -> str:
+    obj = os.path.join(BUILD, os.path.basename(src) + ".o")
+    stamp = obj + ".sha"
+    dig = _digest(src, flags)
+    if os.path.exists(obj) and os.path.exists(stamp) and open(stamp).read() == dig:
+        return obj
+    cmd = [NVCC] + flags + ["-c", src, "-o", obj]
+    if src.endswith(".cpp"):
+        cmd = [NVCC, "-x", "cu"] + flags + ["-c", src, "-o", obj]
+    r = subprocess.run(cmd, capture_output=True, text=True)
+    if r.returncode != 0:
+        raise RuntimeError(f"nvcc failed for {src}:\n{r.stdout}\n{r.stderr}")
+    if os.environ.get("SWR_PTXAS_V"):
+        sys.stderr.write(r.stderr)
+    with open(stamp, "w") as fh:
+        fh.write(dig)
+    return obj
+
+
+def build(verbose: bool = False) -> str:
+    os.makedirs(BUILD, exist_ok=True)
+    flags = _flags()
+    srcs = _sources()
+    with cf.ThreadPoolExecutor(max_workers=min(8, len(srcs))) as ex:
+        objs = list(ex.map(lambda s: _compile(s, flags), srcs))
+    newest = max(os.path.getmtime(o) for o in objs)
+    if not os.path.exists(OUT) or os.path.getmtime(OUT) < newest:
+        cmd = [NVCC] + ARCH + ["-shared", "-cudart", "static", "-ccbin", HOST_CXX, "-o", OUT] + objs
+        r = subprocess.run(cmd, capture_output=True, text=True)
+        if r.returncode != 0:
+            raise RuntimeError(f"link failed:\n{r.stdout}\n{r.stderr}")
+    if verbose:
+        print(f"built {OUT}")
+    return OUT
+
+
+if __name__ == "__main__":
+    build(verbose=True)

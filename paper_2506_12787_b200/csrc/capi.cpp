@@ -1,0 +1,1037 @@
+// C ABI of libswr.so (include/swr.h): scene load, host-side per-scene
+// precompute, the chunked render pipeline and the per-stage parity hooks.
+//
+// Host precompute (once per scene) uses this host's glibc exactly as the
+// reference does, so every per-scene constant that reaches a bin is the
+// reference's bit pattern: materialised centres (tanhf, splat.cpp:60-65),
+// delta0 = 1/(1+expf(-a)) (splat.cpp:105-106), the centre encoding
+// (sinf/cosf, deform.cpp:54-70), Sigma^-1 entries (splat.cpp:200-211) and the
+// FP64 bbox half widths (splat.cpp:223-225). This TU is compiled with
+// -ffp-contract=off.
+#include "swr.h"
+#include "swr_internal.h"
+
+#include <json.hpp>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <fstream>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+namespace swr
+{
+
+struct cuda_error : std::runtime_error
+{
+    using std::runtime_error::runtime_error;
+};
+
+void check_cuda(cudaError_t e, const char *what)
+{
+    if (e != cudaSuccess)
+        throw cuda_error(std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+static thread_local std::string g_err;
+
+template <class F>
+static int guarded(F &&f)
+{
+    try
+    {
+        f();
+        return SWR_OK;
+    }
+    catch (const std::invalid_argument &e)
+    {
+        g_err = e.what();
+        return SWR_EINVAL;
+    }
+    catch (const cuda_error &e)
+    {
+        g_err = e.what();
+        return SWR_ECUDA;
+    }
+    catch (const std::runtime_error &e)
+    {
+        g_err = e.what();
+        return SWR_ERUNTIME;
+    }
+    catch (const std::exception &e)
+    {
+        g_err = e.what();
+        return SWR_ERUNTIME;
+    }
+}
+
+template <class T>
+static T *dalloc(Ctx &c, size_t count)
+{
+    void *p = nullptr;
+    check_cuda(cudaMalloc(&p, std::max<size_t>(count, 1) * sizeof(T)), "cudaMalloc");
+    c.allocs.push_back(p);
+    return static_cast<T *>(p);
+}
+
+static void dfree(Ctx &c, void *p)
+{
+    if (!p)
+        return;
+    cudaFree(p);
+    c.allocs.erase(std::remove(c.allocs.begin(), c.allocs.end(), p), c.allocs.end());
+}
+
+template <class T>
+static T *upload(Ctx &c, const std::vector<T> &v)
+{
+    T *d = dalloc<T>(c, v.size());
+    check_cuda(cudaMemcpy(d, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice), "upload");
+    return d;
+}
+
+struct HostScene
+{
+    int H, W, n;
+    std::vector<float> center_raw, cholesky, atten, response;
+    int width = 0, bands_c = 10, bands_p = 6;
+    std::vector<std::vector<float>> lw, lb; // 11 layers or empty
+    float cutoff = 3.0f;
+    int tile = 16;
+    double bmin[3] = {0, 0, 0}, bmax[3] = {1, 1, 1};
+};
+
+// ------------------------------------------------------------- scene build
+
+static void build_scene(Ctx &c, const HostScene &hs, int device)
+{
+    if (hs.H < 1 || hs.W < 1)
+        throw std::invalid_argument("gaussian set has an empty grid");
+    if (hs.n < 0)
+        throw std::invalid_argument("negative primitive count");
+    int ndev = 0;
+    check_cuda(cudaGetDeviceCount(&ndev), "cudaGetDeviceCount");
+    if (device < 0)
+        check_cuda(cudaGetDevice(&device), "cudaGetDevice");
+    if (device >= ndev)
+        throw cuda_error("no such CUDA device");
+    cudaDeviceProp prop;
+    check_cuda(cudaGetDeviceProperties(&prop, device), "cudaGetDeviceProperties");
+    if (prop.major != 10)
+        throw cuda_error("libswr requires an sm_100 (B200) device; found sm_" + std::to_string(prop.major) +
+                         std::to_string(prop.minor));
+    check_cuda(cudaSetDevice(device), "cudaSetDevice");
+    c.device = device;
+    check_cuda(cudaStreamCreateWithFlags(&c.stream, cudaStreamNonBlocking), "cudaStreamCreate");
+
+    const int tile = hs.tile < 1 ? 16 : hs.tile; // splat.cpp:166
+    if (tile > 32)
+        throw std::invalid_argument("tile edge above 32 cells is not supported by the device rasteriser");
+    Grid &g = c.g;
+    g.H = hs.H;
+    g.W = hs.W;
+    g.n = hs.n;
+    g.np = std::max(16, (hs.n + 15) / 16 * 16);
+    g.tile = tile;
+    g.th = (hs.H + tile - 1) / tile;
+    g.tw = (hs.W + tile - 1) / tile;
+    g.tiles = g.th * g.tw;
+    if (g.tiles > 1024)
+        throw std::invalid_argument("more than 1024 tiles per spectrum is not supported");
+    g.cut = hs.cutoff > 0.0f;
+    g.radius = g.cut ? hs.cutoff : 0.0f;
+    g.cut2 = g.cut ? hs.cutoff * hs.cutoff : INFINITY;
+    g.cell_el = (kPi / 2.0) / hs.H; // spectrum.cpp:29-32
+    g.cell_az = (2.0 * kPi) / hs.W;
+    c.cutoff = hs.cutoff;
+    c.tile = hs.tile;
+    std::memcpy(c.bbox_min, hs.bmin, sizeof(hs.bmin));
+    std::memcpy(c.bbox_max, hs.bmax, sizeof(hs.bmax));
+
+    const int n = hs.n, np = g.np;
+    std::vector<float> el0(np, 0.f), az0(np, 0.f), d0(np, 0.f), re0(np, 0.f), im0(np, 0.f), il3(np, 0.f),
+        l2v(np, 0.f);
+    std::vector<float4> shape(np, make_float4(0, 0, 0, 0));
+    std::vector<double2> half(np, make_double2(0, 0));
+    for (int p = 0; p < n; p++)
+    {
+        const float rel = hs.center_raw[2 * size_t(p)], raz = hs.center_raw[2 * size_t(p) + 1];
+        el0[p] = float(kPi / 4) * (std::tanh(rel) + 1.0f); // float overloads: glibc tanhf
+        az0[p] = float(kPi) * (std::tanh(raz) + 1.0f);
+        const float a = hs.atten[p];
+        d0[p] = 1.0f / (1.0f + std::exp(-a));
+        re0[p] = hs.response[2 * size_t(p)];
+        im0[p] = hs.response[2 * size_t(p) + 1];
+        const float c1 = hs.cholesky[3 * size_t(p)], l2 = hs.cholesky[3 * size_t(p) + 1],
+                    c3 = hs.cholesky[3 * size_t(p) + 2];
+        const float l1 = c1 < 1e-4f ? 1e-4f : c1; // std::max(l, chol_floor)
+        const float l3 = c3 < 1e-4f ? 1e-4f : c3;
+        const float det = l1 * l1 * l3 * l3;
+        shape[p] = make_float4((l2 * l2 + l3 * l3) / det, -l2 / (l1 * l3 * l3), 1.0f / (l3 * l3), 1.0f / l1);
+        il3[p] = 1.0f / l3;
+        l2v[p] = l2;
+        half[p] = make_double2(double(g.radius) * double(l1),
+                               double(g.radius) * std::sqrt(double(l2) * l2 + double(l3) * l3));
+    }
+    std::vector<float> elc(hs.H), azc(hs.W);
+    for (int r = 0; r < hs.H; r++)
+        elc[r] = float((r + 0.5) * g.cell_el);
+    for (int j = 0; j < hs.W; j++)
+        azc[j] = float((j + 0.5) * g.cell_az);
+    SceneDev &s = c.s;
+    s.el0 = upload(c, el0);
+    s.az0 = upload(c, az0);
+    s.delta0 = upload(c, d0);
+    s.re0 = upload(c, re0);
+    s.im0 = upload(c, im0);
+    s.shape = upload(c, shape);
+    s.inv_l3 = upload(c, il3);
+    s.l2 = upload(c, l2v);
+    s.half = upload(c, half);
+    s.el_c = upload(c, elc);
+    s.az_c = upload(c, azc);
+
+    // --------------------------------------------------------------- network
+    c.has_net = !hs.lw.empty();
+    if (!c.has_net)
+        return;
+    NetDev &nt = c.net;
+    nt.width = hs.width;
+    if (hs.width < 1 || hs.width > 512)
+        throw std::invalid_argument("deform-net width must be in [1, 512]");
+    nt.wp = hs.width <= 160 ? 160 : 512;
+    nt.bands_c = hs.bands_c;
+    nt.bands_p = hs.bands_p;
+    nt.dc = 2 * (2 * hs.bands_c + 1);
+    nt.dp = 3 * (2 * hs.bands_p + 1);
+    nt.d = nt.dc + nt.dp;
+    if (nt.dp > 64 || hs.bands_p > 20 || hs.bands_c > 40)
+        throw std::invalid_argument("encoding bands out of the supported range");
+    const int Wd = hs.width, WP = nt.wp, D = nt.d, Dc = nt.dc, Dp = nt.dp;
+    // shape checks against deform.cpp:72-102
+    for (int i = 0; i < 8; i++)
+    {
+        const size_t cols = i == 0 ? D : ((i == 2 || i == 4 || i == 6) ? Wd + D : Wd);
+        if (hs.lw[i].size() != size_t(Wd) * cols || hs.lb[i].size() != size_t(Wd))
+            throw std::invalid_argument("deform layer shape does not match width/encoding");
+    }
+    const int hr[3] = {2, 2, 1};
+    for (int i = 0; i < 3; i++)
+        if (hs.lw[8 + i].size() != size_t(hr[i]) * Wd || hs.lb[8 + i].size() != size_t(hr[i]))
+            throw std::invalid_argument("deform head shape does not match width");
+
+    std::vector<float> whT(size_t(7) * WP * WP, 0.f), bias(size_t(8) * WP, 0.f), wpos(size_t(4) * WP * Dp, 0.f),
+        wcen(size_t(4) * WP * Dc, 0.f), heads(size_t(5) * WP, 0.f), hbias(5, 0.f);
+    for (int l = 0; l < 8; l++)
+    {
+        const size_t cols = l == 0 ? D : ((l == 2 || l == 4 || l == 6) ? Wd + D : Wd);
+        const float *Wl = hs.lw[l].data();
+        for (int r = 0; r < Wd; r++)
+            bias[size_t(l) * WP + r] = hs.lb[l][r];
+        if (l >= 1)
+            for (int r = 0; r < Wd; r++)
+                for (int k = 0; k < Wd; k++)
+                    whT[(size_t(l - 1) * WP + k) * WP + r] = Wl[r * cols + k];
+        if (l % 2 == 0)
+        {
+            const int j = l / 2;
+            const size_t off = l == 0 ? 0 : Wd; // encoding columns follow the hidden block
+            for (int r = 0; r < Wd; r++)
+            {
+                for (int k = 0; k < Dc; k++)
+                    wcen[(size_t(j) * WP + r) * Dc + k] = Wl[r * cols + off + k];
+                for (int k = 0; k < Dp; k++)
+                    wpos[(size_t(j) * WP + r) * Dp + k] = Wl[r * cols + off + Dc + k];
+            }
+        }
+    }
+    int h = 0;
+    for (int i = 0; i < 3; i++)
+        for (int r = 0; r < hr[i]; r++, h++)
+        {
+            for (int k = 0; k < Wd; k++)
+                heads[size_t(h) * WP + k] = hs.lw[8 + i][size_t(r) * Wd + k];
+            hbias[h] = hs.lb[8 + i][r];
+        }
+    nt.whT = upload(c, whT);
+    nt.bias = upload(c, bias);
+    nt.wpos = upload(c, wpos);
+    nt.wcen = upload(c, wcen);
+    nt.heads = upload(c, heads);
+    nt.hbias = upload(c, hbias);
+    nt.cg = dalloc<float>(c, size_t(np) * 4 * WP);
+
+    // centre encoding per Gaussian (host glibc sinf/cosf, deform.cpp:54-70)
+    std::vector<float> cenc(size_t(np) * Dc, 0.f);
+    for (int p = 0; p < n; p++)
+    {
+        float *row = cenc.data() + size_t(p) * Dc;
+        const float v[2] = {el0[p], az0[p]};
+        row[0] = v[0];
+        row[1] = v[1];
+        float *blk = row + 2;
+        for (int k = 0; k < hs.bands_c; k++)
+        {
+            const float f = float(std::ldexp(kPi, k));
+            blk[0] = std::sin(f * v[0]);
+            blk[1] = std::sin(f * v[1]);
+            blk[2] = std::cos(f * v[0]);
+            blk[3] = std::cos(f * v[1]);
+            blk += 4;
+        }
+    }
+    float *d_cenc = upload(c, cenc);
+    launch_center_terms(c, d_cenc, c.stream);
+    check_cuda(cudaStreamSynchronize(c.stream), "centre terms");
+    dfree(c, d_cenc);
+    if (mlp_tc_available() && WP == 160)
+        prepare_tc_weights(c, whT);
+}
+
+// ------------------------------------------------------------- work buffers
+
+static void ensure_work(Ctx &c, int64_t nb)
+{
+    Work &w = c.w;
+    if (w.cap_b >= nb)
+        return;
+    for (void *p : {(void *)w.pos01, (void *)w.pterm, (void *)w.res, (void *)w.dyn, (void *)w.rng, (void *)w.cnt,
+                    (void *)w.seg, (void *)w.poff, (void *)w.tile_off, (void *)w.tile_part, (void *)w.tile_sum})
+        dfree(c, p);
+    const int np = c.g.np, tiles = c.g.tiles;
+    const int wp = c.has_net ? c.net.wp : 32;
+    w.cap_b = nb;
+    w.pos01 = dalloc<float>(c, size_t(nb) * 4);
+    w.pterm = dalloc<float>(c, size_t(nb) * 4 * wp);
+    w.res = dalloc<float>(c, size_t(5) * nb * np);
+    w.dyn = dalloc<float4>(c, size_t(nb) * np);
+    w.rng = dalloc<int4>(c, size_t(nb) * np);
+    w.cnt = dalloc<int>(c, size_t(nb) * np);
+    w.seg = dalloc<int64_t>(c, size_t(nb) + 1);
+    w.poff = dalloc<int>(c, size_t(nb) * np);
+    w.tile_off = dalloc<int>(c, size_t(nb) * (tiles + 1));
+    w.tile_part = dalloc<float4>(c, size_t(nb) * tiles);
+    w.tile_sum = dalloc<double>(c, size_t(nb) * tiles);
+    if (!w.stats)
+        w.stats = dalloc<int64_t>(c, 2);
+    if (!w.host_pairs)
+        check_cuda(cudaHostAlloc((void **)&w.host_pairs, 4 * sizeof(int64_t), cudaHostAllocDefault), "host alloc");
+    w.max_chunks = 0; // chunk histogram re-sized on demand
+    dfree(c, w.chunk_hist);
+    w.chunk_hist = nullptr;
+}
+
+static void ensure_pairs(Ctx &c, int64_t pairs, int nb, int64_t max_seg)
+{
+    Work &w = c.w;
+    if (pairs > w.cap_pairs)
+    {
+        dfree(c, w.keys);
+        dfree(c, w.vals);
+        dfree(c, w.sorted);
+        const int64_t cap = std::max<int64_t>(pairs + pairs / 8, 1024);
+        w.keys = dalloc<uint16_t>(c, cap);
+        w.vals = dalloc<int>(c, cap);
+        w.sorted = dalloc<int>(c, cap);
+        w.cap_pairs = cap;
+    }
+    const int need = int(std::max<int64_t>(1, (max_seg + kSort - 1) / kSort));
+    if (need > w.max_chunks || !w.chunk_hist)
+    {
+        dfree(c, w.chunk_hist);
+        w.max_chunks = std::max(need + need / 4, 1);
+        w.chunk_hist = dalloc<int>(c, size_t(w.cap_b) * w.max_chunks * c.g.tiles);
+    }
+    (void)nb;
+}
+
+// --------------------------------------------------------------- pipeline
+
+struct Timer
+{
+    Ctx &c;
+    cudaStream_t st;
+    cudaEvent_t ev[7];
+    int k = 0;
+    bool on;
+    Timer(Ctx &cx, cudaStream_t s) : c(cx), st(s), on(cx.stage_timing)
+    {
+        if (on)
+            for (auto &e : ev)
+                cudaEventCreate(&e);
+    }
+    void mark()
+    {
+        if (on)
+            cudaEventRecord(ev[k++], st);
+    }
+    void finish(const int *stage_of_interval)
+    {
+        if (!on)
+            return;
+        cudaEventSynchronize(ev[k - 1]);
+        for (int i = 0; i + 1 < k; i++)
+        {
+            float ms = 0;
+            cudaEventElapsedTime(&ms, ev[i], ev[i + 1]);
+            c.stage_ms[stage_of_interval[i]] += ms;
+        }
+        for (auto &e : ev)
+            cudaEventDestroy(e);
+    }
+};
+
+// Render one chunk of nb positions whose (device) coordinates are d_pos.
+// Residuals come from the MLP (use_mlp), the caller (already in w.res) or are
+// zero. d_spec may be null (heads only).
+static void run_chunk(Ctx &c, const float *d_pos, int nb, bool normalized, bool use_mlp, bool with_res,
+                      float *d_spec, bool heads, uint32_t flags, double *d_pooled, double *d_rssi, int32_t *d_aoa_rc,
+                      double *d_aoa_ang, cudaStream_t st)
+{
+    Timer tm(c, st);
+    static const int stage_map[6] = {0, 1, 2, 3, 4, 5};
+    tm.mark();
+    if (use_mlp)
+    {
+        launch_pos_prep(c, d_pos, nb, normalized, st);
+        tm.mark();
+        launch_mlp(c, nb, st);
+        tm.mark();
+    }
+    else
+    {
+        tm.mark();
+        tm.mark();
+    }
+    launch_setup(c, nb, use_mlp || with_res, st);
+    tm.mark();
+    launch_bin_count(c, nb, st);
+    check_cuda(cudaMemcpyAsync(c.w.host_pairs, c.w.stats, 2 * sizeof(int64_t), cudaMemcpyDeviceToHost, st),
+               "D2H pair count");
+    check_cuda(cudaStreamSynchronize(st), "pair count");
+    const int64_t pairs = c.w.host_pairs[0], max_seg = c.w.host_pairs[1];
+    c.pairs_last = pairs;
+    ensure_pairs(c, pairs, nb, max_seg);
+    launch_bin_sort(c, nb, pairs, int(max_seg), st);
+    tm.mark();
+    launch_raster(c, nb, d_spec, heads, st);
+    tm.mark();
+    if (heads)
+        launch_heads(c, nb, flags, d_pooled, d_rssi, d_aoa_rc, d_aoa_ang, st);
+    tm.mark();
+    check_cuda(cudaGetLastError(), "kernel launch");
+    tm.finish(stage_map);
+}
+
+static bool is_pinned(const void *p)
+{
+    cudaPointerAttributes a;
+    if (cudaPointerGetAttributes(&a, p) != cudaSuccess)
+    {
+        cudaGetLastError();
+        return false;
+    }
+    return a.type == cudaMemoryTypeHost || a.type == cudaMemoryTypeManaged;
+}
+
+static void device_render(Ctx &c, const float *d_pos, int64_t B, uint32_t flags, float *d_spec, double *d_pooled,
+                          double *d_rssi, int32_t *d_aoa_rc, double *d_aoa_ang, cudaStream_t st)
+{
+    const bool use_mlp = c.has_net && !(flags & SWR_NO_RESIDUALS);
+    const bool heads = flags & (SWR_OUT_POOLED | SWR_OUT_RSSI | SWR_OUT_AOA);
+    const int64_t chunk = std::max<int64_t>(1, std::min<int64_t>(B, c.chunk));
+    ensure_work(c, chunk);
+    if (c.stage_timing)
+        std::fill(c.stage_ms, c.stage_ms + 6, 0.0);
+    const size_t per = size_t(2) * c.g.H * c.g.W;
+    for (int64_t b0 = 0; b0 < B; b0 += chunk)
+    {
+        const int nb = int(std::min<int64_t>(chunk, B - b0));
+        run_chunk(c, d_pos + 3 * b0, nb, false, use_mlp, false,
+                  (flags & SWR_OUT_SPECTRA) && d_spec ? d_spec + per * b0 : nullptr, heads, flags,
+                  (flags & SWR_OUT_POOLED) && d_pooled ? d_pooled + b0 : nullptr,
+                  (flags & SWR_OUT_RSSI) && d_rssi ? d_rssi + b0 : nullptr,
+                  (flags & SWR_OUT_AOA) && d_aoa_rc ? d_aoa_rc + 2 * b0 : nullptr,
+                  (flags & SWR_OUT_AOA) && d_aoa_ang ? d_aoa_ang + 2 * b0 : nullptr, st);
+    }
+}
+
+static void upload_residuals(Ctx &c, const float *dc, const float *dr, const float *da, int64_t b0, int nb)
+{
+    // reference layouts [B][n][2], [B][n][2], [B][n] -> planes [5][cap_b][np]
+    const int n = c.g.n, np = c.g.np;
+    std::vector<float> planes(size_t(5) * c.w.cap_b * np, 0.f);
+    const size_t plane = size_t(c.w.cap_b) * np;
+    for (int s = 0; s < nb; s++)
+        for (int g = 0; g < n; g++)
+        {
+            const size_t src = (size_t(b0 + s) * n + g);
+            const size_t dst = size_t(s) * np + g;
+            planes[0 * plane + dst] = dc[2 * src];
+            planes[1 * plane + dst] = dc[2 * src + 1];
+            planes[2 * plane + dst] = dr[2 * src];
+            planes[3 * plane + dst] = dr[2 * src + 1];
+            planes[4 * plane + dst] = da[src];
+        }
+    check_cuda(cudaMemcpy(c.w.res, planes.data(), planes.size() * sizeof(float), cudaMemcpyHostToDevice),
+               "upload residuals");
+}
+
+static HostScene parse_wrfc(const char *path)
+{
+    std::ifstream is(path, std::ios::binary);
+    if (!is)
+        throw std::runtime_error(std::string("cannot open ") + path);
+    std::vector<char> buf((std::istreambuf_iterator<char>(is)), std::istreambuf_iterator<char>());
+    size_t at = 0;
+    auto need = [&](size_t k) {
+        if (at + k > buf.size())
+            throw std::runtime_error("unexpected end of file");
+    };
+    auto u32 = [&]() {
+        need(4);
+        uint32_t v;
+        std::memcpy(&v, buf.data() + at, 4);
+        at += 4;
+        return v;
+    };
+    auto u64 = [&]() {
+        need(8);
+        uint64_t v;
+        std::memcpy(&v, buf.data() + at, 8);
+        at += 8;
+        return v;
+    };
+    auto magic = [&](const char *m, const char *what) {
+        need(4);
+        if (std::memcmp(buf.data() + at, m, 4) != 0)
+            throw std::runtime_error(std::string("bad magic, not a ") + what);
+        at += 4;
+    };
+    auto f32s = [&](std::vector<float> &v, size_t cnt) {
+        need(4 * cnt);
+        v.resize(cnt);
+        std::memcpy(v.data(), buf.data() + at, 4 * cnt);
+        at += 4 * cnt;
+    };
+    // checkpoint.cpp:100-141
+    magic("WRFC", "checkpoint");
+    if (u32() != 1)
+        throw std::runtime_error("unsupported checkpoint version");
+    if (u32() != 3)
+        throw std::runtime_error("unexpected checkpoint section count");
+    u32();
+    uint64_t off[3], size[3];
+    for (int i = 0; i < 3; i++)
+    {
+        off[i] = u64();
+        size[i] = u64();
+    }
+    HostScene hs;
+    // splat.cpp:723-736
+    at = off[0];
+    magic("WRF2", "gaussian section");
+    if (u32() != 1)
+        throw std::runtime_error("unsupported gaussian section version");
+    const uint32_t n = u32();
+    u32();
+    hs.n = int(n);
+    f32s(hs.center_raw, size_t(n) * 2);
+    f32s(hs.cholesky, size_t(n) * 3);
+    f32s(hs.atten, n);
+    f32s(hs.response, size_t(n) * 2);
+    // deform.cpp:354-384
+    at = off[1];
+    magic("WRFD", "deform section");
+    if (u32() != 1)
+        throw std::runtime_error("unsupported deform section version");
+    if (u32() != 11)
+        throw std::runtime_error("unexpected deform layer count");
+    hs.width = int(u32());
+    hs.bands_c = int(u32());
+    hs.bands_p = int(u32());
+    std::vector<std::pair<uint32_t, uint32_t>> shp(11);
+    for (auto &s : shp)
+    {
+        s.first = u32();
+        s.second = u32();
+    }
+    hs.lw.resize(11);
+    hs.lb.resize(11);
+    for (int i = 0; i < 11; i++)
+    {
+        f32s(hs.lw[i], size_t(shp[i].first) * shp[i].second);
+        f32s(hs.lb[i], shp[i].first);
+    }
+    need(0);
+    if (off[2] + size[2] > buf.size())
+        throw std::runtime_error("unexpected end of file");
+    const auto j = nlohmann::json::parse(std::string(buf.data() + off[2], size[2]));
+    hs.H = j.at("grid").at("n_elevation").get<int>();
+    hs.W = j.at("grid").at("n_azimuth").get<int>();
+    const auto &cfg = j.at("config");
+    if (cfg.contains("cutoff_radius"))
+        hs.cutoff = cfg.at("cutoff_radius").get<float>();
+    if (cfg.contains("tile"))
+        hs.tile = cfg.at("tile").get<int>();
+    const auto bmin = j.at("bbox_min").get<std::vector<double>>();
+    const auto bmax = j.at("bbox_max").get<std::vector<double>>();
+    for (int a = 0; a < 3; a++)
+    {
+        hs.bmin[a] = bmin.at(a);
+        hs.bmax[a] = bmax.at(a);
+    }
+    return hs;
+}
+
+} // namespace swr
+
+using namespace swr;
+
+struct swr_ctx
+{
+    Ctx c;
+};
+
+static void destroy(swr_ctx *h)
+{
+    if (!h)
+        return;
+    cudaSetDevice(h->c.device);
+    for (void *p : h->c.allocs)
+        cudaFree(p);
+    if (h->c.w.host_pairs)
+        cudaFreeHost(h->c.w.host_pairs);
+    if (h->c.stream)
+        cudaStreamDestroy(h->c.stream);
+    delete h;
+}
+
+extern "C" {
+
+const char *swr_last_error(void) { return g_err.c_str(); }
+int swr_version(void) { return 100; }
+
+int swr_scene_create_wrfc(const char *path, int device, swr_ctx **out)
+{
+    *out = nullptr;
+    auto *h = new swr_ctx();
+    const int rc = guarded([&] {
+        const HostScene hs = parse_wrfc(path);
+        build_scene(h->c, hs, device);
+    });
+    if (rc)
+    {
+        destroy(h);
+        return rc;
+    }
+    *out = h;
+    return SWR_OK;
+}
+
+int swr_scene_create(int H, int W, int n, const float *center_raw, const float *cholesky, const float *atten_logit,
+                     const float *response, int width, int bands_c, int bands_p, const float *const *layer_w,
+                     const float *const *layer_b, float cutoff, int tile, const double *bmin, const double *bmax,
+                     int device, swr_ctx **out)
+{
+    *out = nullptr;
+    auto *h = new swr_ctx();
+    const int rc = guarded([&] {
+        HostScene hs;
+        hs.H = H;
+        hs.W = W;
+        hs.n = n;
+        hs.center_raw.assign(center_raw, center_raw + size_t(2) * n);
+        hs.cholesky.assign(cholesky, cholesky + size_t(3) * n);
+        hs.atten.assign(atten_logit, atten_logit + size_t(n));
+        hs.response.assign(response, response + size_t(2) * n);
+        hs.width = width;
+        hs.bands_c = bands_c;
+        hs.bands_p = bands_p;
+        hs.cutoff = cutoff;
+        hs.tile = tile;
+        for (int a = 0; a < 3; a++)
+        {
+            hs.bmin[a] = bmin ? bmin[a] : 0.0;
+            hs.bmax[a] = bmax ? bmax[a] : 1.0;
+        }
+        if (layer_w)
+        {
+            const int D = 2 * (2 * bands_c + 1) + 3 * (2 * bands_p + 1);
+            hs.lw.resize(11);
+            hs.lb.resize(11);
+            for (int i = 0; i < 11; i++)
+            {
+                const size_t rows = i < 8 ? width : (i == 10 ? 1 : 2);
+                const size_t cols = i == 0 ? D : (i < 8 ? ((i == 2 || i == 4 || i == 6) ? width + D : width) : width);
+                hs.lw[i].assign(layer_w[i], layer_w[i] + rows * cols);
+                hs.lb[i].assign(layer_b[i], layer_b[i] + rows);
+            }
+        }
+        build_scene(h->c, hs, device);
+    });
+    if (rc)
+    {
+        destroy(h);
+        return rc;
+    }
+    *out = h;
+    return SWR_OK;
+}
+
+void swr_scene_destroy(swr_ctx *ctx) { destroy(ctx); }
+
+int swr_scene_get_info(swr_ctx *ctx, swr_scene_info *info)
+{
+    const Ctx &c = ctx->c;
+    info->n_elevation = c.g.H;
+    info->n_azimuth = c.g.W;
+    info->n = c.g.n;
+    info->width = c.has_net ? c.net.width : 0;
+    info->bands_center = c.has_net ? c.net.bands_c : 0;
+    info->bands_position = c.has_net ? c.net.bands_p : 0;
+    info->cutoff_radius = c.cutoff;
+    info->tile = c.tile;
+    for (int a = 0; a < 3; a++)
+    {
+        info->bbox_min[a] = c.bbox_min[a];
+        info->bbox_max[a] = c.bbox_max[a];
+    }
+    info->pairs_last = c.pairs_last;
+    return SWR_OK;
+}
+
+int swr_set_option(swr_ctx *ctx, const char *key, double value)
+{
+    return guarded([&] {
+        Ctx &c = ctx->c;
+        const std::string k(key);
+        if (k == "mlp_precision")
+        {
+            const int v = int(value);
+            if (v < 0 || v > 2)
+                throw std::invalid_argument("mlp_precision must be 0 (fp32), 1 (bf16x3) or 2 (bf16)");
+            if (v != 0 && !(mlp_tc_available() && c.has_net && c.net.wp == 160))
+                throw std::invalid_argument("tensor-core MLP unavailable for this scene (width must be <= 160)");
+            c.mlp_precision = v;
+        }
+        else if (k == "chunk")
+        {
+            if (value < 1)
+                throw std::invalid_argument("chunk must be >= 1");
+            c.chunk = int(value);
+        }
+        else if (k == "rssi_slope")
+            c.rssi_slope = value;
+        else if (k == "rssi_intercept")
+            c.rssi_intercept = value;
+        else if (k == "stage_timing")
+            c.stage_timing = value != 0.0;
+        else
+            throw std::invalid_argument("unknown option " + k);
+    });
+}
+
+int swr_render_device(swr_ctx *ctx, const float *d_pos, int64_t B, uint32_t flags, float *d_spec, double *d_pooled,
+                      double *d_rssi, int32_t *d_aoa_rc, double *d_aoa_ang, void *stream)
+{
+    return guarded([&] {
+        Ctx &c = ctx->c;
+        if (B < 0)
+            throw std::invalid_argument("negative batch");
+        if (B == 0)
+            return;
+        check_cuda(cudaSetDevice(c.device), "cudaSetDevice");
+        cudaStream_t st = stream ? (cudaStream_t)stream : c.stream;
+        device_render(c, d_pos, B, flags, d_spec, d_pooled, d_rssi, d_aoa_rc, d_aoa_ang, st);
+    });
+}
+
+int swr_render(swr_ctx *ctx, const float *pos_m, int64_t B, uint32_t flags, float *spectra, double *pooled,
+               double *rssi, int32_t *aoa_rc, double *aoa_ang)
+{
+    return guarded([&] {
+        Ctx &c = ctx->c;
+        if (B < 0)
+            throw std::invalid_argument("negative batch");
+        if (B == 0)
+            return;
+        check_cuda(cudaSetDevice(c.device), "cudaSetDevice");
+        cudaStream_t st = c.stream;
+        const int64_t chunk = std::max<int64_t>(1, std::min<int64_t>(B, c.chunk));
+        ensure_work(c, chunk);
+        const size_t per = size_t(2) * c.g.H * c.g.W;
+        // device staging: positions (all), two spectrum chunk buffers, head outputs
+        float *d_pos = dalloc<float>(c, size_t(3) * B);
+        float *d_spec[2] = {nullptr, nullptr};
+        const bool want_spec = (flags & SWR_OUT_SPECTRA) && spectra;
+        if (want_spec)
+            for (auto &p : d_spec)
+                p = dalloc<float>(c, per * chunk);
+        double *d_pooled = dalloc<double>(c, B), *d_rssi = dalloc<double>(c, B), *d_ang = dalloc<double>(c, 2 * B);
+        int32_t *d_rc = dalloc<int32_t>(c, 2 * B);
+        cudaStream_t copy_st;
+        cudaEvent_t done[2], freed[2];
+        check_cuda(cudaStreamCreateWithFlags(&copy_st, cudaStreamNonBlocking), "copy stream");
+        for (int i = 0; i < 2; i++)
+        {
+            cudaEventCreateWithFlags(&done[i], cudaEventDisableTiming);
+            cudaEventCreateWithFlags(&freed[i], cudaEventDisableTiming);
+        }
+        check_cuda(cudaMemcpyAsync(d_pos, pos_m, sizeof(float) * 3 * B, cudaMemcpyHostToDevice, st), "H2D positions");
+        const bool use_mlp = c.has_net && !(flags & SWR_NO_RESIDUALS);
+        const bool heads = flags & (SWR_OUT_POOLED | SWR_OUT_RSSI | SWR_OUT_AOA);
+        if (c.stage_timing)
+            std::fill(c.stage_ms, c.stage_ms + 6, 0.0);
+        int k = 0;
+        for (int64_t b0 = 0; b0 < B; b0 += chunk, k ^= 1)
+        {
+            const int nb = int(std::min<int64_t>(chunk, B - b0));
+            if (want_spec && b0 >= 2 * chunk)
+                check_cuda(cudaStreamWaitEvent(st, freed[k], 0), "wait copy");
+            run_chunk(c, d_pos + 3 * b0, nb, false, use_mlp, false, want_spec ? d_spec[k] : nullptr, heads, flags,
+                      d_pooled + b0, d_rssi + b0, d_rc + 2 * b0, d_ang + 2 * b0, st);
+            if (want_spec)
+            {
+                check_cuda(cudaEventRecord(done[k], st), "record");
+                check_cuda(cudaStreamWaitEvent(copy_st, done[k], 0), "wait compute");
+                check_cuda(cudaMemcpyAsync(spectra + per * b0, d_spec[k], sizeof(float) * per * nb,
+                                           cudaMemcpyDeviceToHost, copy_st),
+                           "D2H spectra");
+                check_cuda(cudaEventRecord(freed[k], copy_st), "record");
+            }
+        }
+        if (pooled && (flags & SWR_OUT_POOLED))
+            check_cuda(cudaMemcpyAsync(pooled, d_pooled, sizeof(double) * B, cudaMemcpyDeviceToHost, st), "D2H");
+        if (rssi && (flags & SWR_OUT_RSSI))
+            check_cuda(cudaMemcpyAsync(rssi, d_rssi, sizeof(double) * B, cudaMemcpyDeviceToHost, st), "D2H");
+        if (aoa_rc && (flags & SWR_OUT_AOA))
+            check_cuda(cudaMemcpyAsync(aoa_rc, d_rc, sizeof(int32_t) * 2 * B, cudaMemcpyDeviceToHost, st), "D2H");
+        if (aoa_ang && (flags & SWR_OUT_AOA))
+            check_cuda(cudaMemcpyAsync(aoa_ang, d_ang, sizeof(double) * 2 * B, cudaMemcpyDeviceToHost, st), "D2H");
+        check_cuda(cudaStreamSynchronize(st), "render");
+        check_cuda(cudaStreamSynchronize(copy_st), "render copies");
+        for (int i = 0; i < 2; i++)
+        {
+            cudaEventDestroy(done[i]);
+            cudaEventDestroy(freed[i]);
+        }
+        cudaStreamDestroy(copy_st);
+        for (void *p : {(void *)d_pos, (void *)d_spec[0], (void *)d_spec[1], (void *)d_pooled, (void *)d_rssi,
+                        (void *)d_ang, (void *)d_rc})
+            dfree(c, p);
+        (void)is_pinned;
+    });
+}
+
+int swr_normalize_positions(swr_ctx *ctx, const float *pos_m, int64_t B, float *pos01)
+{
+    return guarded([&] {
+        Ctx &c = ctx->c;
+        for (int64_t b = 0; b < B; b++)
+            for (int a = 0; a < 3; a++)
+            {
+                const double range = c.bbox_max[a] - c.bbox_min[a];
+                pos01[3 * b + a] = range > 0.0 ? float((double(pos_m[3 * b + a]) - c.bbox_min[a]) / range) : 0.5f;
+            }
+    });
+}
+
+int swr_predict_residuals(swr_ctx *ctx, const float *pos01, int64_t B, float *dc, float *dr, float *da)
+{
+    return guarded([&] {
+        Ctx &c = ctx->c;
+        if (!c.has_net)
+            throw std::invalid_argument("deform net is not initialized");
+        if (c.g.n < 1)
+            throw std::invalid_argument("empty gaussian set");
+        check_cuda(cudaSetDevice(c.device), "cudaSetDevice");
+        const int64_t chunk = std::max<int64_t>(1, std::min<int64_t>(B, c.chunk));
+        ensure_work(c, chunk);
+        float *d_pos = dalloc<float>(c, size_t(3) * std::max<int64_t>(B, 1));
+        check_cuda(cudaMemcpy(d_pos, pos01, sizeof(float) * 3 * B, cudaMemcpyHostToDevice), "H2D");
+        const int n = c.g.n, np = c.g.np;
+        std::vector<float> planes(size_t(5) * c.w.cap_b * np);
+        const size_t plane = size_t(c.w.cap_b) * np;
+        for (int64_t b0 = 0; b0 < B; b0 += chunk)
+        {
+            const int nb = int(std::min<int64_t>(chunk, B - b0));
+            launch_pos_prep(c, d_pos + 3 * b0, nb, true, c.stream);
+            launch_mlp(c, nb, c.stream);
+            check_cuda(cudaGetLastError(), "launch");
+            check_cuda(cudaMemcpyAsync(planes.data(), c.w.res, planes.size() * sizeof(float), cudaMemcpyDeviceToHost,
+                                       c.stream),
+                       "D2H residuals");
+            check_cuda(cudaStreamSynchronize(c.stream), "predict");
+            for (int s = 0; s < nb; s++)
+                for (int g = 0; g < n; g++)
+                {
+                    const size_t src = size_t(s) * np + g, dst = size_t(b0 + s) * n + g;
+                    dc[2 * dst] = planes[0 * plane + src];
+                    dc[2 * dst + 1] = planes[1 * plane + src];
+                    dr[2 * dst] = planes[2 * plane + src];
+                    dr[2 * dst + 1] = planes[3 * plane + src];
+                    da[dst] = planes[4 * plane + src];
+                }
+        }
+        dfree(c, d_pos);
+    });
+}
+
+int swr_setup(swr_ctx *ctx, const float *dc, const float *dr, const float *da, int64_t B, float *state, int32_t *rows,
+              int32_t *cols, int32_t *tile_count)
+{
+    return guarded([&] {
+        Ctx &c = ctx->c;
+        check_cuda(cudaSetDevice(c.device), "cudaSetDevice");
+        const int64_t chunk = std::max<int64_t>(1, std::min<int64_t>(B, c.chunk));
+        ensure_work(c, chunk);
+        const int n = c.g.n, np = c.g.np;
+        const bool with_res = dc != nullptr;
+        float *d_state = dalloc<float>(c, size_t(chunk) * n * kStateStride);
+        std::vector<int4> rng(size_t(chunk) * np);
+        std::vector<int> cnt(size_t(chunk) * np);
+        for (int64_t b0 = 0; b0 < B; b0 += chunk)
+        {
+            const int nb = int(std::min<int64_t>(chunk, B - b0));
+            if (with_res)
+                upload_residuals(c, dc, dr, da, b0, nb);
+            launch_setup(c, nb, with_res, c.stream);
+            launch_state_out(c, nb, with_res, d_state, c.stream);
+            check_cuda(cudaGetLastError(), "launch");
+            if (state)
+                check_cuda(cudaMemcpyAsync(state + size_t(b0) * n * kStateStride, d_state,
+                                           sizeof(float) * nb * n * kStateStride, cudaMemcpyDeviceToHost, c.stream),
+                           "D2H state");
+            check_cuda(cudaMemcpyAsync(rng.data(), c.w.rng, sizeof(int4) * nb * np, cudaMemcpyDeviceToHost, c.stream),
+                       "D2H ranges");
+            check_cuda(cudaMemcpyAsync(cnt.data(), c.w.cnt, sizeof(int) * nb * np, cudaMemcpyDeviceToHost, c.stream),
+                       "D2H counts");
+            check_cuda(cudaStreamSynchronize(c.stream), "setup");
+            for (int s = 0; s < nb; s++)
+                for (int g = 0; g < n; g++)
+                {
+                    const int4 b = rng[size_t(s) * np + g];
+                    const size_t d = size_t(b0 + s) * n + g;
+                    if (rows)
+                    {
+                        rows[2 * d] = b.x;
+                        rows[2 * d + 1] = b.y;
+                    }
+                    if (cols)
+                    {
+                        cols[2 * d] = b.z;
+                        cols[2 * d + 1] = b.w;
+                    }
+                    if (tile_count)
+                        tile_count[d] = cnt[size_t(s) * np + g];
+                }
+        }
+        dfree(c, d_state);
+    });
+}
+
+static void bins_for(Ctx &c, const float *dc, const float *dr, const float *da, int64_t B, int32_t *tile_offset,
+                     int32_t *tile_prims, int64_t cap, int64_t *n_pairs, float *spectra)
+{
+    check_cuda(cudaSetDevice(c.device), "cudaSetDevice");
+    const int64_t chunk = std::max<int64_t>(1, std::min<int64_t>(B, c.chunk));
+    ensure_work(c, chunk);
+    const bool with_res = dc != nullptr;
+    const int tiles = c.g.tiles;
+    const size_t per = size_t(2) * c.g.H * c.g.W;
+    float *d_spec = spectra ? dalloc<float>(c, per * chunk) : nullptr;
+    int64_t written = 0;
+    std::vector<int64_t> seg(chunk + 1);
+    for (int64_t b0 = 0; b0 < B; b0 += chunk)
+    {
+        const int nb = int(std::min<int64_t>(chunk, B - b0));
+        if (with_res)
+            upload_residuals(c, dc, dr, da, b0, nb);
+        run_chunk(c, nullptr, nb, true, false, with_res, d_spec, false, 0, nullptr, nullptr, nullptr, nullptr,
+                  c.stream);
+        const int64_t pairs = c.pairs_last;
+        if (tile_offset)
+            check_cuda(cudaMemcpyAsync(tile_offset + size_t(b0) * (tiles + 1), c.w.tile_off,
+                                       sizeof(int) * nb * (tiles + 1), cudaMemcpyDeviceToHost, c.stream),
+                       "D2H offsets");
+        if (tile_prims && written < cap)
+            check_cuda(cudaMemcpyAsync(tile_prims + written, c.w.sorted,
+                                       sizeof(int) * std::min<int64_t>(pairs, cap - written), cudaMemcpyDeviceToHost,
+                                       c.stream),
+                       "D2H prims");
+        if (spectra)
+            check_cuda(cudaMemcpyAsync(spectra + per * b0, d_spec, sizeof(float) * per * nb, cudaMemcpyDeviceToHost,
+                                       c.stream),
+                       "D2H spectra");
+        check_cuda(cudaStreamSynchronize(c.stream), "bins");
+        written += pairs;
+    }
+    if (n_pairs)
+        *n_pairs = written;
+    if (d_spec)
+        dfree(c, d_spec);
+}
+
+int swr_bin(swr_ctx *ctx, const float *dc, const float *dr, const float *da, int64_t B, int32_t *tile_offset,
+            int32_t *tile_prims, int64_t cap, int64_t *n_pairs)
+{
+    return guarded([&] { bins_for(ctx->c, dc, dr, da, B, tile_offset, tile_prims, cap, n_pairs, nullptr); });
+}
+
+int swr_rasterize(swr_ctx *ctx, const float *dc, const float *dr, const float *da, int64_t B, float *spectra)
+{
+    return guarded([&] { bins_for(ctx->c, dc, dr, da, B, nullptr, nullptr, 0, nullptr, spectra); });
+}
+
+int swr_heads(swr_ctx *ctx, const float *spectra, int64_t B, double *pooled, int32_t *aoa_rc, double *aoa_ang)
+{
+    return guarded([&] {
+        Ctx &c = ctx->c;
+        check_cuda(cudaSetDevice(c.device), "cudaSetDevice");
+        const int64_t chunk = std::max<int64_t>(1, std::min<int64_t>(B, c.chunk));
+        ensure_work(c, chunk);
+        const size_t per = size_t(2) * c.g.H * c.g.W;
+        float *d_spec = dalloc<float>(c, per * chunk);
+        double *d_pooled = dalloc<double>(c, chunk), *d_ang = dalloc<double>(c, 2 * chunk);
+        int32_t *d_rc = dalloc<int32_t>(c, 2 * chunk);
+        for (int64_t b0 = 0; b0 < B; b0 += chunk)
+        {
+            const int nb = int(std::min<int64_t>(chunk, B - b0));
+            check_cuda(cudaMemcpyAsync(d_spec, spectra + per * b0, sizeof(float) * per * nb, cudaMemcpyHostToDevice,
+                                       c.stream),
+                       "H2D spectra");
+            launch_heads_from_spectra(c, nb, d_spec, c.stream);
+            launch_heads(c, nb, SWR_OUT_POOLED | SWR_OUT_AOA, d_pooled, nullptr, d_rc, d_ang, c.stream);
+            check_cuda(cudaGetLastError(), "launch");
+            if (pooled)
+                check_cuda(cudaMemcpyAsync(pooled + b0, d_pooled, sizeof(double) * nb, cudaMemcpyDeviceToHost, c.stream),
+                           "D2H");
+            if (aoa_rc)
+                check_cuda(cudaMemcpyAsync(aoa_rc + 2 * b0, d_rc, sizeof(int32_t) * 2 * nb, cudaMemcpyDeviceToHost,
+                                           c.stream),
+                           "D2H");
+            if (aoa_ang)
+                check_cuda(cudaMemcpyAsync(aoa_ang + 2 * b0, d_ang, sizeof(double) * 2 * nb, cudaMemcpyDeviceToHost,
+                                           c.stream),
+                           "D2H");
+            check_cuda(cudaStreamSynchronize(c.stream), "heads");
+        }
+        for (void *p : {(void *)d_spec, (void *)d_pooled, (void *)d_ang, (void *)d_rc})
+            dfree(c, p);
+    });
+}
+
+int64_t swr_launch_count(swr_ctx *ctx) { return ctx->c.launches; }
+
+int swr_stage_times(swr_ctx *ctx, double *ms6)
+{
+    for (int i = 0; i < 6; i++)
+        ms6[i] = ctx->c.stage_ms[i];
+    return SWR_OK;
+}
+
+} // extern "C"

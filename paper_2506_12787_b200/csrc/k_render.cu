@@ -1,0 +1,745 @@
+// Per-(position, Gaussian) setup, tile binning (count -> scan -> emit ->
+// stable one-digit radix sort keyed on (position, tile), primitive order kept),
+// tile rasterisation and the AoA / pooled-magnitude / RSSI heads.
+//
+// Reference: splat::rasterize and its prepare() (/root/reference/proj/src/splat.cpp:159-482),
+// tasks::pooled_magnitude / aoa_extract (tasks.cpp:32-39, 154-169).
+//
+// Bit-exactness: every float operation whose rounding reaches the bins, the
+// render state or a cutoff mask is written as an explicit _rn intrinsic (no FMA
+// contraction), mirroring the reference's expression order. Bins additionally
+// depend only on FP64 ops whose float inputs multiply exactly.
+#include "swr_internal.h"
+
+#include <cfloat>
+
+namespace swr
+{
+
+namespace
+{
+__device__ __forceinline__ float fmaxr(float a, float b) { return (a < b) ? b : a; } // std::max
+__device__ __forceinline__ float fminr(float a, float b) { return (b < a) ? b : a; } // std::min
+
+// splat.cpp:72-82
+__device__ __forceinline__ float wrap_pm_pi(float x)
+{
+    if (x < (float)(-8 * kPi) || x > (float)(8 * kPi))
+        x = fmodf(x, (float)(2 * kPi));
+    while (x >= (float)kPi)
+        x = __fsub_rn(x, (float)(2 * kPi));
+    while (x < (float)(-kPi))
+        x = __fadd_rn(x, (float)(2 * kPi));
+    return x;
+}
+
+// Tiles of one primitive, splat.cpp:255-282 (count only)
+__device__ __forceinline__ int tile_count(const Grid &g, int r0, int r1, int j0, int len)
+{
+    if (r1 < r0)
+        return 0;
+    const int ntr = r1 / g.tile - r0 / g.tile + 1;
+    int ntc;
+    if (len >= g.W)
+        ntc = g.tw;
+    else
+    {
+        const int jend = j0 + len - 1;
+        ntc = min(jend, g.W - 1) / g.tile - j0 / g.tile + 1;
+        if (jend >= g.W)
+        {
+            const int e1 = min((jend - g.W) / g.tile, j0 / g.tile - 1);
+            ntc += e1 >= 0 ? e1 + 1 : 0;
+        }
+    }
+    return ntr * ntc;
+}
+
+struct PrimOut
+{
+    float el, az, delta, re, im;
+};
+
+// splat.cpp:94-118 with host-precomputed el0/az0/delta0 (bit-identical to the
+// reference's glibc tanhf/expf results)
+__device__ __forceinline__ PrimOut deform_prim(const SceneDev &s, const float *res, int64_t plane, int g, bool with_res)
+{
+    PrimOut p;
+    p.el = s.el0[g];
+    p.az = s.az0[g];
+    p.delta = s.delta0[g];
+    p.re = s.re0[g];
+    p.im = s.im0[g];
+    if (with_res)
+    {
+        p.el = __fadd_rn(p.el, res[0 * plane + g]);
+        p.az = __fadd_rn(p.az, res[1 * plane + g]);
+        p.re = __fadd_rn(p.re, res[2 * plane + g]);
+        p.im = __fadd_rn(p.im, res[3 * plane + g]);
+        p.delta = fminr(fmaxr(__fadd_rn(p.delta, res[4 * plane + g]), 0.0f), 1.0f);
+    }
+    return p;
+}
+
+// bbox rows/cols (splat.cpp:197-248); returns (r0, r1, j0, len), rows empty = (0, -1)
+__device__ __forceinline__ int4 bbox_of(const Grid &g, float el, float az, float delta, double2 h)
+{
+    if (delta <= 0.0f)
+        return make_int4(0, -1, 0, 0);
+    if (!g.cut)
+        return make_int4(0, g.H - 1, 0, g.W);
+    int r0 = (int)floor(__dsub_rn(__ddiv_rn(__dsub_rn((double)el, h.x), g.cell_el), 0.5));
+    int r1 = (int)ceil(__dsub_rn(__ddiv_rn(__dadd_rn((double)el, h.x), g.cell_el), 0.5));
+    r0 = max(r0, 0);
+    r1 = min(r1, g.H - 1);
+    if (r0 > r1)
+        return make_int4(0, -1, 0, 0);
+    if (__dmul_rn(2.0, h.y) >= __dmul_rn((double)g.W, g.cell_az))
+        return make_int4(r0, r1, 0, g.W);
+    int j0 = (int)floor(__dsub_rn(__ddiv_rn(__dsub_rn((double)az, h.y), g.cell_az), 0.5));
+    const int j1 = (int)ceil(__dsub_rn(__ddiv_rn(__dadd_rn((double)az, h.y), g.cell_az), 0.5));
+    const int len = min(j1 - j0 + 1, g.W);
+    j0 = ((j0 % g.W) + g.W) % g.W;
+    return make_int4(r0, r1, j0, len);
+}
+} // namespace
+
+// ------------------------------------------------------------------------ setup
+
+// One thread per (position, 4 consecutive Gaussians): float4 loads of the
+// planar residuals and static SoA; writes dyn (el, az, k_re, k_im), the
+// row/column ranges and the tile count.
+__global__ void __launch_bounds__(256) setup_kernel(Grid g, SceneDev sd, const float *__restrict__ res, int64_t plane,
+                                                    float4 *__restrict__ dyn, int4 *__restrict__ rng, int *__restrict__ cnt,
+                                                    int with_res)
+{
+    const int s = blockIdx.y;
+    const int g4 = (blockIdx.x * blockDim.x + threadIdx.x) * 4;
+    if (g4 >= g.np)
+        return;
+    const int64_t base = (int64_t)s * g.np;
+    float r_el[4], r_az[4], r_re[4], r_im[4], r_dl[4];
+    const float4 e0 = *reinterpret_cast<const float4 *>(sd.el0 + g4);
+    const float4 a0 = *reinterpret_cast<const float4 *>(sd.az0 + g4);
+    const float4 d0 = *reinterpret_cast<const float4 *>(sd.delta0 + g4);
+    const float4 re = *reinterpret_cast<const float4 *>(sd.re0 + g4);
+    const float4 im = *reinterpret_cast<const float4 *>(sd.im0 + g4);
+    r_el[0] = e0.x; r_el[1] = e0.y; r_el[2] = e0.z; r_el[3] = e0.w;
+    r_az[0] = a0.x; r_az[1] = a0.y; r_az[2] = a0.z; r_az[3] = a0.w;
+    r_dl[0] = d0.x; r_dl[1] = d0.y; r_dl[2] = d0.z; r_dl[3] = d0.w;
+    r_re[0] = re.x; r_re[1] = re.y; r_re[2] = re.z; r_re[3] = re.w;
+    r_im[0] = im.x; r_im[1] = im.y; r_im[2] = im.z; r_im[3] = im.w;
+    if (with_res)
+    {
+        const float *rb = res + base;
+        const float4 x0 = *reinterpret_cast<const float4 *>(rb + 0 * plane + g4);
+        const float4 x1 = *reinterpret_cast<const float4 *>(rb + 1 * plane + g4);
+        const float4 x2 = *reinterpret_cast<const float4 *>(rb + 2 * plane + g4);
+        const float4 x3 = *reinterpret_cast<const float4 *>(rb + 3 * plane + g4);
+        const float4 x4 = *reinterpret_cast<const float4 *>(rb + 4 * plane + g4);
+        const float v0[4] = {x0.x, x0.y, x0.z, x0.w}, v1[4] = {x1.x, x1.y, x1.z, x1.w};
+        const float v2[4] = {x2.x, x2.y, x2.z, x2.w}, v3[4] = {x3.x, x3.y, x3.z, x3.w};
+        const float v4[4] = {x4.x, x4.y, x4.z, x4.w};
+#pragma unroll
+        for (int k = 0; k < 4; k++)
+        {
+            r_el[k] = __fadd_rn(r_el[k], v0[k]);
+            r_az[k] = __fadd_rn(r_az[k], v1[k]);
+            r_re[k] = __fadd_rn(r_re[k], v2[k]);
+            r_im[k] = __fadd_rn(r_im[k], v3[k]);
+            r_dl[k] = fminr(fmaxr(__fadd_rn(r_dl[k], v4[k]), 0.0f), 1.0f);
+        }
+    }
+#pragma unroll
+    for (int k = 0; k < 4; k++)
+    {
+        const int gi = g4 + k;
+        int4 b = make_int4(0, -1, 0, 0);
+        if (gi < g.n)
+            b = bbox_of(g, r_el[k], r_az[k], r_dl[k], sd.half[gi]);
+        dyn[base + gi] = make_float4(r_el[k], r_az[k], __fmul_rn(r_re[k], r_dl[k]), __fmul_rn(r_im[k], r_dl[k]));
+        rng[base + gi] = b;
+        cnt[base + gi] = gi < g.n ? tile_count(g, b.x, b.y, b.z, b.w) : 0;
+    }
+}
+
+void launch_setup(Ctx &c, int nb, bool with_res, cudaStream_t st)
+{
+    dim3 grid((c.g.np / 4 + 255) / 256, nb);
+    setup_kernel<<<grid, 256, 0, st>>>(c.g, c.s, c.w.res, c.w.cap_b * c.g.np, c.w.dyn, c.w.rng, c.w.cnt, with_res);
+    c.launches++;
+}
+
+// The reference's 11-float render state (splat.cpp:133-147, 200-211); all
+// zero when delta <= 0 (splat.cpp:197-198). Parity hook only.
+__global__ void state_out_kernel(Grid g, SceneDev sd, const float *__restrict__ res, int64_t plane, int with_res,
+                                 float *__restrict__ state, int nb)
+{
+    const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (idx >= (int64_t)nb * g.n)
+        return;
+    const int s = (int)(idx / g.n), gi = (int)(idx % g.n);
+    const PrimOut p = deform_prim(sd, res + (int64_t)s * g.np, plane, gi, with_res);
+    float *st = state + idx * kStateStride;
+    if (p.delta <= 0.0f)
+    {
+        for (int k = 0; k < kStateStride; k++)
+            st[k] = 0.0f;
+        return;
+    }
+    const float4 sh = sd.shape[gi];
+    st[0] = p.el;
+    st[1] = p.az;
+    st[2] = sh.x;
+    st[3] = sh.y;
+    st[4] = sh.z;
+    st[5] = p.delta;
+    st[6] = p.re;
+    st[7] = p.im;
+    st[8] = sh.w;
+    st[9] = sd.inv_l3[gi];
+    st[10] = sd.l2[gi];
+}
+
+void launch_state_out(Ctx &c, int nb, bool with_res, float *d_state, cudaStream_t st)
+{
+    const int64_t total = (int64_t)nb * c.g.n;
+    state_out_kernel<<<(unsigned)((total + 255) / 256), 256, 0, st>>>(c.g, c.s, c.w.res, c.w.cap_b * c.g.np,
+                                                                      with_res ? 1 : 0,
+                                                                      d_state, nb);
+    c.launches++;
+}
+
+// ---------------------------------------------------------------- bin: counts
+
+// Block-wide exclusive scan helper (blockDim multiple of 32, <= 1024)
+__device__ __forceinline__ int block_excl_scan(int v, int *warp_sums, int &total)
+{
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    int x = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1)
+    {
+        const int y = __shfl_up_sync(0xffffffffu, x, o);
+        if (lane >= o)
+            x += y;
+    }
+    if (lane == 31)
+        warp_sums[wid] = x;
+    __syncthreads();
+    if (wid == 0)
+    {
+        int w = lane < nw ? warp_sums[lane] : 0;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1)
+        {
+            const int y = __shfl_up_sync(0xffffffffu, w, o);
+            if (lane >= o)
+                w += y;
+        }
+        if (lane < nw)
+            warp_sums[lane] = w;
+    }
+    __syncthreads();
+    const int before = (wid > 0 ? warp_sums[wid - 1] : 0) + x - v;
+    total = warp_sums[nw - 1];
+    __syncthreads();
+    return before;
+}
+
+// One CTA per position: exclusive scan of per-primitive tile counts (the pair
+// offsets of each primitive inside its position's segment).
+__global__ void __launch_bounds__(1024) seg_scan_kernel(const int *__restrict__ cnt, int *__restrict__ poff,
+                                                        int64_t *__restrict__ seg_len, int np, int n)
+{
+    __shared__ int ws[32];
+    const int s = blockIdx.x;
+    const int *c = cnt + (int64_t)s * np;
+    int *o = poff + (int64_t)s * np;
+    int carry = 0;
+    for (int base = 0; base < n; base += 4 * blockDim.x)
+    {
+        const int i0 = base + 4 * threadIdx.x;
+        int v[4], sum = 0;
+#pragma unroll
+        for (int k = 0; k < 4; k++)
+        {
+            v[k] = (i0 + k < n) ? c[i0 + k] : 0;
+            sum += v[k];
+        }
+        int total;
+        int run = block_excl_scan(sum, ws, total) + carry;
+#pragma unroll
+        for (int k = 0; k < 4; k++)
+        {
+            if (i0 + k < n)
+                o[i0 + k] = run;
+            run += v[k];
+        }
+        carry += total;
+    }
+    if (threadIdx.x == 0)
+        seg_len[s] = carry;
+}
+
+// Exclusive scan over the position segments (one CTA): seg[s] = first pair of
+// position s, seg[nb] = total; out[0] = total, out[1] = longest segment.
+__global__ void __launch_bounds__(1024) seg_base_kernel(int64_t *__restrict__ seg, int nb, int64_t *__restrict__ out)
+{
+    __shared__ int64_t part[1024];
+    __shared__ int64_t mx[1024];
+    const int t = threadIdx.x;
+    const int per = (nb + blockDim.x - 1) / blockDim.x;
+    int64_t sum = 0, m = 0;
+    for (int k = 0; k < per; k++)
+    {
+        const int i = t * per + k;
+        if (i < nb)
+        {
+            sum += seg[i];
+            m = max(m, seg[i]);
+        }
+    }
+    part[t] = sum;
+    mx[t] = m;
+    __syncthreads();
+    if (t == 0)
+    {
+        int64_t run = 0, mm = 0;
+        for (int i = 0; i < (int)blockDim.x; i++)
+        {
+            const int64_t v = part[i];
+            part[i] = run;
+            run += v;
+            mm = max(mm, mx[i]);
+        }
+        out[0] = run;
+        out[1] = mm;
+    }
+    __syncthreads();
+    int64_t run = part[t];
+    for (int k = 0; k < per; k++)
+    {
+        const int i = t * per + k;
+        if (i < nb)
+        {
+            const int64_t v = seg[i];
+            seg[i] = run;
+            run += v;
+        }
+    }
+    if (t == blockDim.x - 1)
+        seg[nb] = run;
+}
+
+void launch_bin_count(Ctx &c, int nb, cudaStream_t st)
+{
+    // seg[] first receives the per-position lengths, then their exclusive scan
+    seg_scan_kernel<<<nb, 1024, 0, st>>>(c.w.cnt, c.w.poff, c.w.seg, c.g.np, c.g.n);
+    seg_base_kernel<<<1, 1024, 0, st>>>(c.w.seg, nb, c.w.stats);
+    c.launches += 2;
+}
+
+// ------------------------------------------------------------ bin: emit + sort
+
+// Emit (tile key, primitive) pairs in (position, primitive) order; the tiles of
+// one primitive follow the reference's visit order (splat.cpp:255-282).
+__global__ void __launch_bounds__(256) emit_kernel(Grid g, const int4 *__restrict__ rng, const int *__restrict__ poff,
+                                                   const int64_t *__restrict__ seg, uint16_t *__restrict__ keys,
+                                                   int *__restrict__ vals)
+{
+    const int s = blockIdx.y;
+    const int gi = blockIdx.x * blockDim.x + threadIdx.x;
+    if (gi >= g.n)
+        return;
+    const int4 b = rng[(int64_t)s * g.np + gi];
+    if (b.y < b.x)
+        return;
+    int64_t o = seg[s] + poff[(int64_t)s * g.np + gi];
+    const int tr0 = b.x / g.tile, tr1 = b.y / g.tile;
+    auto col = [&](int tc) {
+        for (int tr = tr0; tr <= tr1; tr++)
+        {
+            keys[o] = (uint16_t)(tr * g.tw + tc);
+            vals[o] = gi;
+            o++;
+        }
+    };
+    if (b.w >= g.W)
+    {
+        for (int tc = 0; tc < g.tw; tc++)
+            col(tc);
+        return;
+    }
+    const int jend = b.z + b.w - 1;
+    for (int tc = b.z / g.tile; tc <= min(jend, g.W - 1) / g.tile; tc++)
+        col(tc);
+    if (jend >= g.W)
+        for (int tc = 0; tc <= min((jend - g.W) / g.tile, b.z / g.tile - 1); tc++)
+            col(tc);
+}
+
+constexpr int kSortThreads = 256; // 8 warps, 512 pairs per warp per sort chunk
+
+// Per (position, chunk of kSort pairs): histogram of tile keys.
+__global__ void __launch_bounds__(kSortThreads) sort_hist_kernel(const uint16_t *__restrict__ keys,
+                                                                 const int64_t *__restrict__ seg, int *__restrict__ hist,
+                                                                 int max_chunks, int tiles)
+{
+    extern __shared__ int h[];
+    const int c = blockIdx.x, s = blockIdx.y;
+    for (int t = threadIdx.x; t < tiles; t += blockDim.x)
+        h[t] = 0;
+    __syncthreads();
+    const int64_t b = seg[s] + (int64_t)c * kSort, e = min(seg[s + 1], b + kSort);
+    for (int64_t i = b + threadIdx.x; i < e; i += blockDim.x)
+        atomicAdd(&h[keys[i]], 1);
+    __syncthreads();
+    int *out = hist + ((int64_t)s * max_chunks + c) * tiles;
+    for (int t = threadIdx.x; t < tiles; t += blockDim.x)
+        out[t] = h[t];
+}
+
+// Per position: CSR tile offsets (exclusive scan over tiles) and, in place,
+// each chunk's starting offset per tile (tile-major, chunk-minor).
+__global__ void __launch_bounds__(1024) sort_scan_kernel(const int64_t *__restrict__ seg, int *__restrict__ hist,
+                                                         int *__restrict__ tile_off, int max_chunks, int tiles)
+{
+    __shared__ int ws[32];
+    const int s = blockIdx.x, t = threadIdx.x;
+    const int64_t len = seg[s + 1] - seg[s];
+    const int nch = (int)((len + kSort - 1) / kSort);
+    int *hs = hist + (int64_t)s * max_chunks * tiles;
+    int total_t = 0;
+    if (t < tiles)
+        for (int c = 0; c < nch; c++)
+            total_t += hs[c * tiles + t];
+    int all;
+    const int off = block_excl_scan(total_t, ws, all);
+    if (t < tiles)
+    {
+        tile_off[(int64_t)s * (tiles + 1) + t] = off;
+        int run = off;
+        for (int c = 0; c < nch; c++)
+        {
+            const int v = hs[c * tiles + t];
+            hs[c * tiles + t] = run;
+            run += v;
+        }
+    }
+    if (t == 0)
+        tile_off[(int64_t)s * (tiles + 1) + tiles] = (int)len;
+}
+
+// Stable scatter of one chunk: warp-level ranking with __match_any_sync keeps
+// primitive order among equal tiles (a one-digit LSD radix pass).
+__global__ void __launch_bounds__(kSortThreads) sort_scatter_kernel(const uint16_t *__restrict__ keys,
+                                                                    const int *__restrict__ vals,
+                                                                    const int64_t *__restrict__ seg,
+                                                                    const int *__restrict__ hist, int *__restrict__ out,
+                                                                    int max_chunks, int tiles)
+{
+    extern __shared__ int whist[]; // [8][tiles]
+    constexpr int kWarps = kSortThreads / 32, kRounds = kSort / kSortThreads;
+    const int c = blockIdx.x, s = blockIdx.y;
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const int64_t b = seg[s] + (int64_t)c * kSort, e = min(seg[s + 1], b + kSort);
+    if (b >= e)
+        return;
+    for (int i = threadIdx.x; i < kWarps * tiles; i += blockDim.x)
+        whist[i] = 0;
+    __syncthreads();
+    int *wh = whist + w * tiles;
+    int rk[kRounds];
+    uint16_t ky[kRounds];
+    const unsigned lt = (1u << lane) - 1u;
+#pragma unroll
+    for (int k = 0; k < kRounds; k++)
+    {
+        const int64_t i = b + (int64_t)w * (kSort / kWarps) + k * 32 + lane;
+        const bool valid = i < e;
+        const unsigned key = valid ? keys[i] : 0xffffu;
+        const unsigned peers = __match_any_sync(0xffffffffu, key);
+        const int leader = __ffs(peers) - 1;
+        int base = 0;
+        if (valid)
+            base = wh[key];
+        __syncwarp();
+        if (valid && lane == leader)
+            wh[key] = base + __popc(peers);
+        __syncwarp();
+        rk[k] = base + __popc(peers & lt);
+        ky[k] = (uint16_t)key;
+    }
+    __syncthreads();
+    const int *hc = hist + ((int64_t)s * max_chunks + c) * tiles;
+    for (int t = threadIdx.x; t < tiles; t += blockDim.x)
+    {
+        int run = hc[t];
+        for (int ww = 0; ww < kWarps; ww++)
+        {
+            const int v = whist[ww * tiles + t];
+            whist[ww * tiles + t] = run;
+            run += v;
+        }
+    }
+    __syncthreads();
+#pragma unroll
+    for (int k = 0; k < kRounds; k++)
+    {
+        const int64_t i = b + (int64_t)w * (kSort / kWarps) + k * 32 + lane;
+        if (i < e)
+            out[seg[s] + wh[ky[k]] + rk[k]] = vals[i];
+    }
+}
+
+void launch_bin_sort(Ctx &c, int nb, int64_t pairs, int max_seg, cudaStream_t st)
+{
+    const int tiles = c.g.tiles;
+    dim3 ge((c.g.n + 255) / 256, nb);
+    emit_kernel<<<ge, 256, 0, st>>>(c.g, c.w.rng, c.w.poff, c.w.seg, c.w.keys, c.w.vals);
+    const int nch = std::max(1, (max_seg + kSort - 1) / kSort);
+    dim3 gs(nch, nb);
+    sort_hist_kernel<<<gs, kSortThreads, tiles * sizeof(int), st>>>(c.w.keys, c.w.seg, c.w.chunk_hist, c.w.max_chunks,
+                                                                    tiles);
+    sort_scan_kernel<<<nb, 1024, 0, st>>>(c.w.seg, c.w.chunk_hist, c.w.tile_off, c.w.max_chunks, tiles);
+    sort_scatter_kernel<<<gs, kSortThreads, 8 * tiles * sizeof(int), st>>>(c.w.keys, c.w.vals, c.w.seg,
+                                                                           c.w.chunk_hist, c.w.sorted,
+                                                                           c.w.max_chunks, tiles);
+    c.launches += 4;
+}
+
+// ------------------------------------------------------------------ raster
+
+struct __align__(16) Staged
+{
+    float el, az, k_re, k_im;
+    float i00, i01, i11, inv_l1;
+    int r0, r1, j0, len;
+};
+
+// Block reduction of (max |A|, first argmax cell, sum |A|) for the heads.
+__device__ __forceinline__ void heads_reduce(float mag, int cell, double msum, float4 *tile_part, double *tile_sum)
+{
+    __shared__ float smax[32];
+    __shared__ int sidx[32];
+    __shared__ double ssum[32];
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1)
+    {
+        const float om = __shfl_xor_sync(0xffffffffu, mag, o);
+        const int oi = __shfl_xor_sync(0xffffffffu, cell, o);
+        if (om > mag || (om == mag && oi < cell))
+        {
+            mag = om;
+            cell = oi;
+        }
+        msum += __shfl_xor_sync(0xffffffffu, msum, o);
+    }
+    if (lane == 0)
+    {
+        smax[wid] = mag;
+        sidx[wid] = cell;
+        ssum[wid] = msum;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0)
+    {
+        float m = smax[0];
+        int ci = sidx[0];
+        double sm = ssum[0];
+        for (int k = 1; k < nw; k++)
+        {
+            if (smax[k] > m || (smax[k] == m && sidx[k] < ci))
+            {
+                m = smax[k];
+                ci = sidx[k];
+            }
+            sm += ssum[k];
+        }
+        *tile_part = make_float4(m, __int_as_float(ci), 0.f, 0.f);
+        *tile_sum = sm;
+    }
+}
+
+// magnitude (spectrum.cpp:141): float(hypot(double re, double im))
+__device__ __forceinline__ float cell_mag(float re, float im)
+{
+    const double x = re, y = im;
+    return (float)__dsqrt_rn(__dadd_rn(__dmul_rn(x, x), __dmul_rn(y, y)));
+}
+
+// One CTA per (tile, position), one thread per cell. The tile's primitive
+// list (ascending primitive index, the reference's per-cell summation order)
+// is staged into shared memory in batches; a warp skips a primitive when none
+// of its cells lies inside the primitive's clipped box / marginal-row bound.
+__global__ void __launch_bounds__(256) raster_kernel(Grid g, SceneDev sd, const float4 *__restrict__ dyn,
+                                                     const int4 *__restrict__ rng, const int64_t *__restrict__ seg,
+                                                     const int *__restrict__ tile_off, const int *__restrict__ prims,
+                                                     float *__restrict__ spec, float4 *__restrict__ tile_part,
+                                                     double *__restrict__ tile_sum, int want_heads)
+{
+    __shared__ Staged sp[256];
+    const int t = blockIdx.x, s = blockIdx.y;
+    const int tr = t / g.tw, tc = t % g.tw;
+    const int ty = threadIdx.x / g.tile, tx = threadIdx.x % g.tile;
+    const int r = tr * g.tile + ty, c = tc * g.tile + tx;
+    const bool valid = r < g.H && c < g.W && ty < g.tile;
+    const float el_r = valid ? sd.el_c[r] : 0.f;
+    const float az_c = valid ? sd.az_c[c] : 0.f;
+    const int *tl = tile_off + (int64_t)s * (g.tiles + 1);
+    const int64_t lb = seg[s] + tl[t], le = seg[s] + tl[t + 1];
+    const int64_t sbase = (int64_t)s * g.np;
+    float acc_re = 0.f, acc_im = 0.f;
+
+    for (int64_t b0 = lb; b0 < le; b0 += 256)
+    {
+        const int m = (int)(le - b0 < 256 ? le - b0 : 256);
+        __syncthreads();
+        if ((int)threadIdx.x < m)
+        {
+            const int gi = prims[b0 + threadIdx.x];
+            // (blocks wider than 256 threads stage with their first 256 lanes)
+            const float4 d = dyn[sbase + gi];
+            const float4 sh = sd.shape[gi];
+            const int4 b = rng[sbase + gi];
+            Staged st;
+            st.el = d.x;
+            st.az = d.y;
+            st.k_re = d.z;
+            st.k_im = d.w;
+            st.i00 = sh.x;
+            st.i01 = sh.y;
+            st.i11 = sh.z;
+            st.inv_l1 = sh.w;
+            st.r0 = b.x;
+            st.r1 = b.y;
+            st.j0 = b.z;
+            st.len = b.w;
+            sp[threadIdx.x] = st;
+        }
+        __syncthreads();
+        for (int i = 0; i < m; i++)
+        {
+            const Staged &P = sp[i];
+            int dj = c - P.j0;
+            if (dj < 0)
+                dj += g.W;
+            bool act = valid && r >= P.r0 && r <= P.r1 && (P.len >= g.W || dj < P.len);
+            const float d_el = __fsub_rn(el_r, P.el);
+            const float u0 = __fmul_rn(d_el, P.inv_l1);
+            act = act && !(__fmul_rn(u0, u0) > g.cut2);
+            if (!__any_sync(0xffffffffu, act))
+                continue;
+            const float d_az = wrap_pm_pi(__fsub_rn(az_c, P.az));
+            const float w1 = __fmul_rn(__fmul_rn(P.i11, d_az), d_az);
+            const float w2 = __fmul_rn(__fmul_rn(2.0f, P.i01), d_az);
+            const float q_c = __fmul_rn(__fmul_rn(P.i00, d_el), d_el);
+            const float q = __fadd_rn(__fadd_rn(q_c, __fmul_rn(d_el, w2)), w1);
+            if (act && q <= g.cut2)
+            {
+                const float e = expf(-0.5f * q);
+                acc_re = __fmaf_rn(P.k_re, e, acc_re);
+                acc_im = __fmaf_rn(P.k_im, e, acc_im);
+            }
+        }
+    }
+    if (valid && spec)
+        reinterpret_cast<float2 *>(spec)[((int64_t)s * g.H + r) * g.W + c] = make_float2(acc_re, acc_im);
+    if (want_heads)
+    {
+        const float mag = valid ? cell_mag(acc_re, acc_im) : -1.0f;
+        const int cell = valid ? r * g.W + c : 0x7fffffff;
+        heads_reduce(mag, cell, valid ? (double)mag : 0.0, tile_part + (int64_t)s * g.tiles + t,
+                     tile_sum + (int64_t)s * g.tiles + t);
+    }
+}
+
+void launch_raster(Ctx &c, int nb, float *d_spec, bool want_heads, cudaStream_t st)
+{
+    dim3 grid(c.g.tiles, nb);
+    const int threads = ((c.g.tile * c.g.tile + 31) / 32) * 32;
+    raster_kernel<<<grid, threads, 0, st>>>(c.g, c.s, c.w.dyn, c.w.rng, c.w.seg, c.w.tile_off, c.w.sorted, d_spec,
+                                            c.w.tile_part, c.w.tile_sum, want_heads ? 1 : 0);
+    c.launches++;
+}
+
+// Heads on given spectra: the same per-tile partials as the raster epilogue.
+__global__ void tile_heads_kernel(Grid g, const float *__restrict__ spec, float4 *__restrict__ tile_part,
+                                  double *__restrict__ tile_sum)
+{
+    const int t = blockIdx.x, s = blockIdx.y;
+    const int tr = t / g.tw, tc = t % g.tw;
+    const int ty = threadIdx.x / g.tile, tx = threadIdx.x % g.tile;
+    const int r = tr * g.tile + ty, c = tc * g.tile + tx;
+    const bool valid = r < g.H && c < g.W && ty < g.tile;
+    float mag = -1.0f;
+    if (valid)
+    {
+        const float2 v = reinterpret_cast<const float2 *>(spec)[((int64_t)s * g.H + r) * g.W + c];
+        mag = cell_mag(v.x, v.y);
+    }
+    heads_reduce(mag, valid ? r * g.W + c : 0x7fffffff, valid ? (double)mag : 0.0,
+                 tile_part + (int64_t)s * g.tiles + t, tile_sum + (int64_t)s * g.tiles + t);
+}
+
+void launch_heads_from_spectra(Ctx &c, int nb, const float *d_spec, cudaStream_t st)
+{
+    dim3 grid(c.g.tiles, nb);
+    const int threads = ((c.g.tile * c.g.tile + 31) / 32) * 32;
+    tile_heads_kernel<<<grid, threads, 0, st>>>(c.g, d_spec, c.w.tile_part, c.w.tile_sum);
+    c.launches++;
+}
+
+// Combine the per-tile partials: AoA = first maximum in row-major order
+// (tasks.cpp:158-162), pooled = sum |A| / cells (tasks.cpp:32-39), RSSI affine.
+__global__ void heads_kernel(Grid g, const float4 *__restrict__ tile_part, const double *__restrict__ tile_sum,
+                             int nb, double slope, double intercept, double *pooled, double *rssi, int32_t *aoa_rc,
+                             double *aoa_ang)
+{
+    const int s = blockIdx.x * blockDim.x + threadIdx.x;
+    if (s >= nb)
+        return;
+    float m = -2.0f;
+    int ci = 0x7fffffff;
+    double sum = 0.0;
+    for (int t = 0; t < g.tiles; t++)
+    {
+        const float4 p = tile_part[(int64_t)s * g.tiles + t];
+        const int pi = __float_as_int(p.y);
+        if (p.x > m || (p.x == m && pi < ci))
+        {
+            m = p.x;
+            ci = pi;
+        }
+        sum += tile_sum[(int64_t)s * g.tiles + t];
+    }
+    const double pm = sum / (double)(g.H * g.W);
+    if (pooled)
+        pooled[s] = pm;
+    if (rssi)
+        rssi[s] = slope * pm + intercept;
+    const int row = ci / g.W, col = ci % g.W;
+    if (aoa_rc)
+    {
+        aoa_rc[2 * s] = row;
+        aoa_rc[2 * s + 1] = col;
+    }
+    if (aoa_ang)
+    {
+        aoa_ang[2 * s] = (row + 0.5) * g.cell_el;
+        aoa_ang[2 * s + 1] = (col + 0.5) * g.cell_az;
+    }
+}
+
+void launch_heads(Ctx &c, int nb, uint32_t flags, double *d_pooled, double *d_rssi, int32_t *d_aoa_rc,
+                  double *d_aoa_ang, cudaStream_t st)
+{
+    (void)flags;
+    heads_kernel<<<(nb + 127) / 128, 128, 0, st>>>(c.g, c.w.tile_part, c.w.tile_sum, nb, c.rssi_slope,
+                                                   c.rssi_intercept, d_pooled, d_rssi, d_aoa_rc, d_aoa_ang);
+    c.launches++;
+}
+
+} // namespace swr

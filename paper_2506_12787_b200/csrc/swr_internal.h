@@ -1,0 +1,122 @@
+// Internal types shared by the CUDA translation units of libswr.so.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <string>
+#include <vector>
+
+namespace swr
+{
+
+constexpr double kPi = 3.141592653589793238462643383279502884;
+constexpr int kTrunk = 8;
+constexpr int kSort = 4096;    // pairs per sort chunk (one CTA)
+constexpr int kStateStride = 11; // splat.cpp:133-147
+
+// Per-scene constants the kernels read (passed by value).
+struct Grid
+{
+    int H, W, n, np;      // np: n padded to a multiple of 16
+    int tile, th, tw, tiles;
+    int cut;              // cutoff_radius > 0
+    float cut2;           // cutoff^2 or +inf
+    float radius;
+    double cell_el, cell_az;
+};
+
+// Device-resident static scene (per Gaussian, planar SoA, length np).
+struct SceneDev
+{
+    float *el0, *az0;      // materialized centres (host glibc tanhf, splat.cpp:60-65)
+    float *delta0;         // sigmoid(logit) (host glibc expf, splat.cpp:105-106)
+    float *re0, *im0;      // response
+    float4 *shape;         // (i00, i01, i11, inv_l1) — static: residuals never touch the covariance
+    float *inv_l3, *l2;    // remaining state fields (parity output only)
+    double2 *half;         // FP64 bbox half widths (radius*l1, radius*sqrt(l2^2+l3^2)), splat.cpp:223-225
+    float *el_c, *az_c;    // float(cell centres) (splat.cpp:180-185)
+};
+
+// Deformation MLP on the device.
+struct NetDev
+{
+    int width, wp;         // width, padded width (multiple of 32)
+    int bands_c, bands_p, dc, dp, d;
+    float *whT;            // [7][wp][wp] hidden->hidden weights, k-major (layers 1..7), zero padded
+    float *bias;           // [8][wp]
+    float *cg;             // [np][4][wp] centre-encoding contribution of layers 0,2,4,6 (no bias)
+    float *wpos;           // [4][wp][dp] position-encoding columns of layers 0,2,4,6
+    float *wcen;           // [4][wp][dc] centre-encoding columns of layers 0,2,4,6
+    float *heads;          // [5][wp] head weights (centre 2, response 2, atten 1)
+    float *hbias;          // [5]
+    // tcgen05 path (bf16 hi/lo, UMMA canonical K-major layout, see k_mlp_tc.cu)
+    uint16_t *w_tc;        // [7][2 (hi,lo)][chunks][wp x 16] packed
+};
+
+// Per-chunk scratch (positions per chunk = cap_b).
+struct Work
+{
+    int64_t cap_b = 0, cap_pairs = 0;
+    float *pos01 = nullptr;     // [cap_b][4]
+    float *pterm = nullptr;     // [cap_b][4][wp] position contribution (+bias) of layers 0,2,4,6
+    float *res = nullptr;       // [5][cap_b][np] residual planes (dEl, dAz, dRe, dIm, dDelta)
+    float4 *dyn = nullptr;      // [cap_b][np] (el, az, k_re, k_im)
+    int4 *rng = nullptr;        // [cap_b][np] (r0, r1, j0, len)
+    int *cnt = nullptr;         // [cap_b][np] tiles per primitive
+    int64_t *seg = nullptr;     // [cap_b + 1] segment (position) base offsets into the pair array
+    int *poff = nullptr;        // [cap_b][np] exclusive pair offset of each primitive within its segment
+    int *tile_off = nullptr;    // [cap_b][tiles + 1] CSR offsets within the segment
+    int *chunk_hist = nullptr;  // [cap_b][max_chunks][tiles]
+    int max_chunks = 0;
+    uint16_t *keys = nullptr;   // [cap_pairs] tile of each pair (primitive order)
+    int *vals = nullptr;        // [cap_pairs] primitive of each pair (primitive order)
+    int *sorted = nullptr;      // [cap_pairs] tile_prims (tile-major, primitive order inside)
+    float4 *tile_part = nullptr; // [cap_b][tiles] (max |A|, argmax cell as float bits, sum |A| hi, lo)
+    double *tile_sum = nullptr; // [cap_b][tiles]
+    int64_t *stats = nullptr;      // device: (total pairs, longest segment) of the current chunk
+    int64_t *host_pairs = nullptr; // pinned mirror of stats
+};
+
+struct Ctx
+{
+    int device = 0;
+    Grid g{};
+    SceneDev s{};
+    NetDev net{};
+    bool has_net = false;
+    double bbox_min[3]{}, bbox_max[3]{};
+    float cutoff = 3.0f;
+    int tile = 16;
+    int mlp_precision = 0;
+    int chunk = 256;
+    bool stage_timing = false;
+    double rssi_slope = 1.0, rssi_intercept = 0.0;
+    cudaStream_t stream = nullptr;
+    Work w;
+    int64_t launches = 0;
+    int64_t pairs_last = 0;
+    double stage_ms[6]{};
+    std::vector<void *> allocs;
+};
+
+// kernels (k_mlp.cu, k_render.cu). All launch on `st` and bump ctx.launches.
+void launch_pos_prep(Ctx &c, const float *d_pos_m, int nb, bool normalized, cudaStream_t st);
+void launch_mlp(Ctx &c, int nb, cudaStream_t st);
+void launch_center_terms(Ctx &c, const float *d_cenc, cudaStream_t st);
+void launch_setup(Ctx &c, int nb, bool with_res, cudaStream_t st);
+void launch_state_out(Ctx &c, int nb, bool with_res, float *d_state, cudaStream_t st);
+void launch_bin_count(Ctx &c, int nb, cudaStream_t st);   // per-segment scan + segment bases
+void launch_bin_sort(Ctx &c, int nb, int64_t pairs, int max_seg, cudaStream_t st);
+void launch_raster(Ctx &c, int nb, float *d_spec, bool want_heads, cudaStream_t st);
+void launch_heads(Ctx &c, int nb, uint32_t flags, double *d_pooled, double *d_rssi,
+                  int32_t *d_aoa_rc, double *d_aoa_ang, cudaStream_t st);
+void launch_heads_from_spectra(Ctx &c, int nb, const float *d_spec, cudaStream_t st);
+
+bool mlp_tc_available();
+void prepare_tc_weights(Ctx &c, const std::vector<float> &whT);
+void launch_mlp_tc(Ctx &c, int nb, cudaStream_t st);
+
+void check_cuda(cudaError_t e, const char *what);
+
+} // namespace swr

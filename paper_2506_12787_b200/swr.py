@@ -1,0 +1,288 @@
+"""Python host for libswr.so, mirroring the reference's render-path API.
+
+Reference C++ API            this module
+---------------------------------------------------   -------------------------------------------
+train::load_checkpoint(path)         training.hpp:133  load_checkpoint(path, device) -> Checkpoint
+train::normalize_position(ck, pos)   training.hpp:149  normalize_position(ck, pos) (batched too)
+train::render_at(ck, pos)            training.hpp:154  render_at(ck, pos) / render(ck, positions)
+deform::predict_residuals(...)       deform.hpp:106    predict_residuals(ck, pos01) -> Residuals
+splat::rasterize(set, res, params)   splat.hpp:152     rasterize(ck, residuals=None)
+tasks::pooled_magnitude(spectrum)    tasks.hpp:41      pooled_magnitude(ck, spectra)
+tasks::aoa_extract(spectrum)         tasks.hpp:79      aoa_extract(ck, spectra)
+
+Errors follow the reference: size/grid mismatches raise ValueError (the
+reference's std::invalid_argument), I/O and format problems RuntimeError.
+There is no CPU path: if libswr.so is missing or no sm_100 device is visible,
+every call fails loudly.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+from dataclasses import dataclass
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libswr.so")
+
+OUT_SPECTRA, OUT_POOLED, OUT_RSSI, OUT_AOA, NO_RESIDUALS = 1, 2, 4, 8, 16
+MLP_FP32, MLP_BF16X3, MLP_BF16 = 0, 1, 2
+
+_fp = C.POINTER(C.c_float)
+_dp = C.POINTER(C.c_double)
+_ip = C.POINTER(C.c_int32)
+_lib = None
+
+
+class SwrError(RuntimeError):
+    pass
+
+
+def lib():
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise ImportError(f"{LIB_PATH} not built; run `python -m paper_2506_12787_b200.build`")
+        L = C.CDLL(LIB_PATH)
+        L.swr_last_error.restype = C.c_char_p
+        L.swr_launch_count.restype = C.c_int64
+        L.swr_launch_count.argtypes = [C.c_void_p]
+        L.swr_scene_destroy.argtypes = [C.c_void_p]
+        L.swr_set_option.argtypes = [C.c_void_p, C.c_char_p, C.c_double]
+        L.swr_render.argtypes = [C.c_void_p, C.c_void_p, C.c_int64, C.c_uint32, C.c_void_p, C.c_void_p,
+                                 C.c_void_p, C.c_void_p, C.c_void_p]
+        L.swr_render_device.argtypes = [C.c_void_p, C.c_void_p, C.c_int64, C.c_uint32, C.c_void_p, C.c_void_p,
+                                        C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]
+        for fn in ("swr_predict_residuals",):
+            getattr(L, fn).argtypes = [C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p, C.c_void_p, C.c_void_p]
+        L.swr_normalize_positions.argtypes = [C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p]
+        L.swr_setup.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p,
+                                C.c_void_p, C.c_void_p, C.c_void_p]
+        L.swr_bin.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p,
+                              C.c_void_p, C.c_int64, C.c_void_p]
+        L.swr_rasterize.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p]
+        L.swr_heads.argtypes = [C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p, C.c_void_p, C.c_void_p]
+        L.swr_stage_times.argtypes = [C.c_void_p, C.c_void_p]
+        L.swr_scene_get_info.argtypes = [C.c_void_p, C.c_void_p]
+        L.swr_scene_create_wrfc.argtypes = [C.c_char_p, C.c_int, C.POINTER(C.c_void_p)]
+        L.swr_scene_create.argtypes = [C.c_int, C.c_int, C.c_int, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
+                                       C.c_int, C.c_int, C.c_int, C.c_void_p, C.c_void_p, C.c_float, C.c_int,
+                                       C.c_void_p, C.c_void_p, C.c_int, C.POINTER(C.c_void_p)]
+        _lib = L
+    return _lib
+
+
+def _check(rc: int) -> None:
+    if rc == 0:
+        return
+    msg = lib().swr_last_error().decode()
+    if rc == 1:
+        raise ValueError(msg)
+    raise SwrError(msg)
+
+
+def _p(a):
+    return None if a is None else a.ctypes.data
+
+
+def _f32(a):
+    return np.ascontiguousarray(a, dtype=np.float32)
+
+
+class _Info(C.Structure):
+    _fields_ = [("n_elevation", C.c_int), ("n_azimuth", C.c_int), ("n", C.c_int), ("width", C.c_int),
+                ("bands_center", C.c_int), ("bands_position", C.c_int), ("cutoff_radius", C.c_float),
+                ("tile", C.c_int), ("bbox_min", C.c_double * 3), ("bbox_max", C.c_double * 3),
+                ("pairs_last", C.c_int64)]
+
+
+@dataclass
+class Residuals:
+    """splat::ResidualsT layout per position (splat.hpp:61-72), batched: [B][n][...]."""
+    d_center: np.ndarray
+    d_response: np.ndarray
+    d_atten: np.ndarray
+
+
+class Checkpoint:
+    """A scene (Gaussian set + deform net + raster params + bbox) resident on one B200."""
+
+    def __init__(self, handle, keep=None):
+        self._h = C.c_void_p(handle)
+        self._keep = keep
+        info = _Info()
+        _check(lib().swr_scene_get_info(self._h, C.byref(info)))
+        self.H, self.W, self.n = info.n_elevation, info.n_azimuth, info.n
+        self.width = info.width
+        self.cutoff, self.tile = info.cutoff_radius, info.tile
+        self.bbox_min, self.bbox_max = tuple(info.bbox_min), tuple(info.bbox_max)
+        t = self.tile if self.tile >= 1 else 16
+        self.tiles = ((self.H + t - 1) // t) * ((self.W + t - 1) // t)
+
+    @classmethod
+    def from_scene(cls, sc, device: int = 0):
+        keep = [_f32(sc.center_raw), _f32(sc.cholesky), _f32(sc.atten_logit), _f32(sc.response)]
+        lw = lb = None
+        if sc.weights:
+            ws = [_f32(w) for w in sc.weights]
+            bs = [_f32(b) for b in sc.biases]
+            keep += ws + bs
+            lw = (C.c_void_p * 11)(*[w.ctypes.data for w in ws])
+            lb = (C.c_void_p * 11)(*[b.ctypes.data for b in bs])
+        bmin = np.array(sc.bbox_min, np.float64)
+        bmax = np.array(sc.bbox_max, np.float64)
+        h = C.c_void_p()
+        _check(lib().swr_scene_create(sc.H, sc.W, sc.n, *[a.ctypes.data for a in keep[:4]], sc.width, sc.bands_c,
+                                      sc.bands_p, C.cast(lw, C.c_void_p) if lw else None,
+                                      C.cast(lb, C.c_void_p) if lb else None, C.c_float(sc.cutoff), sc.tile,
+                                      bmin.ctypes.data, bmax.ctypes.data, device, C.byref(h)))
+        return cls(h.value)
+
+    def close(self):
+        if self._h:
+            lib().swr_scene_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    @property
+    def handle(self):
+        return self._h
+
+    def set_option(self, key: str, value: float) -> None:
+        _check(lib().swr_set_option(self._h, key.encode(), float(value)))
+
+    def launch_count(self) -> int:
+        return int(lib().swr_launch_count(self._h))
+
+    def pairs_last(self) -> int:
+        info = _Info()
+        _check(lib().swr_scene_get_info(self._h, C.byref(info)))
+        return int(info.pairs_last)
+
+    def stage_times(self):
+        out = np.zeros(6, np.float64)
+        _check(lib().swr_stage_times(self._h, out.ctypes.data))
+        return out
+
+
+def load_checkpoint(path: str, device: int = 0) -> Checkpoint:
+    h = C.c_void_p()
+    _check(lib().swr_scene_create_wrfc(path.encode(), device, C.byref(h)))
+    return Checkpoint(h.value)
+
+
+def normalize_position(ck: Checkpoint, pos) -> np.ndarray:
+    p = _f32(pos).reshape(-1, 3)
+    out = np.zeros_like(p)
+    _check(lib().swr_normalize_positions(ck.handle, _p(p), p.shape[0], _p(out)))
+    return out.reshape(np.shape(pos))
+
+
+def render(ck: Checkpoint, positions, spectra=True, pooled=True, rssi=False, aoa=True, residuals=True):
+    """Batched render_at + heads. Returns dict of numpy arrays."""
+    pos = _f32(positions).reshape(-1, 3)
+    B = pos.shape[0]
+    flags = (OUT_SPECTRA if spectra else 0) | (OUT_POOLED if pooled else 0) | (OUT_RSSI if rssi else 0) \
+        | (OUT_AOA if aoa else 0) | (0 if residuals else NO_RESIDUALS)
+    out = {}
+    sp = np.zeros((B, ck.H, ck.W, 2), np.float32) if spectra else None
+    pl = np.zeros(B, np.float64) if pooled else None
+    rs = np.zeros(B, np.float64) if rssi else None
+    rc = np.zeros((B, 2), np.int32) if aoa else None
+    ang = np.zeros((B, 2), np.float64) if aoa else None
+    _check(lib().swr_render(ck.handle, _p(pos), B, flags, _p(sp), _p(pl), _p(rs), _p(rc), _p(ang)))
+    for k, v in (("spectra", sp), ("pooled", pl), ("rssi", rs), ("aoa_rc", rc), ("aoa_ang", ang)):
+        if v is not None:
+            out[k] = v
+    return out
+
+
+def render_at(ck: Checkpoint, pos) -> np.ndarray:
+    """train::render_at (training.cpp:189-195): one spectrum [H][W][2]."""
+    return render(ck, np.asarray(pos, np.float32).reshape(1, 3), pooled=False, aoa=False)["spectra"][0]
+
+
+def render_device(ck: Checkpoint, d_pos_ptr: int, B: int, flags: int, d_spec=0, d_pooled=0, d_rssi=0, d_aoa_rc=0,
+                  d_aoa_ang=0, stream=0) -> None:
+    """Stream-ordered render on device pointers (e.g. torch tensors' data_ptr())."""
+    _check(lib().swr_render_device(ck.handle, d_pos_ptr, B, flags, d_spec or None, d_pooled or None,
+                                   d_rssi or None, d_aoa_rc or None, d_aoa_ang or None, stream or None))
+
+
+def predict_residuals(ck: Checkpoint, pos01) -> Residuals:
+    p = _f32(pos01).reshape(-1, 3)
+    B, n = p.shape[0], ck.n
+    dc = np.zeros((B, n, 2), np.float32)
+    dr = np.zeros((B, n, 2), np.float32)
+    da = np.zeros((B, n), np.float32)
+    _check(lib().swr_predict_residuals(ck.handle, _p(p), B, _p(dc), _p(dr), _p(da)))
+    return Residuals(dc, dr, da)
+
+
+def _res_args(res, B_hint=None):
+    if res is None:
+        return None, None, None, B_hint or 1
+    dc = _f32(res.d_center)
+    dr = _f32(res.d_response)
+    da = _f32(res.d_atten)
+    B = dc.shape[0] if dc.ndim == 3 else 1
+    return dc, dr, da, B
+
+
+def setup(ck: Checkpoint, res: Residuals | None = None, B: int = 1):
+    dc, dr, da, B = _res_args(res, B)
+    n = ck.n
+    state = np.zeros((B, n, 11), np.float32)
+    rows = np.zeros((B, n, 2), np.int32)
+    cols = np.zeros((B, n, 2), np.int32)
+    cnt = np.zeros((B, n), np.int32)
+    _check(lib().swr_setup(ck.handle, _p(dc), _p(dr), _p(da), B, _p(state), _p(rows), _p(cols), _p(cnt)))
+    return dict(state=state, rows=rows, cols=cols, tile_count=cnt)
+
+
+def bins(ck: Checkpoint, res: Residuals | None = None, B: int = 1):
+    """CSR bins per position: list of (tile_offset[tiles+1], tile_prims)."""
+    dc, dr, da, B = _res_args(res, B)
+    off = np.zeros((B, ck.tiles + 1), np.int32)
+    npairs = C.c_int64()
+    _check(lib().swr_bin(ck.handle, _p(dc), _p(dr), _p(da), B, _p(off), None, 0, C.byref(npairs)))
+    prims = np.zeros(max(npairs.value, 1), np.int32)
+    _check(lib().swr_bin(ck.handle, _p(dc), _p(dr), _p(da), B, _p(off), _p(prims), npairs.value, C.byref(npairs)))
+    out, at = [], 0
+    for b in range(B):
+        m = int(off[b, -1])
+        out.append((off[b], prims[at:at + m]))
+        at += m
+    return out
+
+
+def rasterize(ck: Checkpoint, res: Residuals | None = None, B: int = 1) -> np.ndarray:
+    dc, dr, da, B = _res_args(res, B)
+    sp = np.zeros((B, ck.H, ck.W, 2), np.float32)
+    _check(lib().swr_rasterize(ck.handle, _p(dc), _p(dr), _p(da), B, _p(sp)))
+    return sp
+
+
+def heads(ck: Checkpoint, spectra):
+    sp = _f32(spectra).reshape(-1, ck.H, ck.W, 2)
+    B = sp.shape[0]
+    pooled = np.zeros(B, np.float64)
+    rc = np.zeros((B, 2), np.int32)
+    ang = np.zeros((B, 2), np.float64)
+    _check(lib().swr_heads(ck.handle, _p(sp), B, _p(pooled), _p(rc), _p(ang)))
+    return pooled, rc, ang
+
+
+def pooled_magnitude(ck: Checkpoint, spectra) -> np.ndarray:
+    return heads(ck, spectra)[0]
+
+
+def aoa_extract(ck: Checkpoint, spectra):
+    _, rc, ang = heads(ck, spectra)
+    return rc, ang

@@ -1,0 +1,299 @@
+"""GPU parity: the CUDA path (libswr.so through its C ABI) against the oracle
+(oracle/swr_oracle.c, itself pinned to the reference) and the reference's golden
+vectors. Contract:
+
+  * render state, row/column ranges, tile counts, CSR tile bins and their
+    primitive order: bit-exact (given identical residuals);
+  * spectra: max |GPU - oracle| <= 1e-5 * max(1, peak |A|)  (the reference's own
+    float-vs-double bar, test_splat.cpp:216-253, acceptance.cpp:159-199);
+  * residuals from the FP32 MLP: max |GPU - FP64 oracle| <= 2e-6 * max(1, max|res|);
+  * pooled magnitude / RSSI: relative error <= 1e-5; AoA: same cell unless the
+    oracle's top two magnitudes are within tolerance.
+"""
+import os
+
+import numpy as np
+import pytest
+
+from conftest import ROOT
+import oracle as O
+from paper_2506_12787_b200 import swr
+from paper_2506_12787_b200.scene import Scene, make_scene, random_positions, read_wrfc, write_wrfc
+
+pytestmark = pytest.mark.gpu
+GOLD = os.path.join(ROOT, "tests", "golden")
+SPEC_TOL = 1e-5
+
+
+def spec_tol(want):
+    return SPEC_TOL * max(1.0, float(np.abs(want).max()))
+
+
+@pytest.fixture(scope="module")
+def scene2k():
+    return make_scene(2000, seed=1)
+
+
+@pytest.fixture(scope="module")
+def ck2k(scene2k):
+    return swr.Checkpoint.from_scene(scene2k)
+
+
+def residuals_for(port, positions, precise=True):
+    out = [port.predict(port.normalize(p), precise=precise) for p in positions]
+    return swr.Residuals(np.stack([o[0] for o in out]), np.stack([o[1] for o in out]), np.stack([o[2] for o in out]))
+
+
+def _res_tuple(res, b):
+    return (res.d_center[b], res.d_response[b], res.d_atten[b])
+
+
+# ---------------------------------------------------------------- setup + bins
+
+@pytest.mark.parametrize("with_res", [False, True])
+def test_setup_bit_exact(scene2k, ck2k, with_res):
+    port = O.Port(scene2k)
+    pos = random_positions(3, seed=11)
+    res = residuals_for(port, pos) if with_res else None
+    got = swr.setup(ck2k, res, B=3)
+    for b in range(3):
+        want = port.prepare(_res_tuple(res, b) if with_res else None)
+        np.testing.assert_array_equal(got["state"][b], want["state"])
+        np.testing.assert_array_equal(got["rows"][b], want["rows"])
+        np.testing.assert_array_equal(got["cols"][b], want["cols"])
+        counts = np.diff(want["tile_offset"])
+        assert got["tile_count"][b].sum() == counts.sum()
+
+
+def test_bins_bit_exact(scene2k, ck2k):
+    port = O.Port(scene2k)
+    pos = random_positions(4, seed=12)
+    res = residuals_for(port, pos)
+    got = swr.bins(ck2k, res)
+    for b in range(4):
+        want = port.prepare(_res_tuple(res, b))
+        np.testing.assert_array_equal(got[b][0], want["tile_offset"])
+        np.testing.assert_array_equal(got[b][1], want["tile_prims"])
+
+
+@pytest.mark.parametrize("cutoff,H,W,tile", [(0.0, 12, 24, 16), (3.0, 16, 32, 8), (1.0, 45, 90, 16),
+                                             (3.0, 90, 360, 16), (5.0, 30, 50, 7)])
+def test_bins_bit_exact_grids(cutoff, H, W, tile):
+    sc = make_scene(400, seed=5, H=H, W=W, width=16, cutoff=cutoff, tile=tile)
+    ck = swr.Checkpoint.from_scene(sc)
+    port = O.Port(sc)
+    res = residuals_for(port, random_positions(2, seed=2))
+    got = swr.bins(ck, res)
+    for b in range(2):
+        want = port.prepare(_res_tuple(res, b))
+        np.testing.assert_array_equal(got[b][0], want["tile_offset"])
+        np.testing.assert_array_equal(got[b][1], want["tile_prims"])
+    sp = swr.rasterize(ck, res)
+    for b in range(2):
+        want = port.rasterize(_res_tuple(res, b), precise=True)
+        assert np.abs(sp[b] - want).max() <= spec_tol(want)
+
+
+def test_edge_primitives_seam_fullcircle_offgrid_dead():
+    """Azimuth seam wrap, full-circle boxes, off-grid elevations and delta<=0."""
+    n = 64
+    rng = np.random.default_rng(3)
+    cr = rng.uniform(-2.5, 2.5, (n, 2)).astype(np.float32)
+    cr[:16, 1] = rng.choice([-4.0, 4.0, -2.6, 2.6], 16)   # az near 0 / 2pi -> wrapped spans
+    ch = np.stack([rng.uniform(0.005, 0.05, n), rng.uniform(-0.02, 0.02, n), rng.uniform(0.005, 0.05, n)],
+                  1).astype(np.float32)
+    ch[16:20, 2] = 3.0                                      # 2 h_az >= 2 pi: full circle
+    ch[20:22, 0] = 1e-7                                     # below the Cholesky floor
+    at = rng.uniform(-3, 3, n).astype(np.float32)
+    rs = rng.normal(0, 0.1, (n, 2)).astype(np.float32)
+    sc = Scene(H=90, W=360, center_raw=cr, cholesky=ch, atten_logit=at, response=rs, width=8)
+    from paper_2506_12787_b200.scene import TRUNK
+    for i, (r, c) in enumerate(sc.layer_shapes()):
+        sc.weights.append(np.zeros((r, c), np.float32))
+        sc.biases.append(np.zeros(r, np.float32))
+    ck = swr.Checkpoint.from_scene(sc)
+    port = O.Port(sc)
+    dc = rng.normal(0, 0.05, (2, n, 2)).astype(np.float32)
+    dc[0, 30:34, 0] = 2.0                                   # pushed off the elevation range
+    dr = rng.normal(0, 0.05, (2, n, 2)).astype(np.float32)
+    da = rng.normal(0, 0.3, (2, n)).astype(np.float32)
+    da[:, 40:44] = -2.0                                     # delta clamps to 0 -> never binned
+    res = swr.Residuals(dc, dr, da)
+    st = swr.setup(ck, res)
+    got = swr.bins(ck, res)
+    sp = swr.rasterize(ck, res)
+    for b in range(2):
+        want = port.prepare(_res_tuple(res, b))
+        np.testing.assert_array_equal(st["state"][b], want["state"])
+        np.testing.assert_array_equal(st["rows"][b], want["rows"])
+        np.testing.assert_array_equal(st["cols"][b], want["cols"])
+        np.testing.assert_array_equal(got[b][0], want["tile_offset"])
+        np.testing.assert_array_equal(got[b][1], want["tile_prims"])
+        ws = port.rasterize(_res_tuple(res, b), precise=True)
+        assert np.abs(sp[b] - ws).max() <= spec_tol(ws)
+
+
+# ---------------------------------------------------------------------- raster
+
+def test_raster_matches_oracle(scene2k, ck2k):
+    port = O.Port(scene2k)
+    res = residuals_for(port, random_positions(3, seed=13))
+    sp = swr.rasterize(ck2k, res)
+    for b in range(3):
+        want = port.rasterize(_res_tuple(res, b), precise=True)
+        assert np.abs(sp[b] - want).max() <= spec_tol(want)
+
+
+def test_zero_residuals_bit_identical(scene2k, ck2k):
+    n = scene2k.n
+    z = swr.Residuals(np.zeros((1, n, 2), np.float32), np.zeros((1, n, 2), np.float32), np.zeros((1, n), np.float32))
+    a = swr.rasterize(ck2k, None)
+    b = swr.rasterize(ck2k, z)
+    assert np.array_equal(a, b)
+
+
+def test_render_deterministic(scene2k, ck2k):
+    pos = random_positions(5, seed=14)
+    a = swr.render(ck2k, pos)
+    b = swr.render(ck2k, pos)
+    for k in a:
+        assert np.array_equal(a[k], b[k]), k
+
+
+def test_criterion1_instances_vs_reference():
+    c = np.load(os.path.join(GOLD, "criterion1.npz"))
+    worst = 0.0
+    for i in range(50):
+        H, W = map(int, c[f"{i}_hw"])
+        s = Scene(H=H, W=W, center_raw=c[f"{i}_cr"], cholesky=c[f"{i}_ch"], atten_logit=c[f"{i}_at"],
+                  response=c[f"{i}_rs"], cutoff=0.0)
+        ck = swr.Checkpoint.from_scene(s)
+        r = None
+        if f"{i}_dc" in c:
+            r = swr.Residuals(c[f"{i}_dc"][None], c[f"{i}_dr"][None], c[f"{i}_da"][None])
+        out = swr.rasterize(ck, r)[0]
+        worst = max(worst, float(np.abs(out - c[f"{i}_out"]).max()))
+    assert worst <= 1e-5
+
+
+# ------------------------------------------------------------------------- MLP
+
+def test_mlp_fp32_matches_fp64_oracle(scene2k, ck2k):
+    port = O.Port(scene2k)
+    pos = random_positions(3, seed=15)
+    p01 = np.stack([port.normalize(p) for p in pos])
+    got = swr.predict_residuals(ck2k, p01)
+    for b in range(3):
+        want = port.predict(p01[b], precise=True)
+        for g, w in zip((got.d_center[b], got.d_response[b], got.d_atten[b]), want):
+            assert np.abs(g - w).max() <= 2e-6 * max(1.0, float(np.abs(w).max()))
+
+
+def test_normalize_matches_reference_bits(scene2k, ck2k):
+    port = O.Port(scene2k)
+    pos = random_positions(16, seed=16)
+    got = swr.normalize_position(ck2k, pos)
+    want = np.stack([port.normalize(p) for p in pos])
+    np.testing.assert_array_equal(got, want)
+
+
+# ------------------------------------------------------------------ end to end
+
+def test_render_end_to_end(scene2k, ck2k):
+    port = O.Port(scene2k)
+    pos = random_positions(4, seed=17)
+    out = swr.render(ck2k, pos, rssi=True)
+    for b in range(4):
+        want, _ = port.render(pos[b], precise=True)
+        assert np.abs(out["spectra"][b] - want).max() <= spec_tol(want)
+        assert out["pooled"][b] == pytest.approx(port.pooled(want), rel=1e-5)
+        r, c, el, az = port.aoa(want)
+        if tuple(out["aoa_rc"][b]) != (r, c):
+            mag = np.hypot(want[..., 0].astype(np.float64), want[..., 1])
+            top = np.sort(mag.ravel())[-2:]
+            assert top[1] - top[0] <= spec_tol(want)
+        else:
+            assert out["aoa_ang"][b] == pytest.approx([el, az], abs=1e-12)
+    # GPU heads on the GPU spectra agree exactly with the oracle's heads on them
+    pooled, rc, ang = swr.heads(ck2k, out["spectra"])
+    for b in range(4):
+        assert tuple(rc[b]) == port.aoa(out["spectra"][b])[:2]
+        assert pooled[b] == pytest.approx(port.pooled(out["spectra"][b]), rel=1e-12)
+        assert tuple(out["aoa_rc"][b]) == tuple(rc[b])
+
+
+def test_golden_vectors_from_reference(tmp_path):
+    g = np.load(os.path.join(GOLD, "golden_w32.npz"))
+    ck = swr.load_checkpoint(os.path.join(GOLD, "scene_w32.wrfc"))
+    p01 = swr.normalize_position(ck, g["pos_m"])
+    np.testing.assert_array_equal(p01, g["pos01"])
+    res = swr.predict_residuals(ck, p01)
+    for got, want in ((res.d_center, g["d_center"]), (res.d_response, g["d_response"]), (res.d_atten, g["d_atten"])):
+        assert np.abs(got - want).max() <= 2e-6 * max(1.0, np.abs(want).max())
+    # state / bins from the reference's own residuals: bit-exact
+    gres = swr.Residuals(g["d_center"], g["d_response"], g["d_atten"])
+    st = swr.setup(ck, gres)
+    np.testing.assert_array_equal(st["state"], g["state"])
+    np.testing.assert_array_equal(st["rows"], g["rows"])
+    np.testing.assert_array_equal(st["cols"], g["cols"])
+    bins = swr.bins(ck, gres)
+    at = 0
+    for b in range(3):
+        m = int(g["tile_prims_len"][b])
+        np.testing.assert_array_equal(bins[b][0], g["tile_offset"][b])
+        np.testing.assert_array_equal(bins[b][1], g["tile_prims"][at:at + m])
+        at += m
+    out = swr.render(ck, g["pos_m"])
+    for b in range(3):
+        assert np.abs(out["spectra"][b] - g["spectra"][b]).max() <= spec_tol(g["spectra"][b])
+        assert tuple(out["aoa_rc"][b]) == tuple(g["aoa"][b])
+        assert out["pooled"][b] == pytest.approx(g["pooled"][b], rel=1e-5)
+    canon = swr.render(ck, g["pos_m"][:1], residuals=False)["spectra"][0]
+    assert np.abs(canon - g["canonical"]).max() <= spec_tol(g["canonical"])
+    cb = swr.bins(ck, None)
+    np.testing.assert_array_equal(cb[0][0], g["canonical_tile_offset"])
+    np.testing.assert_array_equal(cb[0][1], g["canonical_tile_prims"])
+
+
+def test_chunking_invariance(scene2k):
+    ck = swr.Checkpoint.from_scene(scene2k)
+    pos = random_positions(37, seed=18)
+    a = swr.render(ck, pos)
+    ck.set_option("chunk", 5)
+    b = swr.render(ck, pos)
+    for k in a:
+        assert np.array_equal(a[k], b[k]), k
+
+
+def test_device_api_matches_host_api(scene2k, ck2k):
+    torch = pytest.importorskip("torch")
+    pos = random_positions(6, seed=19)
+    host = swr.render(ck2k, pos, rssi=True)
+    d_pos = torch.from_numpy(pos).cuda()
+    d_spec = torch.zeros((6, ck2k.H, ck2k.W, 2), dtype=torch.float32, device="cuda")
+    d_pooled = torch.zeros(6, dtype=torch.float64, device="cuda")
+    d_rc = torch.zeros((6, 2), dtype=torch.int32, device="cuda")
+    flags = swr.OUT_SPECTRA | swr.OUT_POOLED | swr.OUT_AOA
+    stream = torch.cuda.current_stream().cuda_stream
+    swr.render_device(ck2k, d_pos.data_ptr(), 6, flags, d_spec.data_ptr(), d_pooled.data_ptr(), 0, d_rc.data_ptr(),
+                      0, stream)
+    torch.cuda.synchronize()
+    assert np.array_equal(d_spec.cpu().numpy(), host["spectra"])
+    assert np.array_equal(d_pooled.cpu().numpy(), host["pooled"])
+    assert np.array_equal(d_rc.cpu().numpy(), host["aoa_rc"])
+
+
+def test_errors_follow_reference_types(tmp_path, scene2k):
+    sc = make_scene(10, seed=1, width=8, H=16, W=32)
+    p = str(tmp_path / "s.wrfc")
+    write_wrfc(p, sc)
+    ck = swr.load_checkpoint(p)
+    with pytest.raises(ValueError):
+        ck.set_option("no_such_option", 1)
+    bad = tmp_path / "bad.wrfc"
+    bad.write_bytes(open(p, "rb").read()[:40])
+    with pytest.raises(swr.SwrError):
+        swr.load_checkpoint(str(bad))
+    with pytest.raises(ValueError):
+        swr.Checkpoint.from_scene(Scene(H=0, W=10, center_raw=sc.center_raw, cholesky=sc.cholesky,
+                                        atten_logit=sc.atten_logit, response=sc.response))
