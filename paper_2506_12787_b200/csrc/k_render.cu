@@ -593,9 +593,10 @@ __global__ void __launch_bounds__(256) raster_kernel(Grid g, SceneDev sd, const 
     const int64_t sbase = (int64_t)s * g.np;
     float acc_re = 0.f, acc_im = 0.f;
 
-    for (int64_t b0 = lb; b0 < le; b0 += 256)
+    const int batch = blockDim.x < 256 ? blockDim.x : 256;
+    for (int64_t b0 = lb; b0 < le; b0 += batch)
     {
-        const int m = (int)(le - b0 < 256 ? le - b0 : 256);
+        const int m = (int)(le - b0 < batch ? le - b0 : batch);
         __syncthreads();
         if ((int)threadIdx.x < m)
         {
