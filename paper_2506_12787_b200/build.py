@@ -31,7 +31,8 @@ HOST_CXX = "/usr/bin/g++"
 
 
 def _flags():
-    return ARCH + ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-ffp-contract=off,-O3",
+    extra = ["-DSWR_TC_DEBUG_WAITS"] if os.environ.get("SWR_DEBUG_WAITS") else []
+    return extra + ARCH + ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-ffp-contract=off,-O3",
                    "-ccbin", HOST_CXX, "-I", os.path.join(ROOT, "include"), "-I", CSRC, "-I", JSON_INC,
                    "-Xptxas", "-v" if os.environ.get("SWR_PTXAS_V") else "-O3"]
 

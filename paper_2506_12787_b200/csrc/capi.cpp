@@ -459,6 +459,75 @@ static void device_render(Ctx &c, const float *d_pos, int64_t B, uint32_t flags,
     }
 }
 
+struct Stage
+{
+    int64_t cap_b = 0;
+    size_t cap_spec = 0;
+    float *pos = nullptr;
+    float *spec[2] = {nullptr, nullptr};
+    double *pooled = nullptr, *rssi = nullptr, *ang = nullptr;
+    int32_t *rc = nullptr;
+    cudaStream_t copy = nullptr;
+    cudaEvent_t done[2]{}, freed[2]{};
+};
+
+static Stage &stage_for(Ctx &c, int64_t B, int64_t chunk, size_t spec_elems)
+{
+    static_assert(sizeof(void *) == 8, "64-bit only");
+    if (!c.host_stage)
+        c.host_stage = new Stage();
+    Stage &S = *static_cast<Stage *>(c.host_stage);
+    if (!S.copy)
+    {
+        check_cuda(cudaStreamCreateWithFlags(&S.copy, cudaStreamNonBlocking), "copy stream");
+        for (int i = 0; i < 2; i++)
+        {
+            check_cuda(cudaEventCreateWithFlags(&S.done[i], cudaEventDisableTiming), "event");
+            check_cuda(cudaEventCreateWithFlags(&S.freed[i], cudaEventDisableTiming), "event");
+        }
+    }
+    if (B > S.cap_b)
+    {
+        for (void *p : {(void *)S.pos, (void *)S.pooled, (void *)S.rssi, (void *)S.ang, (void *)S.rc})
+            dfree(c, p);
+        S.pos = dalloc<float>(c, size_t(3) * B);
+        S.pooled = dalloc<double>(c, B);
+        S.rssi = dalloc<double>(c, B);
+        S.ang = dalloc<double>(c, 2 * B);
+        S.rc = dalloc<int32_t>(c, 2 * B);
+        S.cap_b = B;
+    }
+    if (spec_elems > S.cap_spec)
+    {
+        for (auto &p : S.spec)
+        {
+            dfree(c, p);
+            p = dalloc<float>(c, spec_elems);
+        }
+        S.cap_spec = spec_elems;
+    }
+    (void)chunk;
+    return S;
+}
+
+static void free_stage(Ctx &c)
+{
+    if (!c.host_stage)
+        return;
+    Stage *S = static_cast<Stage *>(c.host_stage);
+    if (S->copy)
+    {
+        cudaStreamDestroy(S->copy);
+        for (int i = 0; i < 2; i++)
+        {
+            cudaEventDestroy(S->done[i]);
+            cudaEventDestroy(S->freed[i]);
+        }
+    }
+    delete S;
+    c.host_stage = nullptr;
+}
+
 static void upload_residuals(Ctx &c, const float *dc, const float *dr, const float *da, int64_t b0, int nb)
 {
     // reference layouts [B][n][2], [B][n][2], [B][n] -> planes [5][cap_b][np]
@@ -605,6 +674,7 @@ static void destroy(swr_ctx *h)
         cudaFree(p);
     if (h->c.w.host_pairs)
         cudaFreeHost(h->c.w.host_pairs);
+    free_stage(h->c);
     if (h->c.stream)
         cudaStreamDestroy(h->c.stream);
     delete h;
@@ -764,23 +834,17 @@ int swr_render(swr_ctx *ctx, const float *pos_m, int64_t B, uint32_t flags, floa
         const int64_t chunk = std::max<int64_t>(1, std::min<int64_t>(B, c.chunk));
         ensure_work(c, chunk);
         const size_t per = size_t(2) * c.g.H * c.g.W;
-        // device staging: positions (all), two spectrum chunk buffers, head outputs
-        float *d_pos = dalloc<float>(c, size_t(3) * B);
-        float *d_spec[2] = {nullptr, nullptr};
+        // device staging (kept in the context across calls): positions, two
+        // spectrum chunk buffers (compute of chunk i+1 overlaps the D2H of chunk i),
+        // head outputs; a copy stream and its events
         const bool want_spec = (flags & SWR_OUT_SPECTRA) && spectra;
-        if (want_spec)
-            for (auto &p : d_spec)
-                p = dalloc<float>(c, per * chunk);
-        double *d_pooled = dalloc<double>(c, B), *d_rssi = dalloc<double>(c, B), *d_ang = dalloc<double>(c, 2 * B);
-        int32_t *d_rc = dalloc<int32_t>(c, 2 * B);
-        cudaStream_t copy_st;
-        cudaEvent_t done[2], freed[2];
-        check_cuda(cudaStreamCreateWithFlags(&copy_st, cudaStreamNonBlocking), "copy stream");
-        for (int i = 0; i < 2; i++)
-        {
-            cudaEventCreateWithFlags(&done[i], cudaEventDisableTiming);
-            cudaEventCreateWithFlags(&freed[i], cudaEventDisableTiming);
-        }
+        Stage &S = stage_for(c, B, chunk, want_spec ? per * chunk : 0);
+        float *d_pos = S.pos;
+        float *d_spec[2] = {S.spec[0], S.spec[1]};
+        double *d_pooled = S.pooled, *d_rssi = S.rssi, *d_ang = S.ang;
+        int32_t *d_rc = S.rc;
+        cudaStream_t copy_st = S.copy;
+        cudaEvent_t *done = S.done, *freed = S.freed;
         check_cuda(cudaMemcpyAsync(d_pos, pos_m, sizeof(float) * 3 * B, cudaMemcpyHostToDevice, st), "H2D positions");
         const bool use_mlp = c.has_net && !(flags & SWR_NO_RESIDUALS);
         const bool heads = flags & (SWR_OUT_POOLED | SWR_OUT_RSSI | SWR_OUT_AOA);
@@ -814,15 +878,6 @@ int swr_render(swr_ctx *ctx, const float *pos_m, int64_t B, uint32_t flags, floa
             check_cuda(cudaMemcpyAsync(aoa_ang, d_ang, sizeof(double) * 2 * B, cudaMemcpyDeviceToHost, st), "D2H");
         check_cuda(cudaStreamSynchronize(st), "render");
         check_cuda(cudaStreamSynchronize(copy_st), "render copies");
-        for (int i = 0; i < 2; i++)
-        {
-            cudaEventDestroy(done[i]);
-            cudaEventDestroy(freed[i]);
-        }
-        cudaStreamDestroy(copy_st);
-        for (void *p : {(void *)d_pos, (void *)d_spec[0], (void *)d_spec[1], (void *)d_pooled, (void *)d_rssi,
-                        (void *)d_ang, (void *)d_rc})
-            dfree(c, p);
         (void)is_pinned;
     });
 }
@@ -1026,6 +1081,12 @@ int swr_heads(swr_ctx *ctx, const float *spectra, int64_t B, double *pooled, int
 }
 
 int64_t swr_launch_count(swr_ctx *ctx) { return ctx->c.launches; }
+
+// debug: clock64 trace of the tensor-core MLP (SWR_TC_DEBUG & 8), 3x8x80 stamps
+int swr_debug_mlp_trace(long long *out)
+{
+    return swr::mlp_tc_trace(out);
+}
 
 int swr_stage_times(swr_ctx *ctx, double *ms6)
 {

@@ -511,13 +511,6 @@ void launch_bin_sort(Ctx &c, int nb, int64_t pairs, int max_seg, cudaStream_t st
 
 // ------------------------------------------------------------------ raster
 
-struct __align__(16) Staged
-{
-    float el, az, k_re, k_im;
-    float i00, i01, i11, inv_l1;
-    int r0, r1, j0, len;
-};
-
 // Block reduction of (max |A|, first argmax cell, sum |A|) for the heads.
 __device__ __forceinline__ void heads_reduce(float mag, int cell, double msum, float4 *tile_part, double *tile_sum)
 {
@@ -570,99 +563,171 @@ __device__ __forceinline__ float cell_mag(float re, float im)
     return (float)__dsqrt_rn(__dadd_rn(__dmul_rn(x, x), __dmul_rn(y, y)));
 }
 
-// One CTA per (tile, position), one thread per cell. The tile's primitive
-// list (ascending primitive index, the reference's per-cell summation order)
-// is staged into shared memory in batches; a warp skips a primitive when none
-// of its cells lies inside the primitive's clipped box / marginal-row bound.
+// splat.cpp:72-82 for |x| < 3 pi (one conditional step, same result as the
+// reference's loops); larger displacements take the loop.
+__device__ __forceinline__ float wrap_fast(float x)
+{
+    if (fabsf(x) >= (float)(3 * kPi))
+        return wrap_pm_pi(x);
+    x = x >= (float)kPi ? __fsub_rn(x, (float)(2 * kPi)) : x;
+    x = x < (float)(-kPi) ? __fadd_rn(x, (float)(2 * kPi)) : x;
+    return x;
+}
+
+constexpr int kRasterWarps = 8;
+
+// One CTA per (tile, position); each warp takes every 8th (tile, primitive)
+// pair of the tile's list (ascending primitive index) and maps its lanes onto
+// the pair's clipped box only — rows [max(r0, tile), min(r1, tile)] x the one or
+// two wrapped column spans (splat.cpp:450-470) — so no lane is spent on cells
+// the reference does not evaluate. Each warp accumulates into its own
+// shared-memory copy of the tile (no atomics); the eight copies are summed in
+// fixed warp order at the end, so the result is bit-deterministic. The
+// cutoff mask uses the reference's float q (same operation order, no FMA);
+// exp(-q/2) is ex2.approx of a prescaled argument.
 __global__ void __launch_bounds__(256) raster_kernel(Grid g, SceneDev sd, const float4 *__restrict__ dyn,
                                                      const int4 *__restrict__ rng, const int64_t *__restrict__ seg,
                                                      const int *__restrict__ tile_off, const int *__restrict__ prims,
                                                      float *__restrict__ spec, float4 *__restrict__ tile_part,
                                                      double *__restrict__ tile_sum, int want_heads)
 {
-    __shared__ Staged sp[256];
+    extern __shared__ float2 acc[]; // [8][T*T]
+    __shared__ float elc[32], azc[32];
+    const int T = g.tile, TT = T * T;
     const int t = blockIdx.x, s = blockIdx.y;
-    const int tr = t / g.tw, tc = t % g.tw;
-    const int ty = threadIdx.x / g.tile, tx = threadIdx.x % g.tile;
-    const int r = tr * g.tile + ty, c = tc * g.tile + tx;
-    const bool valid = r < g.H && c < g.W && ty < g.tile;
-    const float el_r = valid ? sd.el_c[r] : 0.f;
-    const float az_c = valid ? sd.az_c[c] : 0.f;
+    const int tr0 = (t / g.tw) * T, tc0 = (t % g.tw) * T;
+    const int tr1 = min(tr0 + T, g.H) - 1, tc1 = min(tc0 + T, g.W) - 1;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    for (int i = threadIdx.x; i < kRasterWarps * TT; i += blockDim.x)
+        acc[i] = make_float2(0.f, 0.f);
+    if (threadIdx.x < T)
+    {
+        elc[threadIdx.x] = tr0 + (int)threadIdx.x <= tr1 ? sd.el_c[tr0 + threadIdx.x] : 0.f;
+        azc[threadIdx.x] = tc0 + (int)threadIdx.x <= tc1 ? sd.az_c[tc0 + threadIdx.x] : 0.f;
+    }
+    __syncthreads();
     const int *tl = tile_off + (int64_t)s * (g.tiles + 1);
     const int64_t lb = seg[s] + tl[t], le = seg[s] + tl[t + 1];
     const int64_t sbase = (int64_t)s * g.np;
-    float acc_re = 0.f, acc_im = 0.f;
+    float2 *my = acc + warp * TT;
+    const float kExp = -0.72134752044448170368f; // -0.5 * log2(e)
 
-    const int batch = blockDim.x < 256 ? blockDim.x : 256;
-    for (int64_t b0 = lb; b0 < le; b0 += batch)
+    // magic reciprocals: floor(x / d) == (x * m[d]) >> 16 for x <= 32, d <= 32
+    __shared__ uint32_t magic[33];
+    if (threadIdx.x <= 32)
+        magic[threadIdx.x] = threadIdx.x ? (65536u / threadIdx.x) + 1u : 0u;
+    __syncthreads();
+    int64_t i = lb + warp;
+    int gi = i < le ? prims[i] : 0;
+    int4 b = i < le ? rng[sbase + gi] : make_int4(0, -1, 0, 0);
+    for (; i < le; i += kRasterWarps)
     {
-        const int m = (int)(le - b0 < batch ? le - b0 : batch);
-        __syncthreads();
-        if ((int)threadIdx.x < m)
+        // prefetch the warp's next pair while this one is evaluated
+        const int64_t inext = i + kRasterWarps;
+        const int gnext = inext < le ? prims[inext] : 0;
+        const float4 d = dyn[sbase + gi];
+        const float4 sh = sd.shape[gi];
+        const int pr0 = max(b.x, tr0), pr1 = min(b.y, tr1);
+        int a0, na, nb2;
+        if (b.w >= g.W)
         {
-            const int gi = prims[b0 + threadIdx.x];
-            // (blocks wider than 256 threads stage with their first 256 lanes)
-            const float4 d = dyn[sbase + gi];
-            const float4 sh = sd.shape[gi];
-            const int4 b = rng[sbase + gi];
-            Staged st;
-            st.el = d.x;
-            st.az = d.y;
-            st.k_re = d.z;
-            st.k_im = d.w;
-            st.i00 = sh.x;
-            st.i01 = sh.y;
-            st.i11 = sh.z;
-            st.inv_l1 = sh.w;
-            st.r0 = b.x;
-            st.r1 = b.y;
-            st.j0 = b.z;
-            st.len = b.w;
-            sp[threadIdx.x] = st;
+            a0 = tc0;
+            na = tc1 - tc0 + 1;
+            nb2 = 0;
         }
-        __syncthreads();
-        for (int i = 0; i < m; i++)
+        else
         {
-            const Staged &P = sp[i];
-            int dj = c - P.j0;
-            if (dj < 0)
-                dj += g.W;
-            bool act = valid && r >= P.r0 && r <= P.r1 && (P.len >= g.W || dj < P.len);
-            const float d_el = __fsub_rn(el_r, P.el);
-            const float u0 = __fmul_rn(d_el, P.inv_l1);
-            act = act && !(__fmul_rn(u0, u0) > g.cut2);
-            if (!__any_sync(0xffffffffu, act))
-                continue;
-            const float d_az = wrap_pm_pi(__fsub_rn(az_c, P.az));
-            const float w1 = __fmul_rn(__fmul_rn(P.i11, d_az), d_az);
-            const float w2 = __fmul_rn(__fmul_rn(2.0f, P.i01), d_az);
-            const float q_c = __fmul_rn(__fmul_rn(P.i00, d_el), d_el);
-            const float q = __fadd_rn(__fadd_rn(q_c, __fmul_rn(d_el, w2)), w1);
-            if (act && q <= g.cut2)
+            const int jend = b.z + b.w - 1;
+            a0 = max(tc0, b.z);
+            const int b0 = min(tc1, min(jend, g.W - 1));
+            na = max(0, b0 - a0 + 1);
+            nb2 = jend >= g.W ? max(0, min(tc1, jend - g.W) - tc0 + 1) : 0;
+        }
+        const int ncol = na + nb2;
+        const int nrow = pr1 - pr0 + 1;
+        const int4 bnext = inext < le ? rng[sbase + gnext] : make_int4(0, -1, 0, 0);
+        if (ncol > 0 && nrow > 0)
+        {
+            const uint32_t m = magic[ncol];
+            const int rpi = (int)((32u * m) >> 16); // rows per lane sweep
+            const int lr = (int)(((uint32_t)lane * m) >> 16), lc = lane - lr * ncol;
+            const int c = lc < na ? a0 + lc : tc0 + (lc - na);
+            const bool lane_on = lr < rpi;
+            const float d_az = wrap_fast(__fsub_rn(azc[min(c - tc0, 31)], d.y));
+            const float w1 = __fmul_rn(__fmul_rn(sh.z, d_az), d_az);
+            const float w2 = __fmul_rn(__fmul_rn(2.0f, sh.y), d_az);
+            const int niter = (nrow + rpi - 1) / rpi;
+            float2 *col = my + (c - tc0);
+            for (int it = 0; it < niter; it++)
             {
-                const float e = expf(-0.5f * q);
-                acc_re = __fmaf_rn(P.k_re, e, acc_re);
-                acc_im = __fmaf_rn(P.k_im, e, acc_im);
+                const int r = pr0 + lr + it * rpi;
+                const float d_el = __fsub_rn(elc[min(r - tr0, 31)], d.x);
+                const float u0 = __fmul_rn(d_el, sh.w);
+                const float q_c = __fmul_rn(__fmul_rn(sh.x, d_el), d_el);
+                const float q = __fadd_rn(__fadd_rn(q_c, __fmul_rn(d_el, w2)), w1);
+                const bool ok = lane_on && r <= pr1 && !(__fmul_rn(u0, u0) > g.cut2) && q <= g.cut2;
+                float e;
+                asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(e) : "f"(q * kExp));
+                if (ok)
+                {
+                    float2 &cell = col[(r - tr0) * T];
+                    cell.x = __fmaf_rn(d.z, e, cell.x);
+                    cell.y = __fmaf_rn(d.w, e, cell.y);
+                }
             }
         }
+        gi = gnext;
+        b = bnext;
     }
-    if (valid && spec)
-        reinterpret_cast<float2 *>(spec)[((int64_t)s * g.H + r) * g.W + c] = make_float2(acc_re, acc_im);
-    if (want_heads)
+    __syncthreads();
+    float best = -1.0f, lsum_f = 0.f;
+    int bidx = 0x7fffffff;
+    double lsum = 0.0;
+    (void)lsum_f;
+    for (int cl = threadIdx.x; cl < TT; cl += blockDim.x)
     {
-        const float mag = valid ? cell_mag(acc_re, acc_im) : -1.0f;
-        const int cell = valid ? r * g.W + c : 0x7fffffff;
-        heads_reduce(mag, cell, valid ? (double)mag : 0.0, tile_part + (int64_t)s * g.tiles + t,
-                     tile_sum + (int64_t)s * g.tiles + t);
+        const int r = tr0 + cl / T, c = tc0 + cl % T;
+        if (r > tr1 || c > tc1)
+            continue;
+        float re = 0.f, im = 0.f;
+#pragma unroll
+        for (int w = 0; w < kRasterWarps; w++)
+        {
+            const float2 v = acc[w * TT + cl];
+            re = __fadd_rn(re, v.x);
+            im = __fadd_rn(im, v.y);
+        }
+        if (spec)
+            reinterpret_cast<float2 *>(spec)[((int64_t)s * g.H + r) * g.W + c] = make_float2(re, im);
+        if (want_heads)
+        {
+            const float m = cell_mag(re, im);
+            const int ci = r * g.W + c;
+            if (m > best || (m == best && ci < bidx))
+            {
+                best = m;
+                bidx = ci;
+            }
+            lsum += (double)m;
+        }
     }
+    if (want_heads)
+        heads_reduce(best, bidx, lsum, tile_part + (int64_t)s * g.tiles + t, tile_sum + (int64_t)s * g.tiles + t);
 }
 
 void launch_raster(Ctx &c, int nb, float *d_spec, bool want_heads, cudaStream_t st)
 {
     dim3 grid(c.g.tiles, nb);
-    const int threads = ((c.g.tile * c.g.tile + 31) / 32) * 32;
-    raster_kernel<<<grid, threads, 0, st>>>(c.g, c.s, c.w.dyn, c.w.rng, c.w.seg, c.w.tile_off, c.w.sorted, d_spec,
-                                            c.w.tile_part, c.w.tile_sum, want_heads ? 1 : 0);
+    const size_t smem = (size_t)kRasterWarps * c.g.tile * c.g.tile * sizeof(float2);
+    static size_t configured = 0;
+    if (smem > 48 * 1024 && configured < smem)
+    {
+        check_cuda(cudaFuncSetAttribute(raster_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem),
+                   "raster smem attribute");
+        configured = smem;
+    }
+    raster_kernel<<<grid, 256, smem, st>>>(c.g, c.s, c.w.dyn, c.w.rng, c.w.seg, c.w.tile_off, c.w.sorted, d_spec,
+                                          c.w.tile_part, c.w.tile_sum, want_heads ? 1 : 0);
     c.launches++;
 }
 

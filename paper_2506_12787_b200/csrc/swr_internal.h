@@ -98,6 +98,7 @@ struct Ctx
     int64_t pairs_last = 0;
     double stage_ms[6]{};
     std::vector<void *> allocs;
+    void *host_stage = nullptr; // persistent staging of the host-buffer API (capi.cpp)
 };
 
 // kernels (k_mlp.cu, k_render.cu). All launch on `st` and bump ctx.launches.
@@ -116,6 +117,7 @@ void launch_heads_from_spectra(Ctx &c, int nb, const float *d_spec, cudaStream_t
 bool mlp_tc_available();
 void prepare_tc_weights(Ctx &c, const std::vector<float> &whT);
 void launch_mlp_tc(Ctx &c, int nb, cudaStream_t st);
+int mlp_tc_trace(long long *out);
 
 void check_cuda(cudaError_t e, const char *what);
 
