@@ -617,60 +617,62 @@ __global__ void __launch_bounds__(256) raster_kernel(Grid g, SceneDev sd, const 
     if (threadIdx.x <= 32)
         magic[threadIdx.x] = threadIdx.x ? (65536u / threadIdx.x) + 1u : 0u;
     __syncthreads();
-    int64_t i = lb + warp;
-    int gi = i < le ? prims[i] : 0;
-    int4 b = i < le ? rng[sbase + gi] : make_int4(0, -1, 0, 0);
-    for (; i < le; i += kRasterWarps)
+    // 32-bit offsets inside this (position, tile) list
+    const int *plist = prims + lb;
+    const int cnt = (int)(le - lb);
+    const float4 *dyn_s = dyn + sbase;
+    const int4 *rng_s = rng + sbase;
+    int i = warp;
+    int gi = i < cnt ? plist[i] : 0;
+    int4 b = i < cnt ? rng_s[gi] : make_int4(0, -1, 0, 0);
+    const int tcw = tc1 - tc0 + 1;
+#pragma unroll 1
+    for (; i < cnt; i += kRasterWarps)
     {
         // prefetch the warp's next pair while this one is evaluated
-        const int64_t inext = i + kRasterWarps;
-        const int gnext = inext < le ? prims[inext] : 0;
-        const float4 d = dyn[sbase + gi];
-        const float4 sh = sd.shape[gi];
+        const int inext = i + kRasterWarps;
+        const int gnext = inext < cnt ? plist[inext] : 0;
         const int pr0 = max(b.x, tr0), pr1 = min(b.y, tr1);
-        int a0, na, nb2;
-        if (b.w >= g.W)
-        {
-            a0 = tc0;
-            na = tc1 - tc0 + 1;
-            nb2 = 0;
-        }
-        else
+        int a0 = tc0, na = tcw, nb2 = 0;
+        if (b.w < g.W)
         {
             const int jend = b.z + b.w - 1;
             a0 = max(tc0, b.z);
-            const int b0 = min(tc1, min(jend, g.W - 1));
-            na = max(0, b0 - a0 + 1);
+            na = max(0, min(tc1, min(jend, g.W - 1)) - a0 + 1);
             nb2 = jend >= g.W ? max(0, min(tc1, jend - g.W) - tc0 + 1) : 0;
         }
         const int ncol = na + nb2;
         const int nrow = pr1 - pr0 + 1;
-        const int4 bnext = inext < le ? rng[sbase + gnext] : make_int4(0, -1, 0, 0);
+        const float4 d = dyn_s[gi];
+        const float4 sh = sd.shape[gi];
+        const int4 bnext = inext < cnt ? rng_s[gnext] : make_int4(0, -1, 0, 0);
         if (ncol > 0 && nrow > 0)
         {
             const uint32_t m = magic[ncol];
             const int rpi = (int)((32u * m) >> 16); // rows per lane sweep
+            const int niter = (int)(((uint32_t)(nrow + rpi - 1) * magic[rpi]) >> 16);
             const int lr = (int)(((uint32_t)lane * m) >> 16), lc = lane - lr * ncol;
-            const int c = lc < na ? a0 + lc : tc0 + (lc - na);
             const bool lane_on = lr < rpi;
-            const float d_az = wrap_fast(__fsub_rn(azc[min(c - tc0, 31)], d.y));
+            const int cc = lc < na ? a0 - tc0 + lc : lc - na; // column inside the tile
+            const float d_az = wrap_fast(__fsub_rn(azc[min(cc, 31)], d.y));
             const float w1 = __fmul_rn(__fmul_rn(sh.z, d_az), d_az);
             const float w2 = __fmul_rn(__fmul_rn(2.0f, sh.y), d_az);
-            const int niter = (nrow + rpi - 1) / rpi;
-            float2 *col = my + (c - tc0);
-            for (int it = 0; it < niter; it++)
+            int rr = pr0 - tr0 + lr; // row inside the tile
+            const int rlast = pr1 - tr0;
+            float2 *col = my + cc;
+#pragma unroll 1
+            for (int it = 0; it < niter; it++, rr += rpi)
             {
-                const int r = pr0 + lr + it * rpi;
-                const float d_el = __fsub_rn(elc[min(r - tr0, 31)], d.x);
+                const float d_el = __fsub_rn(elc[min(rr, 31)], d.x);
                 const float u0 = __fmul_rn(d_el, sh.w);
                 const float q_c = __fmul_rn(__fmul_rn(sh.x, d_el), d_el);
                 const float q = __fadd_rn(__fadd_rn(q_c, __fmul_rn(d_el, w2)), w1);
-                const bool ok = lane_on && r <= pr1 && !(__fmul_rn(u0, u0) > g.cut2) && q <= g.cut2;
+                const bool ok = lane_on && rr <= rlast && !(__fmul_rn(u0, u0) > g.cut2) && q <= g.cut2;
                 float e;
                 asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(e) : "f"(q * kExp));
                 if (ok)
                 {
-                    float2 &cell = col[(r - tr0) * T];
+                    float2 &cell = col[rr * T];
                     cell.x = __fmaf_rn(d.z, e, cell.x);
                     cell.y = __fmaf_rn(d.w, e, cell.y);
                 }
