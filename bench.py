@@ -145,7 +145,7 @@ def run_reference_arm(args, scene, rank):
     value = per_step * args.steps / total
     return {"metric": "spectra/sec", "value": value, "unit": "spectra/s", "n_gpus": args.gpus, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": 1e3 * total / args.steps, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "scaling": args.scaling, "vs_baseline": None, "dtype": "f32", "data": "synthetic",
             "impl": "reference",
             "config": config_dict(args, scene),
             "cpu_baseline": {"value": value, "unit": "spectra/s", "cores": cores, "kind": "reference",
@@ -155,8 +155,11 @@ def run_reference_arm(args, scene, rank):
 
 
 def config_dict(args, scene):
-    return {"workload": f"BASELINE config 2: batched render of {args.batch} TX positions per GPU, "
-                        f"{scene.n} Gaussians, 90x360 grid, spectra + RSSI",
+    names = {2: "batched render of {b} TX positions per GPU, {n} Gaussians, 90x360 grid, spectra + RSSI",
+             3: "batched render of 65536 TX positions ({b} per GPU), {n} Gaussians, spectra + pooled",
+             4: "AoA sweep: dense 64x32x32 TX grid ({b} per GPU), {n} Gaussians, argmax only",
+             5: "large scene stress: {n} Gaussians, width-512 deformation MLP, {b} positions per GPU"}
+    return {"workload": f"BASELINE config {args.config}: " + names[args.config].format(b=args.batch, n=scene.n),
             "gaussians": scene.n, "positions_per_gpu": args.batch, "grid": [scene.H, scene.W],
             "mlp_width": scene.width, "mlp_precision": args.precision, "parallelism": f"positions sharded x{args.gpus}",
             "l2": "per-step working set (spectra 265 MB + bins ~1 GB) exceeds the 126 MB L2"}
@@ -168,9 +171,13 @@ def main():
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="native", choices=["native", "reference"])
-    ap.add_argument("--n", type=int, default=50000)
-    ap.add_argument("--batch", type=int, default=1024)
-    ap.add_argument("--precision", default=os.environ.get("SWR_BENCH_PRECISION", "fp32"),
+    ap.add_argument("--config", type=int, default=2, choices=[2, 3, 4, 5],
+                    help="BASELINE.json config: 2 = 50k Gaussians x 1024 positions/GPU, spectra+RSSI (headline); "
+                         "3 = 100k x 65536 positions sharded; 4 = AoA sweep over a 64x32x32 TX grid; "
+                         "5 = 1M Gaussians, width-512 MLP")
+    ap.add_argument("--n", type=int, default=None)
+    ap.add_argument("--batch", type=int, default=None, help="positions per GPU (configs 2 and 5)")
+    ap.add_argument("--precision", default=os.environ.get("SWR_BENCH_PRECISION", "bf16x3"),
                     choices=["fp32", "bf16x3", "bf16"])
     ap.add_argument("--chunk", type=int, default=256)
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -181,8 +188,22 @@ def main():
     local = int(os.environ.get("LOCAL_RANK", "0"))
     args.gpus = world if world > 1 else args.gpus
 
-    from paper_2506_12787_b200.scene import make_scene, random_positions
-    scene = make_scene(args.n, seed=0)
+    from paper_2506_12787_b200.scene import grid_positions, make_scene, random_positions
+    preset = {2: (50000, 1024, 156), 3: (100000, None, 156), 4: (50000, None, 156), 5: (1000000, 16, 512)}[args.config]
+    args.n = args.n or preset[0]
+    width = preset[2]
+    if args.config == 5:
+        args.precision = "fp32"  # the tensor-core MLP is built for width <= 160
+    scene = make_scene(args.n, seed=0, width=width)
+    if args.config == 3:
+        total_pos = 65536
+    elif args.config == 4:
+        total_pos = 64 * 32 * 32
+    else:
+        total_pos = None
+    if args.batch is None:
+        args.batch = preset[1] if total_pos is None else -(-total_pos // max(world, 1))
+    args.scaling = "weak" if total_pos is None else "strong"
 
     if args.impl == "reference":
         out = run_reference_arm(args, scene, rank)
@@ -201,30 +222,44 @@ def main():
     ck = swr.Checkpoint.from_scene(scene, device=local)
     ck.set_option("mlp_precision", {"fp32": 0, "bf16x3": 1, "bf16": 2}[args.precision])
     ck.set_option("chunk", args.chunk)
-    B = args.batch
+    from paper_2506_12787_b200.shard import gather_to_root, max_over_ranks, shard_range
     H, W = scene.H, scene.W
-    pos_all = random_positions(B * world, seed=1)
-    pos = np.ascontiguousarray(pos_all[rank * B:(rank + 1) * B])
+    if total_pos is None:                       # weak scaling: fixed positions per GPU
+        B = args.batch
+        pos_all = random_positions(B * world, seed=1)
+        start, count = rank * B, B
+        total = B * world
+    else:                                       # strong scaling: a fixed batch sharded over the GPUs
+        total = total_pos
+        pos_all = grid_positions(64, 32, 32) if args.config == 4 else random_positions(total, seed=1)
+        start, count = shard_range(total, world, rank)
+        B = count
+    args.batch = B
+    pos = np.ascontiguousarray(pos_all[start:start + count])
     stream = torch.cuda.Stream()
     sptr = stream.cuda_stream
     d_pos = torch.from_numpy(pos).cuda()
     d_spec = torch.empty((B, H, W, 2), dtype=torch.float32, device="cuda")
     d_pooled = torch.empty(B, dtype=torch.float64, device="cuda")
     d_rssi = torch.empty(B, dtype=torch.float64, device="cuda")
-    flags = swr.OUT_SPECTRA | swr.OUT_POOLED | swr.OUT_RSSI
-    gather = None
-    if world > 1 and rank == 0:
-        gather = [torch.empty_like(d_spec) for _ in range(world)]
+    d_rc = torch.empty((B, 2), dtype=torch.int32, device="cuda")
+    d_ang = torch.empty((B, 2), dtype=torch.float64, device="cuda")
+    aoa_only = args.config == 4
+    flags = (swr.OUT_AOA | swr.OUT_POOLED) if aoa_only else (swr.OUT_SPECTRA | swr.OUT_POOLED | swr.OUT_RSSI)
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device="cuda")
 
     def step(timed_events=None):
         with torch.cuda.stream(stream):
-            swr.render_device(ck, d_pos.data_ptr(), B, flags, d_spec.data_ptr(), d_pooled.data_ptr(),
-                              d_rssi.data_ptr(), 0, 0, sptr)
+            swr.render_device(ck, d_pos.data_ptr(), B, flags, 0 if aoa_only else d_spec.data_ptr(),
+                              d_pooled.data_ptr(), d_rssi.data_ptr(), d_rc.data_ptr(), d_ang.data_ptr(), sptr)
             if world > 1:
-                dist.gather(d_spec, gather_list=gather, dst=0)
-                dist.gather(d_rssi, gather_list=[torch.empty_like(d_rssi) for _ in range(world)] if rank == 0 else None,
-                            dst=0)
+                # the one collective: outputs gathered to rank 0 over NVLink (NCCL)
+                if aoa_only:
+                    gather_to_root(d_rc, total, world, rank)
+                    gather_to_root(d_ang, total, world, rank)
+                else:
+                    gather_to_root(d_spec, total, world, rank)
+                    gather_to_root(d_rssi, total, world, rank)
 
     for _ in range(args.warmup):
         step()
@@ -252,12 +287,8 @@ def main():
         if dist:
             dist.barrier()
     launches = ck.launch_count() - l0
-    total_ms = float(sum(ms))
-    if dist:
-        t = torch.tensor([total_ms], device="cuda", dtype=torch.float64)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        total_ms = float(t.item())
-    value = world * B * args.steps / (total_ms / 1e3)
+    total_ms = max_over_ranks(float(sum(ms)), device="cuda")
+    value = total * args.steps / (total_ms / 1e3)
 
     # ---------------- stage split + dominant kernel timing (separate pass, events per stage)
     ck.set_option("stage_timing", 1)
@@ -269,13 +300,15 @@ def main():
     # ---------------- end to end through the host C ABI (pinned host buffers)
     h_pos = torch.from_numpy(pos).pin_memory()
     h_spec = torch.empty((B, H, W, 2), dtype=torch.float32).pin_memory()
+    h_rc = torch.empty((B, 2), dtype=torch.int32).pin_memory()
+    h_ang = torch.empty((B, 2), dtype=torch.float64).pin_memory()
     h_pooled = torch.empty(B, dtype=torch.float64).pin_memory()
     h_rssi = torch.empty(B, dtype=torch.float64).pin_memory()
     L = swr.lib()
 
     def host_step():
-        swr._check(L.swr_render(ck.handle, h_pos.data_ptr(), B, flags, h_spec.data_ptr(), h_pooled.data_ptr(),
-                                h_rssi.data_ptr(), None, None))
+        swr._check(L.swr_render(ck.handle, h_pos.data_ptr(), B, flags, None if aoa_only else h_spec.data_ptr(),
+                                h_pooled.data_ptr(), h_rssi.data_ptr(), h_rc.data_ptr(), h_ang.data_ptr()))
 
     host_step()
     torch.cuda.synchronize()
@@ -284,12 +317,8 @@ def main():
     t0 = time.perf_counter()
     for _ in range(max(1, args.steps)):
         host_step()
-    e2e_s = time.perf_counter() - t0
-    if dist:
-        t = torch.tensor([e2e_s], device="cuda", dtype=torch.float64)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        e2e_s = float(t.item())
-    e2e_value = world * B * max(1, args.steps) / e2e_s
+    e2e_s = max_over_ranks(time.perf_counter() - t0, device="cuda")
+    e2e_value = total * max(1, args.steps) / e2e_s
 
     if rank != 0:
         if dist:
@@ -300,7 +329,7 @@ def main():
     d_in = 2 * (2 * scene.bands_c + 1) + 3 * (2 * scene.bands_p + 1)
     fmin, flit = mlp_flops_per_row(scene.width, d_in)
     mlp_ms = stages[1]
-    rows = scene.n * B
+    rows = scene.n * B  # rows of one rank's launch set (the stage timing is rank 0's)
     if args.precision == "fp32":
         peak = 148 * 128 * 2 * (peaks.get("sm_max_mhz", 1965.0) * 1e6) / 1e12
         bound, peak_note = "fp32", "FP32 CUDA-core peak 148 SM x 128 FMA x 2 x 1965 MHz (derived, not measured)"
@@ -310,8 +339,8 @@ def main():
     achieved = fmin * rows / (mlp_ms / 1e3) / 1e12 if mlp_ms > 0 else None
     traffic = None
     prof = os.path.join(ROOT, "profiles", "ncu_mlp_traffic.json")
-    if os.path.exists(prof):
-        try:
+    if os.path.exists(prof) and args.chunk == 256 and args.config == 2:
+        try:  # DRAM bytes of one MLP launch (256-position chunk) from the committed ncu capture
             traffic = json.load(open(prof)).get(args.precision)
         except Exception:
             traffic = None
@@ -323,18 +352,21 @@ def main():
 
     out = {
         "metric": "spectra/sec", "value": value, "unit": "spectra/s", "n_gpus": world, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": True, "scaling": "weak",
-        "vs_baseline": None, "dtype": "f32" if args.precision == "fp32" else f"f32 ({args.precision} MLP)",
+        "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": True, "scaling": args.scaling,
+        "vs_baseline": None,
+        "dtype": "f32" if args.precision == "fp32" else "f32 (MLP products as 3xBF16 split, fp32 accumulate)"
+        if args.precision == "bf16x3" else "bf16 MLP",
         "data": "synthetic (seeded scene + TX positions)",
         "config": config_dict(args, scene),
-        "roofline": {"bound": bound, "kernel": "deform MLP", "achieved": achieved, "peak": peak,
-                     "unit": "TFLOP/s", "frac": (achieved / peak) if achieved else None, "traffic": traffic,
+        "roofline": {"bound": bound, "kernel": "deform MLP (mlp_tc_kernel)", "achieved": achieved, "peak": peak,
+                     "unit": "TFLOP/s", "traffic_unit": "bytes per launch (256-position chunk)", "frac": (achieved / peak) if achieved else None, "traffic": traffic,
                      "peak_source": peak_note,
                      "flop_per_row": fmin, "flop_per_row_literal": flit, "rows_per_launch": rows},
         "stage_ms": {k: round(float(v), 3) for k, v in zip(["pos_prep", "mlp", "setup", "bin", "raster", "heads"], stages)},
         "cpu_baseline": cpu,
-        "e2e": {"value": e2e_value, "unit": "spectra/s", "h2d_bytes_per_step": int(pos.nbytes),
-                "d2h_bytes_per_step": int(B * H * W * 2 * 4 + 2 * B * 8)},
+        "e2e": {"value": e2e_value, "unit": "spectra/s", "h2d_bytes_per_step": int(pos.nbytes) * world,
+                "d2h_bytes_per_step": world * (int(B * (16 + 8)) if aoa_only else int(B * H * W * 2 * 4 + 2 * B * 8)),
+                "path": "swr_render (C ABI) with pinned host buffers per rank, H2D positions + D2H outputs inside"},
         "gpu_launches": int(launches),
         "clocks": clk.summary(),
     }
