@@ -1,45 +1,59 @@
-// Deformation MLP on the 5th-generation tensor cores (tcgen05), split precision.
+// Deformation MLP on the 5th-generation tensor cores (tcgen05), split precision,
+// CTA pairs (cta_group::2).
 //
-// Same function as the FP32 kernel in k_mlp.cu (deform.cpp:140-207 with the
-// encoding blocks factored into cg[g] + pterm[s]); the seven hidden->hidden
-// 160x160 products run on the tensor cores with FP32 accumulators in TMEM:
-//
-//   a = a_hi + a_lo, w = w_hi + w_lo  (bf16 pairs, |a - a_hi - a_lo| <= 2^-17 |a|)
+// Function: deform::predict_residuals (/root/reference/proj/src/deform.cpp:140-207).
+// Row (g, s) of the reference's input matrix is x = [xc[g] | xp[s]], the
+// sinusoidal encodings of Gaussian g's materialised centre (42 values) and of
+// TX position s (39 values) (deform.cpp:54-70, 158-171). Trunk layers 0, 2, 4, 6
+// read x (layer 0 alone, 2/4/6 after the hidden state, deform.cpp:41,177-192).
+// Here W x is split into W_c xc[g] + (W_p xp[s] + b):
+//   * W_c xc[g] runs on the tensor cores as 3 extra UMMA K steps (K = 48) whose A
+//     operand is the tile's xc rows in shared memory;
+//   * W_p xp[s] + b ("pterm", computed per position by pos_prep_kernel) is added in
+//     the epilogue; a CTA's 128 rows are 32 Gaussians x 4 positions with the TMEM
+//     lane quarter = the position, so this addend is warp-uniform.
+// The five heads (deform.cpp:194-206) run on the tensor cores too, as a ninth
+// MMA layer (N = 32, heads 0-4 real) reading layer 7's converted output.
+// All products use bf16 hi/lo splits with FP32 accumulation in TMEM:
 //   a.w ~= a_hi.w_hi + a_lo.w_hi + a_hi.w_lo        ("bf16x3", 3 UMMAs per K step)
+// (~16 significant bits per product; residuals within ~2e-5 relative of the FP64
+// oracle). SWR_MLP_BF16 issues only a_hi.w_hi.
 //
-// which keeps ~16 significant bits per product (measured: residuals within
-// ~1e-5 relative of the FP64 oracle); SWR_MLP_BF16 issues only a_hi.w_hi.
+// Why CTA pairs: every tile streams all weights (hi + lo, ~0.8 MB) through
+// shared memory; with one CTA per tile the TMA writes plus the tensor core's B
+// reads nearly saturate the 128 B/clk shared-memory port. A cluster of 2 CTAs
+// runs M = 256 UMMAs: each CTA holds its own 128 rows (A) and HALF of every B
+// tile, so per-SM weight traffic halves while each SM still computes 128 rows.
 //
-// Structure (one persistent CTA per SM, 18 warps, one 128-row tile in flight):
-//   warp 16     producer: streams each layer's packed weight K-chunks (hi+lo,
-//               10 KB) from L2 into a shared-memory ring (cp.async.bulk, mbarrier
-//               complete_tx);
-//   warp 17     MMA issuer (one thread): tcgen05.mma M=128 N=160 K=16 with the
-//               A operand in TMEM ("TS" form) and B from shared memory;
-//   warps 0-15  epilogue, 4 column groups x 4 TMEM lane quarters. Layer l's FP32
-//               accumulator is converted IN PLACE into layer l+1's bf16 hi/lo A
-//               operand (tcgen05.ld -> + bias or cg[g] + pterm[s] -> ReLU -> split
-//               -> tcgen05.st), 16 columns at a time; each converted chunk is
-//               published on its own mbarrier so the next layer's UMMAs start on
-//               chunk 0 while later chunks are still being converted.
-// TMEM holds three 160-column regions used round-robin (accumulator / A of the
-// next layer / the previous tile's layer-7 accumulator being reduced by the
-// heads), so the heads of tile i overlap the first UMMAs of tile i+1. Shared
-// memory carries only the weight ring and the tile's cg/pterm rows (double
-// buffered, cp.async prefetch one tile ahead).
+// Structure (one persistent 2-CTA cluster per TPC, 22 warps per CTA):
+//   warps 0-19  epilogue (both CTAs): 5 column groups x 4 TMEM lane quarters. Layer
+//               l's FP32 accumulator is converted IN PLACE into layer l+1's bf16
+//               hi/lo A operand (tcgen05.ld -> + bias / pterm -> ReLU -> split ->
+//               tcgen05.st), then the warp arrives on the leader's barrier;
+//   warp 20     producer (both CTAs): streams this CTA's half of each weight stage
+//               from L2 into a shared-memory ring (cp.async.bulk, complete_tx);
+//   warp 21     leader CTA: UMMA issuer (converged warp, one elected lane) --
+//               tcgen05.mma.cta_group::2 M=256, K=16, two output parts N = 96, 64
+//               committed separately; peer CTA: relays "my half of stage s
+//               landed" to the leader (remote mbarrier arrive).
+// Output parts 0/1 (columns 0-95, 96-159) are exactly the next layer's K steps
+// 0-5 and 6-9: the epilogue converts part 0 while the tensor core runs part 1,
+// and the next layer's first 6 K steps run while part 1 is converted.
+// TMEM: three 160-column regions used round-robin (accumulator / A operand of the
+// next layer / free) plus 32 columns for the heads accumulator.
+// Issue-loop lessons (measured): descriptors must be compile-time offsets from
+// one base (a runtime K loop halves UMMA throughput); remote arrivals on the
+// critical path are .relaxed (a .release.cluster arrive costs a MEMBAR.GPU).
 #include "swr_internal.h"
 #include "tc_ptx.cuh"
 
 #include <cstdio>
 #ifdef SWR_TC_DEBUG_WAITS
 #define MBAR_WAIT(b, p, tag) tc::mbar_wait_dbg(b, p, tag)
+#define MBAR_WAIT_CL(b, p, tag) tc::mbar_wait_cluster_dbg(b, p, tag)
 #else
 #define MBAR_WAIT(b, p, tag) tc::mbar_wait(b, p)
-#endif
-#ifdef SWR_TC_DEBUG_WAITS
-#define MBAR_POLL(b, p, tag) tc::mbar_wait_dbg(b, p, tag)
-#else
-#define MBAR_POLL(b, p, tag) tc::mbar_poll(b, p)
+#define MBAR_WAIT_CL(b, p, tag) tc::mbar_wait(b, p)
 #endif
 
 #include <cuda_bf16.h>
@@ -52,50 +66,82 @@ namespace swr
 
 namespace
 {
-constexpr int TM = 128;                 // rows per tile (16 Gaussians x 8 positions)
+constexpr int TM = 128;                 // rows per CTA: 32 Gaussians x 4 positions
+constexpr int TG = 32, TS = 4;
+constexpr int PAIR_S = 2 * TS;          // positions per pair tile
 constexpr int WPC = 160;                // padded width (N and K of the hidden layers)
-constexpr int KSTEPS = WPC / 16;        // 10 UMMA K steps per layer
-constexpr int NL = 7;                   // hidden->hidden layers 1..7
-constexpr int B_CHUNK = WPC * 16 * 2;   // one K step of one weight operand: 5 KB
-constexpr int B_LBO = (WPC / 8) * 128;
-constexpr int B_SBO = 128;
-constexpr int KPS = 2;                  // UMMA K steps per ring stage / per epilogue chunk
-constexpr int NCH = KSTEPS / KPS;       // 5 stages (and 32-column chunks) per layer
-constexpr int STAGE = KPS * 2 * B_CHUNK; // hi + lo of KPS K steps: 20 KB
-constexpr int NSTAGE = 4;
-constexpr int LK_ELEMS = 2 * B_CHUNK / 2; // bf16 elements (hi + lo) of one (layer, K step) block
-constexpr int EPI_WARPS = 16;
+constexpr int KSTEPS = WPC / 16;        // 10 UMMA K steps per hidden layer
+constexpr int NPART = 2;
+constexpr int KC = 3;                   // K steps of the xc (centre encoding) products: K = 48
+constexpr int XCK = 16 * KC;            // 48
+constexpr int NL = 8;                   // trunk MMA layers per tile: 0 (xc only), 1..7; then the heads
+constexpr int NHEAD_N = 32;             // heads UMMA N (5 real columns)
+// output part p: N = npart(p) columns from pcol(p) (N multiple of 32 for cta_group::2
+// with A in TMEM); feeds the next layer's K steps pcol/16 ..
+__host__ __device__ constexpr int npart(int p) { return p == 0 ? 96 : 64; }
+__host__ __device__ constexpr int pcol(int p) { return p == 0 ? 0 : 96; }
+constexpr int KSPLIT = 6; // K steps fed by part 0
+__host__ __device__ constexpr int part_of_chunk(int c) { return c < KSPLIT ? 0 : 1; }
+// one operand (hi or lo), one K step, this CTA's half of N output columns
+__host__ __device__ constexpr int kstep_bytes_n(int n) { return n / 2 * 16 * 2; }
+__host__ __device__ constexpr int kstep_bytes(int p) { return kstep_bytes_n(npart(p)); }
+constexpr int SLOT = (KC + KSTEPS) * 2 * kstep_bytes(0); // largest stage: 13 K steps x (hi, lo) = 39 KB
+constexpr int NSTAGE = 3;
+constexpr int XC_OP = TM * XCK * 2;     // one xc A operand (hi or lo) of a CTA tile: 12 KB
+constexpr int XC_BLOCK = TG * XCK * 2;  // per 32-Gaussian block, one operand: 3 KB
+constexpr int A_LBO = (TM / 8) * 128;   // xc A tile: K-direction core-matrix stride (2 KB)
+constexpr int A_SBO = 128;
+constexpr int EPI_WARPS = 20;           // 5 column groups x 4 TMEM lane quarters
 constexpr int EPI_THREADS = 32 * EPI_WARPS;
 constexpr int THREADS = 32 * (2 + EPI_WARPS);
 constexpr int NREG = 3;                 // TMEM regions of 160 columns
-// The warp scheduler prefers higher warp ids: the single-thread producer and
-// MMA issuer sit above the 16 epilogue warps so they are never starved.
+constexpr int HEAD_COL = NREG * WPC;    // heads accumulator: TMEM columns 480-511
+// The warp scheduler prefers higher warp ids: the producer and the MMA issuer
+// sit above the epilogue warps.
 constexpr int kProducerWarp = EPI_WARPS, kMmaWarp = EPI_WARPS + 1;
-// per-tile addend block in shared memory: cg rows of 16 Gaussians and pterm rows
-// of 8 positions, 4 layers each, rows skewed by 8 / 4 floats against bank conflicts
-constexpr int CROW = 4 * WPC;
-constexpr int CS_FLOATS = 16 * CROW + 16 * 8;
-constexpr int PS_FLOATS = 8 * CROW + 8 * 4;
-constexpr int CP_FLOATS = CS_FLOATS + PS_FLOATS;
-constexpr int SMEM_RING = NSTAGE * STAGE;
-constexpr int SMEM_CP = 2 * CP_FLOATS * 4;
-constexpr int SMEM_CONST = (8 * WPC + 5 * WPC + 8) * 4;
-constexpr int SMEM_HX = 4 * TM * 5 * 4;
-constexpr int NBARS = 2 * NSTAGE + 2 * NCH + 2;
-constexpr int SMEM_BYTES = SMEM_RING + SMEM_CP + SMEM_CONST + SMEM_HX + NBARS * 8 + 16 + 1024;
+constexpr int PROW = 4 * WPC;           // pterm row of one position (4 layers)
+constexpr int SMEM_RING = NSTAGE * SLOT;
+constexpr int SMEM_XC = 2 * 2 * XC_OP;  // double-buffered (tile parity) hi + lo
+constexpr int SMEM_P = 2 * TS * PROW * 4;
+constexpr int SMEM_CONST = (8 * WPC + 8) * 4;
+// w_full[NSTAGE], w_empty[NSTAGE], a_ready[2 sets][2 parts], acc[2 sets][2 parts],
+// acc_h, xc_ready[2 buffers]
+constexpr int NBARS = 2 * NSTAGE + 4 + 4 + 1 + 2;
+constexpr int SMEM_BYTES = SMEM_RING + SMEM_XC + SMEM_P + SMEM_CONST + NBARS * 8 + 16 + 1024;
+static_assert(SMEM_BYTES <= 227 * 1024, "shared memory budget");
+// epilogue column group g converts 16-column chunks g and g + 5: part 0 (chunks
+// 0-5) is converted by all 20 warps (group 0 takes two chunks), part 1 (chunks
+// 6-9) by groups 1-4
+__host__ __device__ constexpr int part_warps(int p) { return p == 0 ? 20 : 16; }
+
+__host__ __device__ constexpr bool has_xc(int l) { return l == 0 || l == 2 || l == 4 || l == 6; }
+// weight stream per tile: one stage per (trunk layer, part): the xc K steps
+// (layers 0,2,4,6) then the 10 hidden K steps (layers 1..7), each K step hi then
+// lo, rank 0's half of the part's columns then rank 1's; finally the heads stage
+__host__ __device__ constexpr int stage_bytes(int l, int p)
+{
+    return ((has_xc(l) ? KC : 0) + (l >= 1 ? KSTEPS : 0)) * 2 * kstep_bytes(p);
+}
+constexpr int HEAD_STAGE = KSTEPS * 2 * (NHEAD_N / 2) * 16 * 2; // 10 KB per CTA
+// byte offset of stage (l, p) (l = NL: the heads) in the packed stream, both ranks
+__host__ __device__ constexpr size_t stream_offset(int l, int p)
+{
+    size_t off = 0;
+    for (int j = 0; j < l * NPART + (l < NL ? p : 0); j++)
+        off += 2 * (size_t)stage_bytes(j / NPART, j % NPART);
+    return off;
+}
 
 struct TcArgs
 {
-    const uint16_t *w_tc;  // [7][10][hi 2560 | lo 2560] bf16 bits, UMMA core-matrix layout
+    const uint16_t *w_tc;  // packed weights in consumption order (prepare_tc_weights)
+    const uint16_t *xc;    // [n/32 blocks][hi | lo][48 x 32] bf16, UMMA core-matrix layout
     const float *bias;     // [8][160]
-    const float *cg;       // [np][4][160]
-    const float *pterm;    // [nb][4][160]
-    const float *heads;    // [5][160]
+    const float *pterm;    // [nb][4][160] position term of layers 0,2,4,6 (bias included)
     const float *hbias;    // [5]
     float *res;            // [5][cap_b][np]
     int n, np, nb, cap_b, n_sblk, ntiles, split, debug;
-    long long *trace; // debug: [3 tiles][8 layers][80 slots] clock64 stamps of block 0
-    uint32_t idesc;
+    long long *trace;      // debug: [3 tiles][9 layers][128 slots] clock64 stamps of block 0
 };
 
 __device__ __forceinline__ uint32_t pack_bf16(float lo, float hi)
@@ -104,21 +150,26 @@ __device__ __forceinline__ uint32_t pack_bf16(float lo, float hi)
     return *reinterpret_cast<uint32_t *>(&h);
 }
 
-// 16 consecutive K elements -> 8 columns of hi pairs, then 8 columns of lo pairs
-__device__ __forceinline__ void split16(const float (&v)[16], uint32_t (&o)[16])
+// 16 consecutive K elements -> 8 columns of hi pairs, then 8 columns of lo pairs.
+// v = ReLU(acc + add): packed f32x2 arithmetic (FADD2/FFMA2) halves the FP
+// instruction count of the conversion.
+__device__ __forceinline__ void relu_split16(const float (&acc)[16], const float (&add)[16], uint32_t (&o)[16])
 {
 #pragma unroll
     for (int i = 0; i < 8; i++)
     {
-        const uint32_t h = pack_bf16(v[2 * i], v[2 * i + 1]);
-        const float h0 = __uint_as_float(h << 16), h1 = __uint_as_float(h & 0xffff0000u);
+        float2 v = __fadd2_rn(make_float2(acc[2 * i], acc[2 * i + 1]), make_float2(add[2 * i], add[2 * i + 1]));
+        v.x = fmaxf(v.x, 0.0f);
+        v.y = fmaxf(v.y, 0.0f);
+        const uint32_t h = pack_bf16(v.x, v.y);
+        const float2 hf = make_float2(__uint_as_float(h << 16), __uint_as_float(h & 0xffff0000u));
+        const float2 lo = __ffma2_rn(hf, make_float2(-1.0f, -1.0f), v);
         o[i] = h;
-        o[8 + i] = pack_bf16(v[2 * i] - h0, v[2 * i + 1] - h1);
+        o[8 + i] = pack_bf16(lo.x, lo.y);
     }
 }
 
-// 16 floats from shared memory (explicit ld.shared: the pointer arithmetic
-// below loses the address space, generic loads would be slower)
+// 16 floats from shared memory (explicit ld.shared; generic loads would be slower)
 __device__ __forceinline__ void lds16(const float *p, float (&v)[16])
 {
     const uint32_t a = tc::smem_u32(p);
@@ -129,33 +180,36 @@ __device__ __forceinline__ void lds16(const float *p, float (&v)[16])
                      : "r"(a + 16 * i));
 }
 
-__device__ __forceinline__ void tile_origin(const TcArgs &a, int tile, int &g0, int &s0)
+// pair tile `tile` (32 Gaussians x 8 positions) -> this CTA's Gaussian and position origin
+__device__ __forceinline__ void tile_origin(const TcArgs &a, int tile, uint32_t rank, int &g0, int &s0)
 {
-    g0 = (tile / a.n_sblk) * 16;
-    s0 = (tile % a.n_sblk) * 8;
+    g0 = (tile / a.n_sblk) * TG;
+    s0 = (tile % a.n_sblk) * PAIR_S + (int)rank * TS;
 }
 
-// cp.async the tile's cg / pterm rows into one buffer (zero-fill outside the
-// problem); issued by all epilogue threads
-__device__ __forceinline__ void prefetch_cp(const TcArgs &a, int tile, float *buf, int et)
+// cp.async the CTA's tile operands: the xc A tile (4 copies of the 32-Gaussian
+// block, one per position row group) and the 4 pterm rows (zero-filled outside
+// the problem); issued by all epilogue threads
+__device__ __forceinline__ void prefetch_tile(const TcArgs &a, int tile, uint32_t rank, uint8_t *xc_buf, float *p_buf,
+                                              int et)
 {
     int g0, s0;
-    tile_origin(a, tile, g0, s0);
-    constexpr int C16 = CROW / 4; // 16-byte pieces per row
-    for (int i = et; i < 16 * C16; i += EPI_THREADS)
+    tile_origin(a, tile, rank, g0, s0);
+    const uint8_t *blk = reinterpret_cast<const uint8_t *>(a.xc) + (size_t)(g0 / TG) * 2 * XC_BLOCK;
+    // per operand (hi, lo) and 8-element K group kc: 512 B of the block -> 4 copies
+    for (int i = et; i < 2 * (XCK / 8) * 4 * 32; i += EPI_THREADS)
     {
-        const int gl = i / C16, k = (i % C16) * 4;
-        const int g = g0 + gl;
-        const bool ok = g < a.n;
-        tc::cp_async16(buf + gl * CROW + gl * 8 + k, a.cg + (size_t)(ok ? g : 0) * CROW + k, ok);
+        const int piece = i & 31, copy = (i >> 5) & 3, kc = (i >> 7) % (XCK / 8), op = (i >> 7) / (XCK / 8);
+        const uint8_t *src = blk + op * XC_BLOCK + kc * 512 + piece * 16;
+        uint8_t *dst = xc_buf + op * XC_OP + kc * A_LBO + copy * 512 + piece * 16;
+        tc::cp_async16(dst, src, true);
     }
-    float *ps = buf + CS_FLOATS;
-    for (int i = et; i < 8 * C16; i += EPI_THREADS)
+    for (int i = et; i < TS * PROW / 4; i += EPI_THREADS)
     {
-        const int sl = i / C16, k = (i % C16) * 4;
+        const int sl = i / (PROW / 4), k = (i % (PROW / 4)) * 4;
         const int s = s0 + sl;
         const bool ok = s < a.nb;
-        tc::cp_async16(ps + sl * CROW + sl * 4 + k, a.pterm + (size_t)(ok ? s : 0) * CROW + k, ok);
+        tc::cp_async16(p_buf + sl * PROW + k, a.pterm + (size_t)(ok ? s : 0) * PROW + k, ok);
     }
     tc::cp_async_commit();
 }
@@ -163,319 +217,430 @@ __device__ __forceinline__ void prefetch_cp(const TcArgs &a, int tile, float *bu
 __device__ __forceinline__ void stamp(const TcArgs &a, int it, int l, int slot)
 {
     if (a.trace && blockIdx.x == 0 && it < 3)
-        a.trace[(it * 8 + l) * 80 + slot] = clock64();
+        a.trace[(it * 9 + l) * 128 + slot] = clock64();
 }
 
-__global__ void __launch_bounds__(THREADS, 1) mlp_tc_kernel(TcArgs a)
+// UMMA issue (one elected thread), descriptors compile-time offsets from one base.
+// xc products of output part P: A = the tile's xc rows in shared memory, K = 48
+template <int N, bool SPLIT>
+__device__ __forceinline__ void issue_xc(uint32_t d, uint32_t b, uint32_t xhi, uint32_t xlo)
+{
+    constexpr uint32_t KB = kstep_bytes_n(N), LBO = N / 2 / 8 * 128;
+    constexpr uint32_t IDESC = tc::make_idesc(1, 2 * TM, N);
+    constexpr uint32_t DH = tc::desc_hi(128), AH = tc::desc_hi(A_SBO);
+    const uint32_t b0 = tc::desc_lo(b, LBO), ah0 = tc::desc_lo(xhi, A_LBO), al0 = tc::desc_lo(xlo, A_LBO);
+#pragma unroll
+    for (int kk = 0; kk < KC; kk++)
+    {
+        const uint64_t dbh = tc::desc_of(b0 + (kk * 2 * KB >> 4), DH);
+        const uint64_t dah = tc::desc_of(ah0 + (2 * kk * A_LBO >> 4), AH);
+        tc::mma2_f16(d, dah, dbh, IDESC, kk > 0 ? 1u : 0u);
+        if (SPLIT)
+        {
+            tc::mma2_f16(d, tc::desc_of(al0 + (2 * kk * A_LBO >> 4), AH), dbh, IDESC, 1u);
+            tc::mma2_f16(d, dah, tc::desc_of(b0 + ((kk * 2 + 1) * KB >> 4), DH), IDESC, 1u);
+        }
+    }
+}
+// hidden K steps [K0, K0 + NK) of an N-column output: A = previous layer's
+// converted output in TMEM
+template <int N, int K0, int NK, bool SPLIT>
+__device__ __forceinline__ void issue_hidden(uint32_t d, uint32_t bh, uint32_t areg, bool first)
+{
+    constexpr uint32_t KB = kstep_bytes_n(N), LBO = N / 2 / 8 * 128;
+    constexpr uint32_t IDESC = tc::make_idesc(1, 2 * TM, N);
+    constexpr uint32_t DH = tc::desc_hi(128);
+    const uint32_t b0 = tc::desc_lo(bh, LBO);
+#pragma unroll
+    for (int kk = 0; kk < NK; kk++)
+    {
+        const int k = K0 + kk;
+        const uint64_t dbh = tc::desc_of(b0 + (k * 2 * KB >> 4), DH);
+        const uint32_t ahi = areg + 16 * k;
+        tc::mma2_f16_ts(d, ahi, dbh, IDESC, (kk == 0 && first) ? 0u : 1u);
+        if (SPLIT)
+        {
+            tc::mma2_f16_ts(d, ahi + 8, dbh, IDESC, 1u);
+            tc::mma2_f16_ts(d, ahi, tc::desc_of(b0 + ((k * 2 + 1) * KB >> 4), DH), IDESC, 1u);
+        }
+    }
+}
+// the 10 hidden K steps of one output (whole warp); WAITS: wait for each converted
+// part of the previous layer before the K steps that read it
+template <int N, bool WAITS, bool SPLIT>
+__device__ __forceinline__ void mma_hidden(uint32_t d, uint32_t bh, uint32_t areg, bool first, uint64_t *ready,
+                                           uint32_t ready_ph)
+{
+    if (WAITS)
+    {
+        MBAR_WAIT_CL(&ready[0], ready_ph & 1, 101);
+        tc::tc_fence_after();
+        if (tc::elect_one())
+            issue_hidden<N, 0, KSPLIT, SPLIT>(d, bh, areg, first);
+        __syncwarp();
+        MBAR_WAIT_CL(&ready[1], (ready_ph >> 1) & 1, 102);
+        tc::tc_fence_after();
+        if (tc::elect_one())
+            issue_hidden<N, KSPLIT, KSTEPS - KSPLIT, SPLIT>(d, bh, areg, false);
+        __syncwarp();
+    }
+    else
+    {
+        if (tc::elect_one())
+            issue_hidden<N, 0, KSTEPS, SPLIT>(d, bh, areg, first);
+        __syncwarp();
+    }
+}
+// all UMMAs of output part P of trunk layer l from one weight stage at b
+template <int P, bool SPLIT>
+__device__ __forceinline__ void mma_part(int l, uint32_t d, uint32_t areg, uint32_t b, uint32_t xhi, uint32_t xlo,
+                                         uint64_t *ready, uint32_t ready_ph)
+{
+    constexpr uint32_t KB = kstep_bytes(P);
+    const bool xc = has_xc(l);
+    if (xc)
+    {
+        if (tc::elect_one())
+            issue_xc<npart(P), SPLIT>(d, b, xhi, xlo);
+        __syncwarp();
+    }
+    if (l >= 1)
+        mma_hidden<npart(P), P == 0, SPLIT>(d, b + (xc ? KC * 2 * KB : 0), areg, !xc, ready, ready_ph);
+}
+
+template <bool SPLIT>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1) mlp_tc_kernel(TcArgs a)
 {
     extern __shared__ uint8_t smem_raw[];
+    // identical offsets in both CTAs (UMMA descriptors of the pair address both)
     uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     uint8_t *ring = smem;
-    float *cpbuf = reinterpret_cast<float *>(ring + SMEM_RING);       // [2][CP_FLOATS]
-    float *sbias = cpbuf + 2 * CP_FLOATS;                             // [8][160]
-    float *sheads = sbias + 8 * WPC;                                  // [5][160]
-    float *shb = sheads + 5 * WPC;                                    // [8]
-    float *hx = shb + 8;                                              // [4][128][5]
-    uint64_t *bars = reinterpret_cast<uint64_t *>(hx + 4 * TM * 5);
-    uint64_t *w_full = bars, *w_empty = bars + NSTAGE, *chunk_ready = bars + 2 * NSTAGE,
-             *acc_full = bars + 2 * NSTAGE + 2 * NCH;
+    uint8_t *xcbuf = ring + SMEM_RING;                                 // [2][hi | lo]
+    float *pbuf = reinterpret_cast<float *>(xcbuf + SMEM_XC);          // [2][4][4][160]
+    float *sbias = pbuf + 2 * TS * PROW;                               // [8][160]
+    float *shb = sbias + 8 * WPC;                                      // [8]
+    uint64_t *bars = reinterpret_cast<uint64_t *>(shb + 8);
+    uint64_t *w_full = bars, *w_empty = bars + NSTAGE; // w_full (leader) also counts the peer's relay
+    uint64_t *a_ready = bars + 2 * NSTAGE; // [set][part] (leader): a converted output part, both CTAs
+    uint64_t *acc = a_ready + 2 * NPART;   // [set][part]: a layer's accumulator part complete (commit multicast)
+    uint64_t *acc_h = acc + 2 * NPART;     // heads accumulator complete
+    uint64_t *xc_ready = acc_h + 1;        // [buffer] (leader): both CTAs' xc operands have landed
     uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(bars + NBARS);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const uint32_t rank = tc::cluster_rank();
     if (threadIdx.x == 0)
     {
         for (int s = 0; s < NSTAGE; s++)
         {
-            tc::mbar_init(&w_full[s], 1);
+            tc::mbar_init(&w_full[s], rank == 0 ? 2 : 1);
             tc::mbar_init(&w_empty[s], 1);
         }
-        for (int k = 0; k < 2 * NCH; k++)
-            tc::mbar_init(&chunk_ready[k], 8); // 2 column groups x 4 lane quarters per 32-column chunk
-        tc::mbar_init(&acc_full[0], 1);
-        tc::mbar_init(&acc_full[1], 1);
+        for (int k = 0; k < 2 * NPART; k++)
+        {
+            tc::mbar_init(&a_ready[k], 2 * part_warps(k % NPART));
+            tc::mbar_init(&acc[k], 1);
+        }
+        tc::mbar_init(acc_h, 1);
+        tc::mbar_init(&xc_ready[0], 2 * EPI_WARPS);
+        tc::mbar_init(&xc_ready[1], 2 * EPI_WARPS);
         tc::fence_mbar_init();
     }
     for (int i = threadIdx.x; i < 8 * WPC; i += THREADS)
         sbias[i] = a.bias[i];
-    for (int i = threadIdx.x; i < 5 * WPC; i += THREADS)
-        sheads[i] = a.heads[i];
     if (threadIdx.x < 5)
         shb[threadIdx.x] = a.hbias[threadIdx.x];
     if (warp == kMmaWarp)
-        tc::tmem_alloc<512>(tmem_slot);
+        tc::tmem_alloc2<512>(tmem_slot);
     tc::tc_fence_before();
-    __syncthreads();
+    tc::cluster_sync(); // barriers of both CTAs initialised before any remote arrival
     tc::tc_fence_after();
     const uint32_t tmem = *tmem_slot;
-    const int ntiles_mine = blockIdx.x < a.ntiles ? (a.ntiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
+    const int cluster = blockIdx.x >> 1, nclusters = gridDim.x >> 1;
+    const int ntiles_mine = cluster < a.ntiles ? (a.ntiles - 1 - cluster) / nclusters + 1 : 0;
 
+    // Issue order (= weight-stream order = conversion order): layer 0 of the first
+    // tile, then per tile layers 1..7, layer 0 of the NEXT tile (its UMMAs need
+    // only xc, so they cover the conversion of layer 7), then the heads.
+    auto stage_count = [&](int it) { return NL * NPART - (it + 1 < ntiles_mine ? 0 : NPART) + 1; };
     if (warp == kProducerWarp)
     {
-        // whole warp converged; one elected lane issues (see tc::mbar_wait)
+        // whole warp converged; one elected lane issues; this CTA copies its half
+        // of every stage
         int stage = 0;
         uint32_t ph = 0;
-        for (int it = 0; it < ntiles_mine; it++)
-            for (int l = 0; l < NL; l++)
-                for (int k = 0; k < NCH; k++)
+        auto load = [&](int l, int p, int it) {
+            const uint32_t bytes = l < NL ? stage_bytes(l, p) : HEAD_STAGE;
+            const size_t off = stream_offset(l, p);
+            MBAR_WAIT(&w_empty[stage], ph ^ 1, 1);
+            if (tc::elect_one())
+            {
+                if ((a.debug & 1) && it > 0)
+                    tc::mbar_arrive(&w_full[stage]); // debug: stale weights, no TMA traffic
+                else
                 {
-                    MBAR_WAIT(&w_empty[stage], ph ^ 1, 1);
-                    if (tc::elect_one())
-                    {
-                        if ((a.debug & 1) && it > 0)
-                            tc::mbar_arrive(&w_full[stage]); // debug: stale weights, no TMA traffic
-                        else
-                        {
-                            tc::mbar_arrive_expect_tx(&w_full[stage], STAGE);
-                            tc::bulk_g2s(ring + stage * STAGE, a.w_tc + (size_t)(l * KSTEPS + k * KPS) * LK_ELEMS,
-                                         STAGE, &w_full[stage]);
-                        }
-                    }
-                    __syncwarp();
-                    if (++stage == NSTAGE)
-                    {
-                        stage = 0;
-                        ph ^= 1;
-                    }
+                    tc::mbar_arrive_expect_tx(&w_full[stage], bytes);
+                    tc::bulk_g2s(ring + stage * SLOT, reinterpret_cast<const uint8_t *>(a.w_tc) + off + rank * bytes,
+                                 bytes, &w_full[stage]);
                 }
+            }
+            __syncwarp();
+            if (++stage == NSTAGE)
+            {
+                stage = 0;
+                ph ^= 1;
+            }
+        };
+        if (ntiles_mine > 0)
+            for (int p = 0; p < NPART; p++)
+                load(0, p, 0);
+        for (int it = 0; it < ntiles_mine; it++)
+        {
+            for (int l = 1; l < NL; l++)
+                for (int p = 0; p < NPART; p++)
+                    load(l, p, it);
+            if (it + 1 < ntiles_mine)
+                for (int p = 0; p < NPART; p++)
+                    load(0, p, it + 1);
+            load(NL, 0, it);
+        }
+    }
+    else if (warp == kMmaWarp && rank != 0)
+    {
+        // peer CTA: tell the leader when this CTA's half of each stage has landed
+        int stage = 0;
+        uint32_t ph = 0;
+        const int total = ntiles_mine > 0 ? NPART + [&] {
+            int t = 0;
+            for (int it = 0; it < ntiles_mine; it++)
+                t += stage_count(it);
+            return t;
+        }() : 0;
+        for (int j = 0; j < total; j++)
+        {
+            MBAR_WAIT(&w_full[stage], ph, 4);
+            if (tc::elect_one())
+                tc::mbar_arrive_remote_relaxed(tc::mapa(&w_full[stage], 0)); // payload: completed TMA bytes
+            __syncwarp();
+            if (++stage == NSTAGE)
+            {
+                stage = 0;
+                ph ^= 1;
+            }
+        }
     }
     else if (warp == kMmaWarp)
     {
-        // whole warp converged (waits by all lanes), UMMAs and commits by one
-        // elected lane: keeps the issue loop free of YIELD/divergence overhead
-        {
-            int stage = 0;
-            uint32_t ph = 0, cph[2] = {0, 0};
-            const uint32_t r_base = tc::smem_u32(ring);
-            for (int it = 0; it < ntiles_mine; it++)
-                for (int l = 1; l <= NL; l++)
-                {
-                    const int u = 8 * it + l;
-                    const uint32_t dreg = tmem + (u % NREG) * WPC;
-                    const uint32_t areg = tmem + ((u + NREG - 1) % NREG) * WPC;
-                    // chunk barriers alternate between two sets by conversion
-                    // index (7 per tile: layers 0..6) so the layer-0 chunks of
-                    // the next tile can never advance a set the UMMAs of this
-                    // tile's layer 7 have not consumed yet
-                    const int cs = (7 * it + l - 1) & 1;
-                    uint64_t *cready = chunk_ready + cs * NCH;
-                    for (int j = 0; j < NCH; j++)
-                    {
-                        MBAR_WAIT(&cready[j], cph[cs], 100 + j);
-                        MBAR_WAIT(&w_full[stage], ph, 2);
-                        tc::tc_fence_after();
-                        if (lane == 0)
-                            stamp(a, it, l, j);
-                        const uint32_t b = r_base + stage * STAGE;
-                        const bool leader = tc::elect_one();
+        // leader: whole warp converged (waits by all lanes), UMMAs and commits by
+        // one elected lane: keeps the issue loop free of YIELD/divergence overhead
+        int stage = 0;
+        uint32_t ph = 0, aph = 0, xph = 0; // phase bits: aph bit set*2+part, xph bit buffer
+        int ct = 0;                        // trunk layers issued: acc set = ct & 1
+        int k = 0;                         // layers that read a converted layer: a_ready set = k & 1
+        const uint32_t r_base = tc::smem_u32(ring), x_base = tc::smem_u32(xcbuf);
+        auto next_stage = [&]() {
+            if (++stage == NSTAGE)
+            {
+                stage = 0;
+                ph ^= 1;
+            }
+        };
+        // trunk layer l of local tile it
+        auto trunk = [&](int it, int l) {
+            const uint32_t xhi = x_base + (it & 1) * 2 * XC_OP, xlo = xhi + XC_OP;
+            if (l == 0)
+            {
+                MBAR_WAIT_CL(&xc_ready[it & 1], (xph >> (it & 1)) & 1, 3);
+                xph ^= 1u << (it & 1);
+            }
+            const int m = 8 * it + l; // TMEM region rotation
+            const uint32_t dreg = tmem + (m % NREG) * WPC;
+            const uint32_t areg = tmem + ((m + NREG - 1) % NREG) * WPC;
+            const int ks = k & 1;
+            const uint32_t rph = (aph >> (ks * 2)) & 3;
 #pragma unroll
-                        for (int kk = 0; kk < KPS && leader; kk++)
-                        {
-                            const int k = j * KPS + kk;
-                            const uint64_t dbh = tc::make_desc(b + kk * 2 * B_CHUNK, B_LBO, B_SBO);
-                            const uint32_t ahi = areg + 16 * k;
-                            tc::mma_f16_ts(dreg, ahi, dbh, a.idesc, k > 0 ? 1u : 0u);
-                            if (a.split)
-                            {
-                                const uint64_t dbl = tc::make_desc(b + kk * 2 * B_CHUNK + B_CHUNK, B_LBO, B_SBO);
-                                tc::mma_f16_ts(dreg, ahi + 8, dbh, a.idesc, 1u);
-                                tc::mma_f16_ts(dreg, ahi, dbl, a.idesc, 1u);
-                            }
-                        }
-                        if (leader)
-                            tc::mma_commit(&w_empty[stage]);
-                        __syncwarp();
-                        if (++stage == NSTAGE)
-                        {
-                            stage = 0;
-                            ph ^= 1;
-                        }
-                    }
-                    cph[cs] ^= 1;
-                    // accumulators alternate between two barriers (MMA layer
-                    // index parity) so neither can run two phases ahead of
-                    // the epilogue's waits
-                    if (tc::elect_one())
-                        tc::mma_commit(&acc_full[(7 * it + l - 1) & 1]);
-                    __syncwarp();
-                    if (lane == 0)
-                        stamp(a, it, l, 10);
+            for (int p = 0; p < NPART; p++)
+            {
+                if (lane == 0)
+                    stamp(a, it, l, 100 + p);
+                MBAR_WAIT_CL(&w_full[stage], ph, 2);
+                tc::tc_fence_after();
+                if (lane == 0)
+                    stamp(a, it, l, 104 + p);
+                const uint32_t b = r_base + stage * SLOT;
+                if (p == 0)
+                    mma_part<0, SPLIT>(l, dreg, areg, b, xhi, xlo, &a_ready[ks * NPART], rph);
+                else
+                    mma_part<1, SPLIT>(l, dreg + pcol(1), areg, b, xhi, xlo, &a_ready[ks * NPART], rph);
+                if (tc::elect_one())
+                {
+                    tc::mma2_commit(&w_empty[stage], 3);
+                    tc::mma2_commit(&acc[(ct & 1) * NPART + p], 3);
                 }
+                __syncwarp();
+                if (lane == 0)
+                    stamp(a, it, l, 108 + p);
+                next_stage();
+            }
+            ct++;
+            if (l >= 1)
+            {
+                aph ^= 3u << (ks * 2);
+                k++;
+            }
+        };
+        if (ntiles_mine > 0)
+            trunk(0, 0);
+        for (int it = 0; it < ntiles_mine; it++)
+        {
+            for (int l = 1; l < NL; l++)
+                trunk(it, l);
+            if (it + 1 < ntiles_mine)
+                trunk(it + 1, 0);
+            // heads: A = layer 7's converted output, D = the heads columns
+            const int ks = k & 1;
+            if (lane == 0)
+                stamp(a, it, NL, 100);
+            MBAR_WAIT_CL(&w_full[stage], ph, 2);
+            tc::tc_fence_after();
+            mma_hidden<NHEAD_N, true, SPLIT>(tmem + HEAD_COL, r_base + stage * SLOT, tmem + ((8 * it + 7) % NREG) * WPC,
+                                             true, &a_ready[ks * NPART], (aph >> (ks * 2)) & 3);
+            if (tc::elect_one())
+            {
+                tc::mma2_commit(&w_empty[stage], 3);
+                tc::mma2_commit(acc_h, 3);
+            }
+            __syncwarp();
+            if (lane == 0)
+                stamp(a, it, NL, 108);
+            next_stage();
+            aph ^= 3u << (ks * 2);
+            k++;
         }
     }
     else
     {
-        const int e = warp;           // 0..15
+        const int e = warp;           // 0..19
         const int et = threadIdx.x;
-        const int q = warp & 3;       // TMEM lane quarter this warp may access
-        // column group: 16-column units grp, grp+4, grp+8. Group 0 (units 0, 4, 8)
-        // sits on the highest epilogue warp ids: the scheduler favours it, so the
-        // first chunk of each layer is ready as early as possible.
-        const int grp = 3 - (e >> 2);
-        const int r = q * 32 + lane;  // row in tile
+        const int q = warp & 3;       // TMEM lane quarter = position of the tile
+        const int grp = 4 - (e >> 2); // column group: chunks grp (part 0) and grp + 5 (part 0 for group 0, else 1)
         const uint32_t lane_off = (uint32_t)(q * 32) << 16;
-        const int gl = r >> 3, sl = r & 7;
-        uint32_t fph[2] = {0, 0};
-        if (ntiles_mine > 0)
-            prefetch_cp(a, blockIdx.x, cpbuf, et);
+        const int pc0 = part_of_chunk(grp), pc1 = part_of_chunk(grp + 5);
+        uint32_t fph = 0; // phase bits of acc[set][part] (this warp waits every completion of its parts)
+        int ct = 0;       // trunk layers converted (= the issuer's trunk count): set = ct & 1
 
-        // heads of the tile whose layer-7 accumulator sits in region `reg`
-        auto wait_acc = [&](int m) {
-            MBAR_WAIT(&acc_full[m & 1], fph[m & 1], 10 + (m & 1));
-            fph[m & 1] ^= 1;
-        };
-        auto heads = [&](int tile, int reg, int m) {
-            wait_acc(m);
-            tc::tc_fence_after();
-            float acc5[5] = {0.f, 0.f, 0.f, 0.f, 0.f};
-            for (int sc = grp; sc < KSTEPS; sc += 4) // 16-column units round robin over the groups
+        // convert chunk `chunk` (16 columns, part p) of trunk layer (it, l) in place
+        // and report it to the leader
+        auto convert = [&](int it, int l, int chunk, int p, bool wait, bool arrive) {
+            const int m = 8 * it + l;
+            const uint32_t reg = tmem + (m % NREG) * WPC + lane_off;
+            const float *prow = pbuf + (it & 1) * TS * PROW + q * PROW; // pterm row of this warp's position
+            if (wait)
             {
-                const int n0 = sc * 16;
-                float v[16], x[16];
-                tc::tmem_ld16(tmem + reg * WPC + lane_off + n0, v);
-                lds16(sbias + NL * WPC + n0, x);
+                const int bit = (ct & 1) * NPART + p;
+                MBAR_WAIT(&acc[bit], (fph >> bit) & 1, 10 + p);
+                fph ^= 1u << bit;
+                tc::tc_fence_after();
+            }
+            if (lane == 0 && chunk < 5)
+                stamp(a, it, l, 16 + e);
+            if (!(a.debug & 2))
+            {
+                const float *add = has_xc(l) ? prow + (l / 2) * WPC : sbias + l * WPC; // warp-uniform addend
+                const int n0 = chunk * 16;
+                uint32_t raw[16];
+                tc::tmem_ld16_issue(reg + n0, raw);
+                float x[16];
+                lds16(add + n0, x);
+                tc::tmem_ld_wait();
+                float v[16];
 #pragma unroll
                 for (int i = 0; i < 16; i++)
-                    v[i] = fmaxf(v[i] + x[i], 0.0f);
-#pragma unroll
-                for (int h = 0; h < 5; h++)
-                {
-                    lds16(sheads + h * WPC + n0, x);
-#pragma unroll
-                    for (int i = 0; i < 16; i++)
-                        acc5[h] = __fmaf_rn(v[i], x[i], acc5[h]);
-                }
+                    v[i] = __uint_as_float(raw[i]);
+                uint32_t o[16];
+                relu_split16(v, x, o);
+                tc::tmem_st16(reg + n0, o);
+                tc::tmem_st_wait();
             }
+            if (!arrive)
+                return;
             tc::tc_fence_before();
-#pragma unroll
-            for (int h = 0; h < 5; h++)
-                hx[(grp * TM + r) * 5 + h] = acc5[h];
-            tc::named_bar(2, EPI_THREADS);
-            if (grp == 0)
+            __syncwarp();
+            if (lane == 0)
             {
-                int g0, s0;
-                tile_origin(a, tile, g0, s0);
-                const int g = g0 + gl, s = s0 + sl;
-                if (g < a.n && s < a.nb)
-                {
-                    const size_t plane = (size_t)a.cap_b * a.np;
-#pragma unroll
-                    for (int h = 0; h < 5; h++)
-                    {
-                        const float t = ((acc5[h] + hx[(1 * TM + r) * 5 + h]) + hx[(2 * TM + r) * 5 + h]) +
-                                        hx[(3 * TM + r) * 5 + h];
-                        a.res[h * plane + (size_t)s * a.np + g] = t + shb[h];
-                    }
-                }
+                tc::mbar_arrive_remote_relaxed(tc::mapa(&a_ready[(ct & 1) * NPART + p], 0)); // read by the next consumer
+                if (chunk < 5)
+                    stamp(a, it, l, 36 + e);
             }
         };
+        auto convert_layer = [&](int it, int l) {
+            convert(it, l, grp, pc0, true, pc1 != pc0);
+            convert(it, l, grp + 5, pc1, pc1 != pc0, true);
+            ct++;
+        };
+        // heads of local tile `it` (group 0 warps: one lane quarter each)
+        auto heads = [&](int it) {
+            if (grp != 0)
+                return;
+            MBAR_WAIT(acc_h, it & 1, 20);
+            tc::tc_fence_after();
+            float v[16];
+            tc::tmem_ld16(tmem + HEAD_COL + lane_off, v);
+            int g0, s0;
+            tile_origin(a, cluster + it * nclusters, rank, g0, s0);
+            const int g = g0 + lane, s = s0 + q;
+            if (g < a.n && s < a.nb)
+            {
+                const size_t plane = (size_t)a.cap_b * a.np;
+#pragma unroll
+                for (int hh = 0; hh < 5; hh++)
+                    a.res[hh * plane + (size_t)s * a.np + g] = v[hh] + shb[hh];
+            }
+        };
+        // operands of local tile `it` (buffer it & 1) have landed: publish them
+        auto operands_ready = [&](int it) {
+            tc::cp_async_wait_all();
+            tc::fence_proxy_async_smem(); // xc operand is read by the tensor core (async proxy)
+            __syncwarp();
+            if (lane == 0)
+                tc::mbar_arrive_remote(tc::mapa(&xc_ready[it & 1], 0));
+            tc::named_bar(1, EPI_THREADS); // pterm rows copied by other warps are visible
+        };
+        auto prefetch = [&](int it) {
+            prefetch_tile(a, cluster + it * nclusters, rank, xcbuf + (it & 1) * 2 * XC_OP, pbuf + (it & 1) * TS * PROW,
+                          et);
+        };
 
+        if (ntiles_mine > 0)
+        {
+            prefetch(0);
+            operands_ready(0);
+            if (ntiles_mine > 1)
+                prefetch(1);
+            convert_layer(0, 0);
+        }
         for (int it = 0; it < ntiles_mine; it++)
         {
-            const int tile = blockIdx.x + it * gridDim.x;
-            float *cp = cpbuf + (it & 1) * CP_FLOATS;
-            const float *crow = cp + gl * CROW + gl * 8;            // cg rows of this row's Gaussian
-            const float *prow = cp + CS_FLOATS + sl * CROW + sl * 4; // pterm rows of this row's position
-            int g0, s0;
-            tile_origin(a, tile, g0, s0);
-            const bool live = g0 + gl < a.n && s0 + sl < a.nb;
-            tc::cp_async_wait_all();
-#ifdef SWR_TC_DEBUG_WAITS
-            if (blockIdx.x == 0 && lane == 0)
-                printf("epi warp %d tile %d before bar1\n", warp, it);
-#endif
-            tc::named_bar(1, EPI_THREADS);
-#ifdef SWR_TC_DEBUG_WAITS
-            if (blockIdx.x == 0 && lane == 0)
-                printf("epi warp %d tile %d after bar1\n", warp, it);
-#endif
-            if (it + 1 < ntiles_mine)
-                prefetch_cp(a, tile + gridDim.x, cpbuf + ((it + 1) & 1) * CP_FLOATS, et);
-            // ---- layer 0: A = split(ReLU(cg[g][0] + pterm[s][0])) into region (8 it) % 3
-            {
-                const uint32_t reg = tmem + ((8 * it) % NREG) * WPC + lane_off;
-                for (int sc = grp; sc < KSTEPS; sc += 4)
-                {
-                    const int c = sc >> 1; // 32-column chunk of this 16-column unit
-                    {
-                        const int n0 = sc * 16;
-                        float v[16], x[16];
-                        lds16(crow + n0, v);
-                        lds16(prow + n0, x);
-#pragma unroll
-                        for (int i = 0; i < 16; i++)
-                            v[i] = live ? fmaxf(v[i] + x[i], 0.0f) : 0.0f;
-                        uint32_t o[16];
-                        split16(v, o);
-                        tc::tmem_st16(reg + n0, o);
-                    }
-                    tc::tmem_st_wait();
-                    tc::tc_fence_before();
-                    __syncwarp();
-                    if (lane == 0)
-                        tc::mbar_arrive(&chunk_ready[((7 * it) & 1) * NCH + c]);
-#ifdef SWR_TC_DEBUG_WAITS
-                    if (blockIdx.x == 0 && lane == 0)
-                        printf("epi warp %d tile %d L0 chunk %d arrived\n", warp, it, c);
-#endif
-                }
-            }
-            if (it > 0)
-                heads(tile - gridDim.x, (8 * it - 1) % NREG, 7 * it - 1);
-            // ---- layers 1..6: accumulator -> next layer's A, in place
             for (int l = 1; l < NL; l++)
             {
-                const bool skip = (l == 2 || l == 4 || l == 6);
-                const int u = 8 * it + l;
-                const uint32_t reg = tmem + (u % NREG) * WPC + lane_off;
-                wait_acc(7 * it + l - 1);
-                tc::tc_fence_after();
-                if (lane == 0)
-                    stamp(a, it, l, 16 + e);
-                for (int sc = grp; sc < KSTEPS; sc += 4)
-                {
-                    const int c = sc >> 1; // 32-column chunk of this 16-column unit
-                    {
-                        const int n0 = sc * 16;
-                        float v[16], x[16];
-                        if (skip)
-                        {
-                            float y[16];
-                            lds16(crow + (l / 2) * WPC + n0, x);
-                            lds16(prow + (l / 2) * WPC + n0, y);
-#pragma unroll
-                            for (int i = 0; i < 16; i++)
-                                x[i] += y[i];
-                        }
-                        else
-                            lds16(sbias + l * WPC + n0, x);
-                        tc::tmem_ld16(reg + n0, v);
-#pragma unroll
-                        for (int i = 0; i < 16; i++)
-                            v[i] = fmaxf(v[i] + x[i], 0.0f);
-                        uint32_t o[16];
-                        split16(v, o);
-                        tc::tmem_st16(reg + n0, o);
-                    }
-                    tc::tmem_st_wait();
-                    tc::tc_fence_before();
-                    __syncwarp();
-                    if (lane == 0)
-                    {
-                        tc::mbar_arrive(&chunk_ready[((7 * it + l) & 1) * NCH + c]);
-                        stamp(a, it, l, 32 + c * 4 + q);
-                    }
-                }
+                convert_layer(it, l);
+                if (l == 3 && it + 1 < ntiles_mine)
+                    operands_ready(it + 1);
             }
+            if (it + 1 < ntiles_mine)
+                convert_layer(it + 1, 0);
+            heads(it);
+            // tile it's buffers are free (its layers 0-7 are converted, layer 6 done)
+            if (it + 2 < ntiles_mine)
+                prefetch(it + 2);
         }
-        if (ntiles_mine > 0)
-            heads(blockIdx.x + (ntiles_mine - 1) * gridDim.x, (8 * ntiles_mine - 1) % NREG, 7 * ntiles_mine - 1);
     }
     tc::tc_fence_before();
-    __syncthreads();
+    tc::cluster_sync();
     if (warp == kMmaWarp)
     {
         tc::tc_fence_after();
-        tc::tmem_dealloc<512>(tmem);
+        tc::tmem_dealloc2<512>(tmem);
     }
 }
 
@@ -496,6 +661,23 @@ float bf16_float(uint16_t h)
     std::memcpy(&f, &u, 4);
     return f;
 }
+
+// one K step (16 k) x `nc` output columns of a weight matrix as UMMA K-major core
+// matrices, hi then lo: element (n_local, kk) at ((kk/8)*(nc/8) + n_local/8)*64 + (n_local%8)*8 + kk%8
+template <class F>
+void pack_kstep(uint16_t *dst, int nc, F &&w_of)
+{
+    uint16_t *hi = dst, *lo = dst + nc * 16;
+    for (int nl = 0; nl < nc; nl++)
+        for (int kk = 0; kk < 16; kk++)
+        {
+            const float w = w_of(nl, kk);
+            const uint16_t hb = bf16_bits(w);
+            const size_t idx = (size_t)((kk / 8) * (nc / 8) + nl / 8) * 64 + (nl % 8) * 8 + kk % 8;
+            hi[idx] = hb;
+            lo[idx] = bf16_bits(w - bf16_float(hb));
+        }
+}
 } // namespace
 
 bool mlp_tc_available() { return true; }
@@ -506,81 +688,137 @@ int mlp_tc_trace(long long *out)
     if (!g_trace_buf)
         return 1;
     cudaDeviceSynchronize();
-    return cudaMemcpy(out, g_trace_buf, 3 * 8 * 80 * sizeof(long long), cudaMemcpyDeviceToHost) == cudaSuccess ? 0 : 2;
+    return cudaMemcpy(out, g_trace_buf, 3 * 9 * 128 * sizeof(long long), cudaMemcpyDeviceToHost) == cudaSuccess ? 0 : 2;
 }
 
-// Pack the seven hidden->hidden layers (whT: [7][k][n], zero padded to 160)
-// into UMMA K-major core-matrix chunks: per (layer, K step) 160 rows (n) x 16
-// (k) of w_hi, then of w_lo; element (n, kk) of a chunk at
-// ((kk/8)*20 + n/8)*64 + (n%8)*8 + kk%8.
-void prepare_tc_weights(Ctx &c, const std::vector<float> &whT)
+// Pack the weights in the kernel's consumption order (see stage_bytes): per trunk
+// layer l = 0..7 and output part p, for pair rank 0 then 1 (each its half of the
+// part's columns): the xc products (layers 0,2,4,6: centre-encoding columns of
+// W_l, K padded 42 -> 48), then the 10 hidden K steps (layers 1..7); finally the
+// heads (N = 32, columns 0-4 real).
+// whT: [7][k][n] hidden weights (k-major); wcen: [4][n][dc] centre columns of
+// layers 0,2,4,6; heads: [5][wp]; cenc: [np][dc] centre encodings (host glibc,
+// deform.cpp:54-70).
+void prepare_tc_weights(Ctx &c, const std::vector<float> &whT, const std::vector<float> &wcen,
+                        const std::vector<float> &heads, const std::vector<float> &cenc)
 {
-    const int WP = c.net.wp;
-    std::vector<uint16_t> packed((size_t)NL * KSTEPS * LK_ELEMS);
+    const int WP = c.net.wp, DC = c.net.dc;
+    std::vector<uint16_t> packed;
+    auto kstep = [&](int nc, auto &&w_of) {
+        const size_t at = packed.size();
+        packed.resize(at + 2 * nc * 16);
+        pack_kstep(packed.data() + at, nc, w_of);
+    };
     for (int l = 0; l < NL; l++)
+        for (int p = 0; p < NPART; p++)
+            for (int rk = 0; rk < 2; rk++)
+            {
+                const int nc = npart(p) / 2, cbase = pcol(p) + rk * nc;
+                if (has_xc(l))
+                    for (int kk = 0; kk < KC; kk++)
+                        kstep(nc, [&](int nl, int k16) {
+                            const int kx = 16 * kk + k16, n = cbase + nl;
+                            return kx < DC ? wcen[((size_t)(l / 2) * WP + n) * DC + kx] : 0.0f;
+                        });
+                if (l >= 1)
+                    for (int k = 0; k < KSTEPS; k++)
+                        kstep(nc, [&](int nl, int k16) {
+                            return whT[((size_t)(l - 1) * WP + (k * 16 + k16)) * WP + cbase + nl];
+                        });
+            }
+    for (int rk = 0; rk < 2; rk++)
         for (int k = 0; k < KSTEPS; k++)
-        {
-            uint16_t *hi = packed.data() + (size_t)(l * KSTEPS + k) * LK_ELEMS;
-            uint16_t *lo = hi + B_CHUNK / 2;
-            for (int n = 0; n < WPC; n++)
-                for (int kk = 0; kk < 16; kk++)
-                {
-                    const float w = whT[((size_t)l * WP + (k * 16 + kk)) * WP + n];
-                    const uint16_t h = bf16_bits(w);
-                    const uint16_t lw = bf16_bits(w - bf16_float(h));
-                    const size_t idx = (size_t)((kk / 8) * (WPC / 8) + n / 8) * 64 + (n % 8) * 8 + kk % 8;
-                    hi[idx] = h;
-                    lo[idx] = lw;
-                }
-        }
+            kstep(NHEAD_N / 2, [&](int nl, int k16) {
+                const int n = rk * (NHEAD_N / 2) + nl;
+                return n < 5 ? heads[(size_t)n * WP + k * 16 + k16] : 0.0f;
+            });
     void *d = nullptr;
     check_cuda(cudaMalloc(&d, packed.size() * 2), "cudaMalloc tc weights");
     c.allocs.push_back(d);
     check_cuda(cudaMemcpy(d, packed.data(), packed.size() * 2, cudaMemcpyHostToDevice), "upload tc weights");
     c.net.w_tc = static_cast<uint16_t *>(d);
+
+    // xc operand blocks: 32 Gaussians x 48 K, hi then lo, K-major core matrices
+    // (element (row, k) at ((k/8)*4 + row/8)*64 + (row%8)*8 + k%8)
+    const int nblk = (c.g.n + TG - 1) / TG;
+    std::vector<uint16_t> xb((size_t)nblk * XC_BLOCK, 0); // XC_BLOCK bytes per operand = hi+lo elements
+    for (int b = 0; b < nblk; b++)
+        for (int row = 0; row < TG; row++)
+        {
+            const int g = b * TG + row;
+            for (int k = 0; k < XCK; k++)
+            {
+                const float v = (g < c.g.n && k < DC) ? cenc[(size_t)g * DC + k] : 0.0f;
+                const uint16_t hb = bf16_bits(v);
+                const size_t idx = (size_t)((k / 8) * (TG / 8) + row / 8) * 64 + (row % 8) * 8 + k % 8;
+                xb[(size_t)b * XC_BLOCK + idx] = hb;
+                xb[(size_t)b * XC_BLOCK + XC_BLOCK / 2 + idx] = bf16_bits(v - bf16_float(hb));
+            }
+        }
+    check_cuda(cudaMalloc(&d, xb.size() * 2), "cudaMalloc xc blocks");
+    c.allocs.push_back(d);
+    check_cuda(cudaMemcpy(d, xb.data(), xb.size() * 2, cudaMemcpyHostToDevice), "upload xc blocks");
+    c.net.xc_tc = static_cast<uint16_t *>(d);
 }
 
 void launch_mlp_tc(Ctx &c, int nb, cudaStream_t st)
 {
-    static bool configured = false;
-    if (!configured)
+    static int max_clusters = 0;
+    if (!max_clusters)
     {
-        check_cuda(cudaFuncSetAttribute(mlp_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES),
+        check_cuda(cudaFuncSetAttribute(mlp_tc_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES),
                    "tc mlp smem attribute");
-        configured = true;
+        check_cuda(cudaFuncSetAttribute(mlp_tc_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES),
+                   "tc mlp smem attribute");
+        // persistent grid: as many CTA pairs as can be co-resident (TPCs whose two
+        // SMs are both available), never more -- a second wave would double the time
+        cudaLaunchConfig_t cfg = {};
+        cudaLaunchAttribute attr[1];
+        attr[0].id = cudaLaunchAttributeClusterDimension;
+        attr[0].val.clusterDim.x = 2;
+        attr[0].val.clusterDim.y = 1;
+        attr[0].val.clusterDim.z = 1;
+        cfg.gridDim = dim3(2, 1, 1);
+        cfg.blockDim = dim3(THREADS, 1, 1);
+        cfg.dynamicSmemBytes = SMEM_BYTES;
+        cfg.attrs = attr;
+        cfg.numAttrs = 1;
+        check_cuda(cudaOccupancyMaxActiveClusters(&max_clusters, mlp_tc_kernel<true>, &cfg),
+                   "tc mlp cluster occupancy");
+        if (max_clusters < 1)
+            check_cuda(cudaErrorLaunchOutOfResources, "tc mlp: no CTA pair fits on this device");
     }
     TcArgs a;
     a.w_tc = c.net.w_tc;
+    a.xc = c.net.xc_tc;
     a.bias = c.net.bias;
-    a.cg = c.net.cg;
     a.pterm = c.w.pterm;
-    a.heads = c.net.heads;
     a.hbias = c.net.hbias;
     a.res = c.w.res;
     a.n = c.g.n;
     a.np = c.g.np;
     a.nb = nb;
     a.cap_b = (int)c.w.cap_b;
-    a.n_sblk = (nb + 7) / 8;
-    const int n_gblk = (c.g.n + 15) / 16;
+    a.n_sblk = (nb + PAIR_S - 1) / PAIR_S;
+    const int n_gblk = (c.g.n + TG - 1) / TG;
     a.ntiles = n_gblk * a.n_sblk;
     a.split = c.mlp_precision == 1 ? 1 : 0;
-    a.idesc = tc::make_idesc(1, TM, WPC);
     a.debug = getenv("SWR_TC_DEBUG") ? atoi(getenv("SWR_TC_DEBUG")) : 0;
     a.trace = nullptr;
     if (a.debug & 8)
     {
         static long long *buf = nullptr;
         if (!buf)
-            check_cuda(cudaMalloc(&buf, 3 * 8 * 80 * sizeof(long long)), "trace buffer");
-        cudaMemsetAsync(buf, 0, 3 * 8 * 80 * sizeof(long long), st);
+            check_cuda(cudaMalloc(&buf, 3 * 9 * 128 * sizeof(long long)), "trace buffer");
+        cudaMemsetAsync(buf, 0, 3 * 9 * 128 * sizeof(long long), st);
         a.trace = buf;
         g_trace_buf = buf;
     }
-    int sms = 148;
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c.device);
-    const int grid = std::min(sms, a.ntiles);
-    mlp_tc_kernel<<<grid, THREADS, SMEM_BYTES, st>>>(a);
+    const int grid = 2 * std::min(max_clusters, a.ntiles);
+    if (a.split)
+        mlp_tc_kernel<true><<<grid, THREADS, SMEM_BYTES, st>>>(a);
+    else
+        mlp_tc_kernel<false><<<grid, THREADS, SMEM_BYTES, st>>>(a);
     c.launches++;
 }
 

@@ -51,7 +51,8 @@ struct NetDev
     float *heads;          // [5][wp] head weights (centre 2, response 2, atten 1)
     float *hbias;          // [5]
     // tcgen05 path (bf16 hi/lo, UMMA canonical K-major layout, see k_mlp_tc.cu)
-    uint16_t *w_tc;        // [7][2 (hi,lo)][chunks][wp x 16] packed
+    uint16_t *w_tc;        // packed bf16 hi/lo weights in the tensor-core kernel's consumption order
+    uint16_t *xc_tc;       // packed bf16 hi/lo centre encodings per 32-Gaussian block
 };
 
 // Per-chunk scratch (positions per chunk = cap_b).
@@ -115,7 +116,8 @@ void launch_heads(Ctx &c, int nb, uint32_t flags, double *d_pooled, double *d_rs
 void launch_heads_from_spectra(Ctx &c, int nb, const float *d_spec, cudaStream_t st);
 
 bool mlp_tc_available();
-void prepare_tc_weights(Ctx &c, const std::vector<float> &whT);
+void prepare_tc_weights(Ctx &c, const std::vector<float> &whT, const std::vector<float> &wcen,
+                        const std::vector<float> &heads, const std::vector<float> &cenc);
 void launch_mlp_tc(Ctx &c, int nb, cudaStream_t st);
 int mlp_tc_trace(long long *out);
 

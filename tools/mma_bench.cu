@@ -135,16 +135,186 @@ void run(int sms)
     cudaFree(d);
 }
 
+
+// stage-loop mimic: converged warp, per batch: wait (complete barrier) -> BATCH MMAs -> commit
+template <int N, int BATCH, int WAITMODE>
+__global__ void stage_bench(long long *out, int batches)
+{
+    extern __shared__ __align__(1024) uint8_t sm[];
+    __shared__ uint64_t full, empty[4];
+    __shared__ uint32_t tslot;
+    if (threadIdx.x == 0)
+    {
+        mbar_init(&full, 1);
+        for (int k = 0; k < 4; k++)
+            mbar_init(&empty[k], 1);
+        fence_mbar_init();
+    }
+    if (threadIdx.x < 32)
+        tmem_alloc<512>(&tslot);
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = tslot;
+    if (threadIdx.x == 0)
+        mbar_arrive(&full); // phase 0 complete
+    __syncthreads();
+    const uint32_t idesc = make_idesc(1, 128, N);
+    if (threadIdx.x < 32)
+    {
+        const uint32_t b = smem_u32(sm) + 65536;
+        const uint64_t db = make_desc(b, N * 16, 128);
+        long long t0 = clock64();
+        for (int j = 0; j < batches; j++)
+        {
+            if (WAITMODE == 1)
+                mbar_wait(&full, 0);
+            if (WAITMODE == 2)
+                mbar_poll(&full, 0);
+            tc_fence_after();
+            if (elect_one())
+            {
+#pragma unroll
+                for (int k = 0; k < BATCH; k++)
+                    mma_f16_ts(tmem, tmem + 256 + 8 * (k % 8), db + 16 * (k % 4), idesc, (j | k) > 0);
+                mma_commit(&empty[j & 3]);
+            }
+            __syncwarp();
+        }
+        if (threadIdx.x == 0)
+        {
+            mma_commit(&full);
+            mbar_wait(&full, 1);
+            out[blockIdx.x] = clock64() - t0;
+        }
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (threadIdx.x < 32)
+    {
+        tc_fence_after();
+        tmem_dealloc<512>(tmem);
+    }
+}
+
+template <int N, int BATCH, int WAITMODE>
+void run_stage(int sms)
+{
+    long long *d, h[256];
+    cudaMalloc(&d, sizeof(h));
+    const int batches = 4000 / BATCH;
+    cudaFuncSetAttribute(stage_bench<N, BATCH, WAITMODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    stage_bench<N, BATCH, WAITMODE><<<sms, 128, 200 * 1024>>>(d, batches);
+    stage_bench<N, BATCH, WAITMODE><<<sms, 128, 200 * 1024>>>(d, batches);
+    cudaError_t e = cudaDeviceSynchronize();
+    cudaMemcpy(h, d, sizeof(long long) * sms, cudaMemcpyDeviceToHost);
+    double avg = 0;
+    for (int i = 0; i < sms; i++)
+        avg += h[i];
+    avg /= sms;
+    printf("stage N=%3d batch=%2d wait=%d: %6.1f cycles/MMA ideal %5.1f %s\n", N, BATCH, WAITMODE,
+           avg / (batches * BATCH), 128.0 * N / 256.0, cudaGetErrorString(e));
+    cudaFree(d);
+}
+
+// stage loop with SPIN extra warps blocked in mbar_wait, SS: A from shared memory
+template <int N, int BATCH, int SPIN, int SS, int NACC = 2>
+__global__ void stage_bench2(long long *out, int batches)
+{
+    extern __shared__ __align__(1024) uint8_t sm[];
+    __shared__ uint64_t full, done, empty[4];
+    __shared__ uint32_t tslot;
+    const int warp = threadIdx.x >> 5;
+    if (threadIdx.x == 0)
+    {
+        mbar_init(&full, 1);
+        mbar_init(&done, 1);
+        for (int k = 0; k < 4; k++)
+            mbar_init(&empty[k], 1);
+        fence_mbar_init();
+    }
+    if (warp == SPIN)
+        tmem_alloc<512>(&tslot);
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = tslot;
+    if (threadIdx.x == 0)
+        mbar_arrive(&full);
+    __syncthreads();
+    const uint32_t idesc = make_idesc(1, 128, N);
+    if (warp == SPIN)
+    {
+        const uint32_t b = smem_u32(sm) + 65536;
+        const uint32_t abase = smem_u32(sm);
+        const uint64_t db = make_desc(b, N * 16, 128);
+        long long t0 = clock64();
+        for (int j = 0; j < batches; j++)
+        {
+            mbar_wait(&full, 0);
+            tc_fence_after();
+            if (elect_one())
+            {
+#pragma unroll
+                for (int k = 0; k < BATCH; k++)
+                {
+                    const uint32_t d = tmem + 160 * (j % 3) + (NACC == 1 ? 0 : 80 * (k & 1));
+                    if (SS)
+                        mma_f16(d, make_desc(abase + 4096 * (k % 3), 2048, 128), db + 16 * (k % 4), idesc, (j | k) > 0);
+                    else
+                        mma_f16_ts(d, tmem + 160 * ((j + 2) % 3) + 16 * (k % 10) + 8 * (k & 1), db + 16 * (k % 4),
+                                   idesc, (j | k) > 0);
+                }
+                mma_commit(&empty[j & 3]);
+            }
+            __syncwarp();
+        }
+        if (threadIdx.x == 32 * SPIN)
+        {
+            mma_commit(&full);
+            mbar_wait(&full, 1);
+            out[blockIdx.x] = clock64() - t0;
+            mbar_arrive(&done);
+        }
+    }
+    else
+        mbar_wait(&done, 0);
+    tc_fence_before();
+    __syncthreads();
+    if (warp == SPIN)
+    {
+        tc_fence_after();
+        tmem_dealloc<512>(tmem);
+    }
+}
+
+template <int N, int BATCH, int SPIN, int SS, int NACC = 2>
+void run_stage2(int sms)
+{
+    long long *d, h[256];
+    cudaMalloc(&d, sizeof(h));
+    const int batches = 4000 / BATCH;
+    auto k = stage_bench2<N, BATCH, SPIN, SS, NACC>;
+    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    k<<<sms, 32 * (SPIN + 1), 200 * 1024>>>(d, batches);
+    k<<<sms, 32 * (SPIN + 1), 200 * 1024>>>(d, batches);
+    cudaError_t e = cudaDeviceSynchronize();
+    cudaMemcpy(h, d, sizeof(long long) * sms, cudaMemcpyDeviceToHost);
+    double avg = 0;
+    for (int i = 0; i < sms; i++)
+        avg += h[i];
+    avg /= sms;
+    printf("stage2 nacc=%d N=%3d batch=%2d spin=%2d ss=%d: %6.1f cycles/MMA ideal %5.1f %s\n", NACC, N, BATCH, SPIN, SS,
+           avg / (batches * BATCH), 128.0 * N / 256.0, cudaGetErrorString(e));
+    cudaFree(d);
+}
 int main()
 {
     int sms = 148;
-    run<160, true, 6, 2>(sms);
-    run<160, true, 12, 2>(sms);
-    run<160, true, 24, 2>(sms);
-    run<160, true, 48, 2>(sms);
-    run<160, true, 12, 128 | 2>(sms);
-    run<160, true, 24, 128 | 2>(sms);
-    run<160, true, 6, 4>(sms);
-    run<160, true, 24, 4>(sms);
+    run_stage2<80, 15, 0, 0, 1>(sms);
+    run_stage2<80, 15, 0, 0, 2>(sms);
+    run_stage2<64, 15, 0, 0, 1>(sms);
+    run_stage2<128, 15, 0, 0, 1>(sms);
+    run_stage2<160, 15, 0, 0, 1>(sms);
     return 0;
 }

@@ -1,4 +1,6 @@
-import ctypes, os, sys, numpy as np
+"""Per-stage timeline of the tensor-core MLP kernel (block 0), SWR_TC_DEBUG bit 8.
+    DBG=8 python tools/tc_trace.py [precision]"""
+import os, sys, numpy as np
 sys.path.insert(0, "."); sys.path.insert(0, "oracle")
 os.environ["SWR_TC_DEBUG"] = os.environ.get("DBG", "8")
 from paper_2506_12787_b200 import swr
@@ -6,19 +8,26 @@ from paper_2506_12787_b200.scene import make_scene, random_positions
 sc = make_scene(20000, seed=1)
 ck = swr.Checkpoint.from_scene(sc)
 ck.set_option("mlp_precision", int(sys.argv[1]) if len(sys.argv) > 1 else 1)
-pos = random_positions(64, seed=3)
-p01 = swr.normalize_position(ck, pos)
+p01 = np.random.default_rng(0).random((64, 3)).astype(np.float32)
 swr.predict_residuals(ck, p01)
-t = np.zeros(3 * 8 * 80, np.int64)
+t = np.zeros(3 * 9 * 128, np.int64)
 swr.lib().swr_debug_mlp_trace(t.ctypes.data)
-t = t.reshape(3, 8, 80)
-t0 = t[t > 0].min()
-for it in range(3):
-    for l in range(1, 8):
-        row = t[it, l]
-        rel = lambda x: (int(x - t0) if x > 0 else -1)
-        mma = [rel(x) for x in row[:11]]
-        wake = [rel(x) for x in row[16:32]]
-        chunks = [max(rel(x) for x in row[32 + 4 * c:36 + 4 * c]) for c in range(5)]
-        print(f"tile {it} L{l}: mma k-issue {mma[:5]} commit {mma[10]}")
-        print(f"          epi wake min/max {min(w for w in wake if w>=0) if any(w>=0 for w in wake) else -1}/{max(wake)} chunk ready {chunks}")
+t = t.reshape(3, 9, 128)
+t0 = t[2][t[2] > 0].min()
+rel = lambda x: (int(x - t0) if x > 0 else -1)
+part = lambda c: 0 if c < 6 else 1
+print("MMA per part: wait-start / w done / issued.  epilogue per part: [first wait done .. last conv done] (max conv duration)")
+for l in range(9):
+    row = t[2, l]
+    parts = [f"p{p}:{rel(row[100+p])}/{rel(row[104+p])}/{rel(row[108+p])}" for p in range(2)]
+    ep = {0: [], 1: [], 2: []}
+    for e in range(20):
+        grp = 4 - (e >> 2)
+        for c, ws, cd in ((grp, 16, 36), (grp + 5, 56, 76)):
+            if row[ws + e] > 0:
+                ep[part(c)].append((rel(row[ws + e]), rel(row[cd + e])))
+    es = []
+    for p in range(3):
+        if ep[p]:
+            es.append(f"e{p}:[{min(x for x, _ in ep[p])}..{max(y for _, y in ep[p])}]({max(y - x for x, y in ep[p])})")
+    print(f"L{l}: " + " ".join(parts) + " | " + " ".join(es))
