@@ -576,110 +576,161 @@ __device__ __forceinline__ float wrap_fast(float x)
 
 constexpr int kRasterWarps = 8;
 
-// One CTA per (tile, position); each warp takes every 8th (tile, primitive)
-// pair of the tile's list (ascending primitive index) and maps its lanes onto
-// the pair's clipped box only — rows [max(r0, tile), min(r1, tile)] x the one or
-// two wrapped column spans (splat.cpp:450-470) — so no lane is spent on cells
-// the reference does not evaluate. Each warp accumulates into its own
-// shared-memory copy of the tile (no atomics); the eight copies are summed in
-// fixed warp order at the end, so the result is bit-deterministic. The
-// cutoff mask uses the reference's float q (same operation order, no FMA);
-// exp(-q/2) is ex2.approx of a prescaled argument.
+// One CTA per (tile, position). The tile's (tile, primitive) list (ascending
+// primitive index) is cut into chunks of 32 pairs; warp w takes chunks w, w+8, ...
+// For a chunk, each lane first prepares one pair (gathers its dynamic state,
+// shape and box, clips the box to the tile: rows [max(r0, tile), min(r1, tile)]
+// x the one or two wrapped column spans, splat.cpp:450-470) into a per-warp
+// record in shared memory; then the whole warp evaluates the records one by
+// one with its lanes mapped onto the clipped box only (lane -> (row, column)
+// from a small table, rows-per-sweep = 32 / columns), so no lane is spent on
+// cells the reference does not evaluate and the per-pair setup costs one lane,
+// not a warp. Each warp accumulates into its own shared-memory copy of the tile
+// (no atomics); the eight copies are summed in fixed warp order at the end, so
+// the result is bit-deterministic. The cutoff mask uses the reference's float q
+// (same operation order, no FMA); exp(-q/2) is ex2.approx of a prescaled
+// argument.
+struct RasterRec
+{
+    float4 dyn;   // el, az, amplitude re, im
+    float4 shape; // i00, i01, i11, 1/l1
+    int4 box;     // first row, last row (tile-relative), cols: a0 | na << 8 | ncol << 16 | rpi << 24, sweeps
+};
+
 __global__ void __launch_bounds__(256) raster_kernel(Grid g, SceneDev sd, const float4 *__restrict__ dyn,
                                                      const int4 *__restrict__ rng, const int64_t *__restrict__ seg,
                                                      const int *__restrict__ tile_off, const int *__restrict__ prims,
                                                      float *__restrict__ spec, float4 *__restrict__ tile_part,
                                                      double *__restrict__ tile_sum, int want_heads)
 {
-    extern __shared__ float2 acc[]; // [8][T*T]
-    __shared__ float elc[32], azc[32];
+    extern __shared__ float2 acc[]; // [8][T*T], then RasterRec [8][32]
+    __shared__ float elc[64], azc[32]; // elc zero-padded: a lane's last sweep may run past the tile
+    __shared__ uint32_t magic[33];
+    __shared__ uint16_t divtab[33 * 32]; // [ncol][lane] -> lane / ncol | (lane % ncol) << 8
     const int T = g.tile, TT = T * T;
     const int t = blockIdx.x, s = blockIdx.y;
     const int tr0 = (t / g.tw) * T, tc0 = (t % g.tw) * T;
     const int tr1 = min(tr0 + T, g.H) - 1, tc1 = min(tc0 + T, g.W) - 1;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    RasterRec *recs = reinterpret_cast<RasterRec *>(acc + kRasterWarps * TT) + warp * 32;
     for (int i = threadIdx.x; i < kRasterWarps * TT; i += blockDim.x)
         acc[i] = make_float2(0.f, 0.f);
+    if (threadIdx.x < 64)
+        elc[threadIdx.x] = (int)threadIdx.x < T && tr0 + (int)threadIdx.x <= tr1 ? sd.el_c[tr0 + threadIdx.x] : 0.f;
     if (threadIdx.x < T)
-    {
-        elc[threadIdx.x] = tr0 + (int)threadIdx.x <= tr1 ? sd.el_c[tr0 + threadIdx.x] : 0.f;
         azc[threadIdx.x] = tc0 + (int)threadIdx.x <= tc1 ? sd.az_c[tc0 + threadIdx.x] : 0.f;
+    // magic reciprocals: floor(x / d) == (x * m[d]) >> 16 for x <= 32, d <= 32
+    if (threadIdx.x <= 32)
+        magic[threadIdx.x] = threadIdx.x ? (65536u / threadIdx.x) + 1u : 0u;
+    for (int i = threadIdx.x; i < 33 * 32; i += blockDim.x)
+    {
+        const int nc = i >> 5, ln = i & 31;
+        divtab[i] = nc ? (uint16_t)((ln / nc) | ((ln % nc) << 8)) : (uint16_t)0xff;
     }
     __syncthreads();
     const int *tl = tile_off + (int64_t)s * (g.tiles + 1);
     const int64_t lb = seg[s] + tl[t], le = seg[s] + tl[t + 1];
     const int64_t sbase = (int64_t)s * g.np;
     float2 *my = acc + warp * TT;
+    const uint32_t acc_base = (uint32_t)__cvta_generic_to_shared(my);
+    const uint32_t el_base = (uint32_t)__cvta_generic_to_shared(elc);
+    const float cut2 = g.cut2;
     const float kExp = -0.72134752044448170368f; // -0.5 * log2(e)
-
-    // magic reciprocals: floor(x / d) == (x * m[d]) >> 16 for x <= 32, d <= 32
-    __shared__ uint32_t magic[33];
-    if (threadIdx.x <= 32)
-        magic[threadIdx.x] = threadIdx.x ? (65536u / threadIdx.x) + 1u : 0u;
-    __syncthreads();
-    // 32-bit offsets inside this (position, tile) list
-    const int *plist = prims + lb;
+    const int *plist = prims + lb;               // 32-bit offsets inside this (position, tile) list
     const int cnt = (int)(le - lb);
     const float4 *dyn_s = dyn + sbase;
     const int4 *rng_s = rng + sbase;
-    int i = warp;
-    int gi = i < cnt ? plist[i] : 0;
-    int4 b = i < cnt ? rng_s[gi] : make_int4(0, -1, 0, 0);
     const int tcw = tc1 - tc0 + 1;
+
+    // gathered state of the lane's pair in the next chunk (software pipelined)
+    int c0 = warp * 32;
+    int gi = c0 + lane < cnt ? plist[c0 + lane] : -1;
+    int4 b = gi >= 0 ? rng_s[gi] : make_int4(0, -1, 0, 0);
+    float4 d = gi >= 0 ? dyn_s[gi] : make_float4(0.f, 0.f, 0.f, 0.f);
+    float4 sh = gi >= 0 ? sd.shape[gi] : make_float4(0.f, 0.f, 0.f, 0.f);
 #pragma unroll 1
-    for (; i < cnt; i += kRasterWarps)
+    for (; c0 < cnt; c0 += kRasterWarps * 32)
     {
-        // prefetch the warp's next pair while this one is evaluated
-        const int inext = i + kRasterWarps;
-        const int gnext = inext < cnt ? plist[inext] : 0;
-        const int pr0 = max(b.x, tr0), pr1 = min(b.y, tr1);
-        int a0 = tc0, na = tcw, nb2 = 0;
-        if (b.w < g.W)
+        // this lane's pair -> record
         {
-            const int jend = b.z + b.w - 1;
-            a0 = max(tc0, b.z);
-            na = max(0, min(tc1, min(jend, g.W - 1)) - a0 + 1);
-            nb2 = jend >= g.W ? max(0, min(tc1, jend - g.W) - tc0 + 1) : 0;
-        }
-        const int ncol = na + nb2;
-        const int nrow = pr1 - pr0 + 1;
-        const float4 d = dyn_s[gi];
-        const float4 sh = sd.shape[gi];
-        const int4 bnext = inext < cnt ? rng_s[gnext] : make_int4(0, -1, 0, 0);
-        if (ncol > 0 && nrow > 0)
-        {
-            const uint32_t m = magic[ncol];
-            const int rpi = (int)((32u * m) >> 16); // rows per lane sweep
-            const int niter = (int)(((uint32_t)(nrow + rpi - 1) * magic[rpi]) >> 16);
-            const int lr = (int)(((uint32_t)lane * m) >> 16), lc = lane - lr * ncol;
-            const bool lane_on = lr < rpi;
-            const int cc = lc < na ? a0 - tc0 + lc : lc - na; // column inside the tile
-            const float d_az = wrap_fast(__fsub_rn(azc[min(cc, 31)], d.y));
-            const float w1 = __fmul_rn(__fmul_rn(sh.z, d_az), d_az);
-            const float w2 = __fmul_rn(__fmul_rn(2.0f, sh.y), d_az);
-            int rr = pr0 - tr0 + lr; // row inside the tile
-            const int rlast = pr1 - tr0;
-            float2 *col = my + cc;
-#pragma unroll 1
-            for (int it = 0; it < niter; it++, rr += rpi)
+            const int pr0 = max(b.x, tr0), pr1 = min(b.y, tr1);
+            int a0 = tc0, na = tcw, nb2 = 0;
+            if (b.w < g.W)
             {
-                const float d_el = __fsub_rn(elc[min(rr, 31)], d.x);
-                const float u0 = __fmul_rn(d_el, sh.w);
-                const float q_c = __fmul_rn(__fmul_rn(sh.x, d_el), d_el);
+                const int jend = b.z + b.w - 1;
+                a0 = max(tc0, b.z);
+                na = max(0, min(tc1, min(jend, g.W - 1)) - a0 + 1);
+                nb2 = jend >= g.W ? max(0, min(tc1, jend - g.W) - tc0 + 1) : 0;
+            }
+            const int ncol = na + nb2, nrow = pr1 - pr0 + 1;
+            int rpi = 0, sweeps = 0;
+            if (gi >= 0 && ncol > 0 && nrow > 0)
+            {
+                rpi = (int)((32u * magic[ncol]) >> 16);
+                sweeps = (int)(((uint32_t)(nrow + rpi - 1) * magic[rpi]) >> 16);
+            }
+            RasterRec r;
+            r.dyn = d;
+            r.shape = sh;
+            const int a0off = na > 0 ? a0 - tc0 : 0; // (a0 may lie past the tile when only the wrapped span is in it)
+            r.box = make_int4(pr0 - tr0, pr1 - tr0, a0off | (na << 8) | (ncol << 16) | (rpi << 24), sweeps);
+            recs[lane] = r;
+        }
+        // prefetch the pairs of this warp's next chunk
+        const int cn = c0 + kRasterWarps * 32;
+        gi = cn + lane < cnt ? plist[cn + lane] : -1;
+        b = gi >= 0 ? rng_s[gi] : make_int4(0, -1, 0, 0);
+        d = gi >= 0 ? dyn_s[gi] : make_float4(0.f, 0.f, 0.f, 0.f);
+        sh = gi >= 0 ? sd.shape[gi] : make_float4(0.f, 0.f, 0.f, 0.f);
+        __syncwarp();
+        const int nrec = min(32, cnt - c0);
+#pragma unroll 1
+        for (int j = 0; j < nrec; j++)
+        {
+            const int4 bx = recs[j].box;
+            if (bx.w == 0)
+                continue;
+            const float4 A = recs[j].dyn, S = recs[j].shape;
+            const int a0off = bx.z & 0xff, na = (bx.z >> 8) & 0xff, ncol = (bx.z >> 16) & 0xff, rpi = bx.z >> 24;
+            const uint32_t tt = divtab[ncol * 32 + lane];
+            const int lr = (int)(tt & 0xff), lc = (int)(tt >> 8);
+            const bool lane_on = lr < rpi;
+            const int cc = lc < na ? a0off + lc : lc - na; // column inside the tile
+            const float d_az = wrap_fast(__fsub_rn(azc[cc], A.y));
+            const float w1 = __fmul_rn(__fmul_rn(S.z, d_az), d_az);
+            const float w2 = __fmul_rn(__fmul_rn(2.0f, S.y), d_az);
+            // lane-private pointers (32-bit shared addresses): its row's el centre and
+            // its cell; both advance by rpi rows per sweep
+            const int rr0 = bx.x + lr;
+            uint32_t elp = el_base + 4u * (uint32_t)rr0;
+            uint32_t cp = acc_base + 8u * (uint32_t)(rr0 * T + cc);
+            const uint32_t el_step = 4u * (uint32_t)rpi, c_step = 8u * (uint32_t)(rpi * T);
+            // sweeps in which this lane's row is inside the box
+            const int nvalid = lane_on ? min(bx.w, (int)(((uint32_t)(bx.y - rr0 + rpi) * magic[rpi]) >> 16)) : 0;
+#pragma unroll 1
+            for (int it = 0; it < bx.w; it++, elp += el_step, cp += c_step)
+            {
+                float elv;
+                asm volatile("ld.shared.f32 %0, [%1];" : "=f"(elv) : "r"(elp));
+                const float d_el = __fsub_rn(elv, A.x);
+                const float u0 = __fmul_rn(d_el, S.w);
+                const float q_c = __fmul_rn(__fmul_rn(S.x, d_el), d_el);
                 const float q = __fadd_rn(__fadd_rn(q_c, __fmul_rn(d_el, w2)), w1);
-                const bool ok = lane_on && rr <= rlast && !(__fmul_rn(u0, u0) > g.cut2) && q <= g.cut2;
+                const bool ok = it < nvalid && !(__fmul_rn(u0, u0) > cut2) && q <= cut2;
                 float e;
                 asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(e) : "f"(q * kExp));
-                if (ok)
-                {
-                    float2 &cell = col[rr * T];
-                    cell.x = __fmaf_rn(d.z, e, cell.x);
-                    cell.y = __fmaf_rn(d.w, e, cell.y);
-                }
+                // predicated read-modify-write of the cell (no branch)
+                asm volatile("{\n\t.reg .pred p;\n\t.reg .f32 a, b;\n\t"
+                             "setp.ne.u32 p, %0, 0;\n\t"
+                             "@p ld.shared.v2.f32 {a, b}, [%1];\n\t"
+                             "@p fma.rn.f32 a, %2, %4, a;\n\t"
+                             "@p fma.rn.f32 b, %3, %4, b;\n\t"
+                             "@p st.shared.v2.f32 [%1], {a, b};\n\t}" ::"r"((uint32_t)ok),
+                             "r"(cp), "f"(A.z), "f"(A.w), "f"(e)
+                             : "memory");
             }
         }
-        gi = gnext;
-        b = bnext;
+        __syncwarp(); // records are rewritten for the next chunk
     }
     __syncthreads();
     float best = -1.0f, lsum_f = 0.f;
@@ -720,7 +771,7 @@ __global__ void __launch_bounds__(256) raster_kernel(Grid g, SceneDev sd, const 
 void launch_raster(Ctx &c, int nb, float *d_spec, bool want_heads, cudaStream_t st)
 {
     dim3 grid(c.g.tiles, nb);
-    const size_t smem = (size_t)kRasterWarps * c.g.tile * c.g.tile * sizeof(float2);
+    const size_t smem = (size_t)kRasterWarps * c.g.tile * c.g.tile * sizeof(float2) + kRasterWarps * 32 * 48;
     static size_t configured = 0;
     if (smem > 48 * 1024 && configured < smem)
     {
