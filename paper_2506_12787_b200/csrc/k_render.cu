@@ -593,9 +593,12 @@ constexpr int kRasterWarps = 8;
 struct RasterRec
 {
     float4 dyn;   // el, az, amplitude re, im
-    float4 shape; // i00, i01, i11, 1/l1
-    int4 box;     // first row, last row (tile-relative), cols: a0 | na << 8 | ncol << 16 | rpi << 24, sweeps
+    float4 shape; // i00, 2*i01 (exact), i11, 1/l1
+    int4 box;     // first row, last row (tile-relative), ncol | na << 6 | a0 << 12 | rpi << 18 | sweeps << 24,
+                  // magic(ncol) | magic(rpi) << 13
 };
+// floor(x / d) == (x * m[d]) >> 12 for 0 <= x < 128, 1 <= d <= 32, m[d] = ceil(4096 / d)
+__host__ __device__ constexpr uint32_t magic12(int d) { return (4096u + d - 1) / d; }
 
 __global__ void __launch_bounds__(256) raster_kernel(Grid g, SceneDev sd, const float4 *__restrict__ dyn,
                                                      const int4 *__restrict__ rng, const int64_t *__restrict__ seg,
@@ -606,7 +609,6 @@ __global__ void __launch_bounds__(256) raster_kernel(Grid g, SceneDev sd, const 
     extern __shared__ float2 acc[]; // [8][T*T], then RasterRec [8][32]
     __shared__ float elc[64], azc[32]; // elc zero-padded: a lane's last sweep may run past the tile
     __shared__ uint32_t magic[33];
-    __shared__ uint16_t divtab[33 * 32]; // [ncol][lane] -> lane / ncol | (lane % ncol) << 8
     const int T = g.tile, TT = T * T;
     const int t = blockIdx.x, s = blockIdx.y;
     const int tr0 = (t / g.tw) * T, tc0 = (t % g.tw) * T;
@@ -619,14 +621,8 @@ __global__ void __launch_bounds__(256) raster_kernel(Grid g, SceneDev sd, const 
         elc[threadIdx.x] = (int)threadIdx.x < T && tr0 + (int)threadIdx.x <= tr1 ? sd.el_c[tr0 + threadIdx.x] : 0.f;
     if (threadIdx.x < T)
         azc[threadIdx.x] = tc0 + (int)threadIdx.x <= tc1 ? sd.az_c[tc0 + threadIdx.x] : 0.f;
-    // magic reciprocals: floor(x / d) == (x * m[d]) >> 16 for x <= 32, d <= 32
     if (threadIdx.x <= 32)
-        magic[threadIdx.x] = threadIdx.x ? (65536u / threadIdx.x) + 1u : 0u;
-    for (int i = threadIdx.x; i < 33 * 32; i += blockDim.x)
-    {
-        const int nc = i >> 5, ln = i & 31;
-        divtab[i] = nc ? (uint16_t)((ln / nc) | ((ln % nc) << 8)) : (uint16_t)0xff;
-    }
+        magic[threadIdx.x] = threadIdx.x ? magic12(threadIdx.x) : 0u;
     __syncthreads();
     const int *tl = tile_off + (int64_t)s * (g.tiles + 1);
     const int64_t lb = seg[s] + tl[t], le = seg[s] + tl[t + 1];
@@ -664,16 +660,20 @@ __global__ void __launch_bounds__(256) raster_kernel(Grid g, SceneDev sd, const 
             }
             const int ncol = na + nb2, nrow = pr1 - pr0 + 1;
             int rpi = 0, sweeps = 0;
+            uint32_t mn = 0, mr = 0;
             if (gi >= 0 && ncol > 0 && nrow > 0)
             {
-                rpi = (int)((32u * magic[ncol]) >> 16);
-                sweeps = (int)(((uint32_t)(nrow + rpi - 1) * magic[rpi]) >> 16);
+                mn = magic[ncol];
+                rpi = (int)((32u * mn) >> 12); // rows per sweep
+                mr = magic[rpi];
+                sweeps = (int)(((uint32_t)(nrow + rpi - 1) * mr) >> 12);
             }
             RasterRec r;
             r.dyn = d;
-            r.shape = sh;
+            r.shape = make_float4(sh.x, __fmul_rn(2.0f, sh.y), sh.z, sh.w);
             const int a0off = na > 0 ? a0 - tc0 : 0; // (a0 may lie past the tile when only the wrapped span is in it)
-            r.box = make_int4(pr0 - tr0, pr1 - tr0, a0off | (na << 8) | (ncol << 16) | (rpi << 24), sweeps);
+            r.box = make_int4(pr0 - tr0, pr1 - tr0, ncol | (na << 6) | (a0off << 12) | (rpi << 18) | (sweeps << 24),
+                              (int)(mn | (mr << 13)));
             recs[lane] = r;
         }
         // prefetch the pairs of this warp's next chunk
@@ -688,17 +688,18 @@ __global__ void __launch_bounds__(256) raster_kernel(Grid g, SceneDev sd, const 
         for (int j = 0; j < nrec; j++)
         {
             const int4 bx = recs[j].box;
-            if (bx.w == 0)
+            const int sweeps = bx.z >> 24;
+            if (sweeps == 0)
                 continue;
             const float4 A = recs[j].dyn, S = recs[j].shape;
-            const int a0off = bx.z & 0xff, na = (bx.z >> 8) & 0xff, ncol = (bx.z >> 16) & 0xff, rpi = bx.z >> 24;
-            const uint32_t tt = divtab[ncol * 32 + lane];
-            const int lr = (int)(tt & 0xff), lc = (int)(tt >> 8);
+            const int ncol = bx.z & 63, na = (bx.z >> 6) & 63, a0off = (bx.z >> 12) & 63, rpi = (bx.z >> 18) & 63;
+            const uint32_t mn = (uint32_t)bx.w & 0x1fffu, mr = (uint32_t)bx.w >> 13;
+            const int lr = (int)(((uint32_t)lane * mn) >> 12), lc = lane - lr * ncol;
             const bool lane_on = lr < rpi;
             const int cc = lc < na ? a0off + lc : lc - na; // column inside the tile
             const float d_az = wrap_fast(__fsub_rn(azc[cc], A.y));
             const float w1 = __fmul_rn(__fmul_rn(S.z, d_az), d_az);
-            const float w2 = __fmul_rn(__fmul_rn(2.0f, S.y), d_az);
+            const float w2 = __fmul_rn(S.y, d_az); // (2 * i01) * d_az
             // lane-private pointers (32-bit shared addresses): its row's el centre and
             // its cell; both advance by rpi rows per sweep
             const int rr0 = bx.x + lr;
@@ -706,9 +707,9 @@ __global__ void __launch_bounds__(256) raster_kernel(Grid g, SceneDev sd, const 
             uint32_t cp = acc_base + 8u * (uint32_t)(rr0 * T + cc);
             const uint32_t el_step = 4u * (uint32_t)rpi, c_step = 8u * (uint32_t)(rpi * T);
             // sweeps in which this lane's row is inside the box
-            const int nvalid = lane_on ? min(bx.w, (int)(((uint32_t)(bx.y - rr0 + rpi) * magic[rpi]) >> 16)) : 0;
-#pragma unroll 1
-            for (int it = 0; it < bx.w; it++, elp += el_step, cp += c_step)
+            const int nvalid = lane_on ? (int)(((uint32_t)(bx.y - rr0 + rpi) * mr) >> 12) : 0;
+#pragma unroll 2
+            for (int it = 0; it < sweeps; it++, elp += el_step, cp += c_step)
             {
                 float elv;
                 asm volatile("ld.shared.f32 %0, [%1];" : "=f"(elv) : "r"(elp));
