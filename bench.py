@@ -265,7 +265,11 @@ def main():
         step()
     torch.cuda.synchronize()
 
-    # ---------------- device-timed region: K steps, L2 flushed between steps (untimed)
+    # ---------------- device-timed region: K steps, L2 flushed between steps (untimed).
+    # Per-stage CUDA events ride along (recorded on the render stream, read after
+    # the region): the dominant kernel's average launch time for the roofline.
+    ck.set_option("stage_timing", 1)
+    ck.set_option("stage_reset", 1)
     l0 = ck.launch_count()
     ms = []
     with ClockSampler(local) as clk:
@@ -290,12 +294,9 @@ def main():
     total_ms = max_over_ranks(float(sum(ms)), device="cuda")
     value = total * args.steps / (total_ms / 1e3)
 
-    # ---------------- stage split + dominant kernel timing (separate pass, events per stage)
-    ck.set_option("stage_timing", 1)
-    step()
-    torch.cuda.synchronize()
-    stages = ck.stage_times()
     ck.set_option("stage_timing", 0)
+    chunks_per_step = -(-B // args.chunk)
+    stages = ck.stage_times() / float(args.steps)  # ms per step (each stage summed over its chunks)
 
     # ---------------- end to end through the host C ABI (pinned host buffers)
     h_pos = torch.from_numpy(pos).pin_memory()
@@ -337,6 +338,10 @@ def main():
         peak = peaks["bf16_tflops"]
         bound, peak_note = "tensor", f"bf16 dense {peak_src} burst"
     achieved = fmin * rows / (mlp_ms / 1e3) / 1e12 if mlp_ms > 0 else None
+    wp = 160 if scene.width <= 160 else 512
+    issued = None
+    if args.precision != "fp32" and wp == 160:
+        issued = (3 if args.precision == "bf16x3" else 1) * 2 * (7 * wp * wp + 4 * 48 * wp + wp * 32)
     traffic = None
     prof = os.path.join(ROOT, "profiles", "ncu_mlp_traffic.json")
     if os.path.exists(prof) and args.chunk == 256 and args.config == 2:
@@ -359,9 +364,15 @@ def main():
         "data": "synthetic (seeded scene + TX positions)",
         "config": config_dict(args, scene),
         "roofline": {"bound": bound, "kernel": "deform MLP (mlp_tc_kernel)", "achieved": achieved, "peak": peak,
-                     "unit": "TFLOP/s", "traffic_unit": "bytes per launch (256-position chunk)", "frac": (achieved / peak) if achieved else None, "traffic": traffic,
+                     "unit": "TFLOP/s", "frac": (achieved / peak) if achieved else None, "traffic": traffic,
+                     "traffic_unit": "DRAM bytes per launch (256-position chunk), ncu --set full",
                      "peak_source": peak_note,
-                     "flop_per_row": fmin, "flop_per_row_literal": flit, "rows_per_launch": rows},
+                     "flop_per_row": fmin, "flop_per_row_literal": flit, "rows_per_launch": rows // chunks_per_step,
+                     "kernel_ms_per_launch": mlp_ms / chunks_per_step, "launches_timed": chunks_per_step * args.steps,
+                     "timing": "CUDA events on the render stream around every MLP launch of the timed steps",
+                     # what the tensor pipe executes: padded shapes (K 48/160, N 160/32) x 3 split passes
+                     "issued_flop_per_row": issued, "issued_tflops": (issued * rows / (mlp_ms / 1e3) / 1e12)
+                     if mlp_ms > 0 and issued else None},
         "stage_ms": {k: round(float(v), 3) for k, v in zip(["pos_prep", "mlp", "setup", "bin", "raster", "heads"], stages)},
         "cpu_baseline": cpu,
         "e2e": {"value": e2e_value, "unit": "spectra/s", "h2d_bytes_per_step": int(pos.nbytes) * world,

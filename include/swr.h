@@ -75,7 +75,9 @@ void swr_scene_destroy(swr_ctx *ctx);
 int swr_scene_get_info(swr_ctx *ctx, swr_scene_info *info);
 
 /* Options: "mlp_precision" (SWR_MLP_*), "chunk" (positions per device chunk),
- * "rssi_slope" / "rssi_intercept" (affine RSSI calibration, tasks.cpp:60-94). */
+ * "rssi_slope" / "rssi_intercept" (affine RSSI calibration, tasks.cpp:60-94),
+ * "stage_timing" (1: record per-stage CUDA events), "stage_reset" (zero the
+ * accumulated stage times). */
 int swr_set_option(swr_ctx *ctx, const char *key, double value);
 
 /* Batched render_at (training.cpp:189-195) + heads, host buffers, synchronous.
@@ -126,9 +128,10 @@ int swr_heads(swr_ctx *ctx, const float *spectra, int64_t B, double *pooled, int
 /* Kernel launches issued by this context since creation (for the bench). */
 int64_t swr_launch_count(swr_ctx *ctx);
 
-/* Device time (ms) of the last render's stages, accumulated per chunk:
+/* Device time (ms) of the render stages, summed over every chunk rendered while
+ * option "stage_timing" is 1 since the last "stage_reset":
  * [0] position prep, [1] MLP, [2] setup, [3] bin (scan+emit+sort), [4] raster, [5] heads.
- * Only filled when option "stage_timing" is 1. */
+ * Events are read here (no host sync inside the renders). */
 int swr_stage_times(swr_ctx *ctx, double *ms6);
 
 const char *swr_last_error(void);

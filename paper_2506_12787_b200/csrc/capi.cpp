@@ -368,21 +368,36 @@ struct Timer
         if (on)
             cudaEventRecord(ev[k++], st);
     }
-    void finish(const int *stage_of_interval)
+    // events are read lazily (resolve_stage_times) so timing adds no host sync
+    void finish()
     {
         if (!on)
             return;
-        cudaEventSynchronize(ev[k - 1]);
-        for (int i = 0; i + 1 < k; i++)
-        {
-            float ms = 0;
-            cudaEventElapsedTime(&ms, ev[i], ev[i + 1]);
-            c.stage_ms[stage_of_interval[i]] += ms;
-        }
-        for (auto &e : ev)
-            cudaEventDestroy(e);
+        std::array<cudaEvent_t, 7> a;
+        for (int i = 0; i < 7; i++)
+            a[i] = ev[i];
+        c.stage_pending.push_back(a);
     }
 };
+
+// fold the recorded per-chunk stage intervals into c.stage_ms (or drop them)
+static void resolve_stage_times(Ctx &c, bool keep)
+{
+    for (auto &a : c.stage_pending)
+    {
+        cudaEventSynchronize(a[6]);
+        if (keep)
+            for (int i = 0; i < 6; i++)
+            {
+                float ms = 0;
+                cudaEventElapsedTime(&ms, a[i], a[i + 1]);
+                c.stage_ms[i] += ms;
+            }
+        for (auto &e : a)
+            cudaEventDestroy(e);
+    }
+    c.stage_pending.clear();
+}
 
 // Render one chunk of nb positions whose (device) coordinates are d_pos.
 // Residuals come from the MLP (use_mlp), the caller (already in w.res) or are
@@ -392,7 +407,6 @@ static void run_chunk(Ctx &c, const float *d_pos, int nb, bool normalized, bool 
                       double *d_aoa_ang, cudaStream_t st)
 {
     Timer tm(c, st);
-    static const int stage_map[6] = {0, 1, 2, 3, 4, 5};
     tm.mark();
     if (use_mlp)
     {
@@ -423,7 +437,7 @@ static void run_chunk(Ctx &c, const float *d_pos, int nb, bool normalized, bool 
         launch_heads(c, nb, flags, d_pooled, d_rssi, d_aoa_rc, d_aoa_ang, st);
     tm.mark();
     check_cuda(cudaGetLastError(), "kernel launch");
-    tm.finish(stage_map);
+    tm.finish();
 }
 
 static bool is_pinned(const void *p)
@@ -444,8 +458,6 @@ static void device_render(Ctx &c, const float *d_pos, int64_t B, uint32_t flags,
     const bool heads = flags & (SWR_OUT_POOLED | SWR_OUT_RSSI | SWR_OUT_AOA);
     const int64_t chunk = std::max<int64_t>(1, std::min<int64_t>(B, c.chunk));
     ensure_work(c, chunk);
-    if (c.stage_timing)
-        std::fill(c.stage_ms, c.stage_ms + 6, 0.0);
     const size_t per = size_t(2) * c.g.H * c.g.W;
     for (int64_t b0 = 0; b0 < B; b0 += chunk)
     {
@@ -670,6 +682,7 @@ static void destroy(swr_ctx *h)
     if (!h)
         return;
     cudaSetDevice(h->c.device);
+    resolve_stage_times(h->c, false);
     for (void *p : h->c.allocs)
         cudaFree(p);
     if (h->c.w.host_pairs)
@@ -800,6 +813,11 @@ int swr_set_option(swr_ctx *ctx, const char *key, double value)
             c.rssi_intercept = value;
         else if (k == "stage_timing")
             c.stage_timing = value != 0.0;
+        else if (k == "stage_reset")
+        {
+            resolve_stage_times(c, false);
+            std::fill(c.stage_ms, c.stage_ms + 6, 0.0);
+        }
         else
             throw std::invalid_argument("unknown option " + k);
     });
@@ -848,8 +866,6 @@ int swr_render(swr_ctx *ctx, const float *pos_m, int64_t B, uint32_t flags, floa
         check_cuda(cudaMemcpyAsync(d_pos, pos_m, sizeof(float) * 3 * B, cudaMemcpyHostToDevice, st), "H2D positions");
         const bool use_mlp = c.has_net && !(flags & SWR_NO_RESIDUALS);
         const bool heads = flags & (SWR_OUT_POOLED | SWR_OUT_RSSI | SWR_OUT_AOA);
-        if (c.stage_timing)
-            std::fill(c.stage_ms, c.stage_ms + 6, 0.0);
         int k = 0;
         for (int64_t b0 = 0; b0 < B; b0 += chunk, k ^= 1)
         {
@@ -1090,6 +1106,7 @@ int swr_debug_mlp_trace(long long *out)
 
 int swr_stage_times(swr_ctx *ctx, double *ms6)
 {
+    resolve_stage_times(ctx->c, true);
     for (int i = 0; i < 6; i++)
         ms6[i] = ctx->c.stage_ms[i];
     return SWR_OK;

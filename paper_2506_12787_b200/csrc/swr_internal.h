@@ -5,6 +5,7 @@
 
 #include <cstdint>
 #include <string>
+#include <array>
 #include <vector>
 
 namespace swr
@@ -97,7 +98,8 @@ struct Ctx
     Work w;
     int64_t launches = 0;
     int64_t pairs_last = 0;
-    double stage_ms[6]{};
+    double stage_ms[6]{};               // accumulated while stage_timing is on (swr_stage_times resolves)
+    std::vector<std::array<cudaEvent_t, 7>> stage_pending; // recorded per chunk, read lazily
     std::vector<void *> allocs;
     void *host_stage = nullptr; // persistent staging of the host-buffer API (capi.cpp)
 };
