@@ -21,6 +21,8 @@
 #include <stdexcept>
 #include <string>
 #include <vector>
+#include <thread>
+#include <chrono>
 
 namespace swr
 {
@@ -1102,6 +1104,55 @@ int64_t swr_launch_count(swr_ctx *ctx) { return ctx->c.launches; }
 int swr_debug_mlp_trace(long long *out)
 {
     return swr::mlp_tc_trace(out);
+}
+
+// debug: after a render, time (ms) the MLP alone, the raster (8 / 4 warps) alone
+// and the MLP concurrent with the raster on a second stream: out[0..5] =
+// mlp, r8, r4, mlp||r4 (both done), mlp||r8, nb
+int swr_debug_overlap(swr_ctx *ctx, double *out)
+{
+    return guarded([&] {
+        Ctx &c = ctx->c;
+        const int nb = (int)c.w.cap_b;
+        cudaStream_t a = c.stream, b;
+        check_cuda(cudaStreamCreateWithFlags(&b, cudaStreamNonBlocking), "stream");
+        cudaEvent_t e0, e1, e2;
+        cudaEventCreate(&e0);
+        cudaEventCreate(&e1);
+        cudaEventCreate(&e2);
+        auto timed = [&](auto &&f) {
+            cudaStreamSynchronize(a);
+            cudaStreamSynchronize(b);
+            cudaEventRecord(e0, a);
+            cudaStreamWaitEvent(b, e0, 0);
+            f();
+            cudaEventRecord(e2, b);
+            cudaStreamWaitEvent(a, e2, 0);
+            cudaEventRecord(e1, a);
+            cudaEventSynchronize(e1);
+            float ms = 0;
+            cudaEventElapsedTime(&ms, e0, e1);
+            return (double)ms;
+        };
+        out[0] = timed([&] { launch_mlp(c, nb, a); });
+        out[1] = timed([&] { launch_raster(c, nb, nullptr, false, b, 8); });
+        out[2] = timed([&] { launch_raster(c, nb, nullptr, false, b, 4); });
+        out[3] = timed([&] {
+            launch_mlp(c, nb, a);
+            std::this_thread::sleep_for(std::chrono::microseconds(2000)); // MLP CTAs resident first
+            launch_raster(c, nb, nullptr, false, b, 4);
+        });
+        out[4] = timed([&] {
+            launch_mlp(c, nb, a);
+            launch_raster(c, nb, nullptr, false, b, 8);
+        });
+        out[5] = nb;
+        check_cuda(cudaStreamSynchronize(a), "overlap");
+        cudaStreamDestroy(b);
+        cudaEventDestroy(e0);
+        cudaEventDestroy(e1);
+        cudaEventDestroy(e2);
+    });
 }
 
 int swr_stage_times(swr_ctx *ctx, double *ms6)

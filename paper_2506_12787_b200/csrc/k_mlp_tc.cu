@@ -770,6 +770,13 @@ void launch_mlp_tc(Ctx &c, int nb, cudaStream_t st)
                    "tc mlp smem attribute");
         check_cuda(cudaFuncSetAttribute(mlp_tc_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES),
                    "tc mlp smem attribute");
+        // all 228 KB as shared memory: the SM then has room for a raster CTA next to
+        // this persistent CTA (without it the driver sizes the carveout to this
+        // kernel alone and nothing else can share the SM)
+        for (auto k : {mlp_tc_kernel<true>, mlp_tc_kernel<false>})
+            check_cuda(cudaFuncSetAttribute(k, cudaFuncAttributePreferredSharedMemoryCarveout,
+                                            (int)cudaSharedmemCarveoutMaxShared),
+                       "tc mlp carveout");
         // persistent grid: as many CTA pairs as can be co-resident (TPCs whose two
         // SMs are both available), never more -- a second wave would double the time
         cudaLaunchConfig_t cfg = {};

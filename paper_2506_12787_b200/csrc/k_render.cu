@@ -574,7 +574,6 @@ __device__ __forceinline__ float wrap_fast(float x)
     return x;
 }
 
-constexpr int kRasterWarps = 8;
 
 // One CTA per (tile, position). The tile's (tile, primitive) list (ascending
 // primitive index) is cut into chunks of 32 pairs; warp w takes chunks w, w+8, ...
@@ -600,7 +599,8 @@ struct RasterRec
 // floor(x / d) == (x * m[d]) >> 12 for 0 <= x < 128, 1 <= d <= 32, m[d] = ceil(4096 / d)
 __host__ __device__ constexpr uint32_t magic12(int d) { return (4096u + d - 1) / d; }
 
-__global__ void __launch_bounds__(256) raster_kernel(Grid g, SceneDev sd, const float4 *__restrict__ dyn,
+template <int kRasterWarps>
+__global__ void __launch_bounds__(32 * kRasterWarps) raster_kernel(Grid g, SceneDev sd, const float4 *__restrict__ dyn,
                                                      const int4 *__restrict__ rng, const int64_t *__restrict__ seg,
                                                      const int *__restrict__ tile_off, const int *__restrict__ prims,
                                                      float *__restrict__ spec, float4 *__restrict__ tile_part,
@@ -769,20 +769,34 @@ __global__ void __launch_bounds__(256) raster_kernel(Grid g, SceneDev sd, const 
         heads_reduce(best, bidx, lsum, tile_part + (int64_t)s * g.tiles + t, tile_sum + (int64_t)s * g.tiles + t);
 }
 
-void launch_raster(Ctx &c, int nb, float *d_spec, bool want_heads, cudaStream_t st)
+template <int WARPS>
+static void launch_raster_w(Ctx &c, int nb, float *d_spec, bool want_heads, cudaStream_t st)
 {
     dim3 grid(c.g.tiles, nb);
-    const size_t smem = (size_t)kRasterWarps * c.g.tile * c.g.tile * sizeof(float2) + kRasterWarps * 32 * 48;
+    const size_t smem = (size_t)WARPS * c.g.tile * c.g.tile * sizeof(float2) + WARPS * 32 * sizeof(RasterRec);
     static size_t configured = 0;
-    if (smem > 48 * 1024 && configured < smem)
+    if (configured < smem)
     {
-        check_cuda(cudaFuncSetAttribute(raster_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem),
+        check_cuda(cudaFuncSetAttribute(raster_kernel<WARPS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem),
                    "raster smem attribute");
+        // same L1/shared split as the MLP kernel, so raster CTAs can share its SMs
+        check_cuda(cudaFuncSetAttribute(raster_kernel<WARPS>, cudaFuncAttributePreferredSharedMemoryCarveout,
+                                        (int)cudaSharedmemCarveoutMaxShared),
+                   "raster carveout");
         configured = smem;
     }
-    raster_kernel<<<grid, 256, smem, st>>>(c.g, c.s, c.w.dyn, c.w.rng, c.w.seg, c.w.tile_off, c.w.sorted, d_spec,
-                                          c.w.tile_part, c.w.tile_sum, want_heads ? 1 : 0);
+    raster_kernel<WARPS><<<grid, 32 * WARPS, smem, st>>>(c.g, c.s, c.w.dyn, c.w.rng, c.w.seg, c.w.tile_off, c.w.sorted,
+                                                         d_spec, c.w.tile_part, c.w.tile_sum, want_heads ? 1 : 0);
     c.launches++;
+}
+
+// warps = 8 (standalone) or 4 (small enough to run beside the persistent MLP kernel)
+void launch_raster(Ctx &c, int nb, float *d_spec, bool want_heads, cudaStream_t st, int warps)
+{
+    if (warps == 4)
+        launch_raster_w<4>(c, nb, d_spec, want_heads, st);
+    else
+        launch_raster_w<8>(c, nb, d_spec, want_heads, st);
 }
 
 // Heads on given spectra: the same per-tile partials as the raster epilogue.
