@@ -32,6 +32,7 @@ enum swr_status
     SWR_EINVAL = 1,   /* std::invalid_argument in the reference (size / grid mismatch) */
     SWR_ERUNTIME = 2, /* std::runtime_error (I/O, magic, version) */
     SWR_ECUDA = 3,    /* device error (no sm_100 device, launch failure, OOM) */
+    SWR_EDOMAIN = 4,  /* std::domain_error (non-finite spectrum value in a metric, spectrum.cpp:44-49) */
 };
 
 /* render flags (swr_render / swr_render_device) */
@@ -124,6 +125,26 @@ int swr_rasterize(swr_ctx *ctx, const float *d_center, const float *d_response,
 /* Heads on caller spectra [B][H][W][2] (tasks.cpp:32-39, 154-169). */
 int swr_heads(swr_ctx *ctx, const float *spectra, int64_t B, double *pooled, int32_t *aoa_rc,
               double *aoa_ang);
+
+/* Evaluation metrics of predicted against target spectra, both [B][H][W][2] on
+ * the context's grid: PSNR in dB (clamped at 100, spectrum.cpp:145-161), SSIM
+ * (11x11 Gaussian window, per channel, averaged, spectrum.cpp:177-250), L1 mean
+ * absolute difference (spectrum.cpp:163-172); all statistics in double. Any
+ * output may be NULL (skips that metric). peak = the reference's `peak`
+ * argument (1.0 in train::evaluate). Replaces wrfsplat::psnr / ssim / l1.
+ * SWR_EDOMAIN on a non-finite value, SWR_EINVAL when the grid is below 11x11
+ * and SSIM is requested. Host buffers, synchronous: */
+int swr_metrics(swr_ctx *ctx, const float *pred, const float *target, int64_t B, double peak,
+                double *psnr, double *ssim, double *l1);
+/* same on device pointers (outputs too), ordered on `stream` (a cudaStream_t,
+ * NULL = the context's stream); returns after the work completes */
+int swr_metrics_device(swr_ctx *ctx, const float *d_pred, const float *d_target, int64_t B,
+                       double peak, double *d_psnr, double *d_ssim, double *d_l1, void *stream);
+/* train::evaluate (training.cpp:380-406) batched: render each TX position
+ * (metres, [B][3]) and score it against target[b] ([B][H][W][2], host); the
+ * spectra stay on the device, only the metrics come back. */
+int swr_evaluate(swr_ctx *ctx, const float *pos_m, const float *target, int64_t B, double peak,
+                 double *psnr, double *ssim, double *l1);
 
 /* Kernel launches issued by this context since creation (for the bench). */
 int64_t swr_launch_count(swr_ctx *ctx);

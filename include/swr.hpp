@@ -38,6 +38,8 @@ inline void check(int rc)
     const std::string msg = swr_last_error();
     if (rc == SWR_EINVAL)
         throw std::invalid_argument(msg);
+    if (rc == SWR_EDOMAIN)
+        throw std::domain_error(msg);
     throw std::runtime_error(msg);
 }
 } // namespace detail
@@ -182,5 +184,63 @@ inline double pooled_magnitude(const train::Checkpoint &ck, const Spectrum &s)
     return pooled;
 }
 } // namespace tasks
+
+// spectrum.hpp:73-84: evaluation metrics (the context supplies the grid)
+inline double psnr(const train::Checkpoint &ck, const Spectrum &a, const Spectrum &b, double peak = 1.0)
+{
+    if (a.data.size() != b.data.size())
+        throw std::invalid_argument("spectrum shape mismatch");
+    double v = 0.0;
+    detail::check(swr_metrics(ck.handle(), a.data.data(), b.data.data(), 1, peak, &v, nullptr, nullptr));
+    return v;
+}
+inline double ssim(const train::Checkpoint &ck, const Spectrum &a, const Spectrum &b, double peak = 1.0)
+{
+    if (a.data.size() != b.data.size())
+        throw std::invalid_argument("spectrum shape mismatch");
+    double v = 0.0;
+    detail::check(swr_metrics(ck.handle(), a.data.data(), b.data.data(), 1, peak, nullptr, &v, nullptr));
+    return v;
+}
+inline double l1(const train::Checkpoint &ck, const Spectrum &a, const Spectrum &b)
+{
+    if (a.data.size() != b.data.size())
+        throw std::invalid_argument("spectrum shape mismatch");
+    double v = 0.0;
+    detail::check(swr_metrics(ck.handle(), a.data.data(), b.data.data(), 1, 1.0, nullptr, nullptr, &v));
+    return v;
+}
+
+namespace train
+{
+// spectrum.hpp:99-104
+struct MetricRow
+{
+    int sample_id = 0;
+    double psnr_db = 0.0, ssim = 0.0, l1 = 0.0;
+};
+
+// train::evaluate (training.cpp:380-406) over (position, target spectrum) samples
+inline std::vector<MetricRow> evaluate(const Checkpoint &ck, const std::vector<std::array<float, 3>> &positions,
+                                       const std::vector<Spectrum> &targets)
+{
+    if (positions.size() != targets.size())
+        throw std::invalid_argument("one target spectrum per position");
+    const size_t B = positions.size();
+    std::vector<float> pos(3 * B), tgt;
+    for (size_t b = 0; b < B; b++)
+    {
+        for (int a = 0; a < 3; a++)
+            pos[3 * b + a] = positions[b][a];
+        tgt.insert(tgt.end(), targets[b].data.begin(), targets[b].data.end());
+    }
+    std::vector<double> p(B), s(B), l(B);
+    detail::check(swr_evaluate(ck.handle(), pos.data(), tgt.data(), (int64_t)B, 1.0, p.data(), s.data(), l.data()));
+    std::vector<MetricRow> rows(B);
+    for (size_t b = 0; b < B; b++)
+        rows[b] = {int(b), p[b], s[b], l[b]};
+    return rows;
+}
+} // namespace train
 
 } // namespace wrfsplat::b200

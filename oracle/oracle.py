@@ -135,6 +135,18 @@ class Port:
     def pooled(self, spec):
         return self.lib.so_pooled(_f(_c32(spec)), spec.shape[0] * spec.shape[1])
 
+    def metrics(self, pred, target, peak=1.0, ssim=True):
+        """(psnr, ssim, l1) of one spectrum pair (spectrum.cpp:145-250); ssim None if not asked."""
+        pred, target = _c32(pred), _c32(target)
+        out = [C.c_double(), C.c_double(), C.c_double()]
+        rc = self.lib.so_metrics(_f(pred), _f(target), pred.shape[0], pred.shape[1], C.c_double(peak),
+                                 C.byref(out[0]), C.byref(out[1]) if ssim else None, C.byref(out[2]))
+        if rc == 1:
+            raise ArithmeticError("spectrum contains a non-finite value")
+        if rc == 2:
+            raise ValueError("grid too small for the 11x11 SSIM window")
+        return out[0].value, (out[1].value if ssim else None), out[2].value
+
 
 class Reference:
     """The reference library built from /root/reference sources (oracle/_ref)."""
@@ -267,6 +279,17 @@ class Reference:
 
     def pooled(self, spec):
         return self.lib.wref_pooled(_f(_c32(spec)), spec.shape[0], spec.shape[1])
+
+    def metrics(self, pred, target, peak=1.0):
+        """(psnr, ssim, l1) through the reference's own psnr / ssim / l1."""
+        pred, target = _c32(pred), _c32(target)
+        out = np.zeros(3)
+        rc = self.lib.wref_metrics(_f(pred), _f(target), pred.shape[0], pred.shape[1], C.c_double(peak), _d(out))
+        if rc == 1:
+            raise ArithmeticError("spectrum contains a non-finite value")
+        if rc == 2:
+            raise ValueError("grid too small for the 11x11 SSIM window")
+        return tuple(out)
 
     def materialize_center(self, rel, raz, double=False):
         if double:

@@ -338,6 +338,28 @@ double wref_pooled(const float *spectrum, int H, int W)
     return tasks::pooled_magnitude(wrap_spectrum(spectrum, H, W));
 }
 
+// spectrum.cpp:145-250 on the reference's own functions: out = (psnr, ssim, l1).
+// Returns 0, 1 for std::domain_error (non-finite), 2 for std::invalid_argument.
+int wref_metrics(const float *a, const float *b, int H, int W, double peak, double *out)
+{
+    try
+    {
+        const auto sa = wrap_spectrum(a, H, W), sb = wrap_spectrum(b, H, W);
+        out[0] = psnr(sa, sb, peak);
+        out[2] = l1(sa, sb);
+        out[1] = ssim(sa, sb, peak);
+        return 0;
+    }
+    catch (const std::domain_error &)
+    {
+        return 1;
+    }
+    catch (const std::invalid_argument &)
+    {
+        return 2;
+    }
+}
+
 int wref_magnitude(const float *spectrum, int H, int W, float *out)
 {
     const auto m = magnitude(wrap_spectrum(spectrum, H, W));

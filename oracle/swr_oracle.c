@@ -489,3 +489,115 @@ double so_pooled(const float *spectrum, int cells)
         sum += (float)hypot((double)spectrum[2 * (size_t)k], (double)spectrum[2 * (size_t)k + 1]);
     return sum / (double)cells;
 }
+
+/* ------------------------------------------------------------------ metrics
+ * spectrum.cpp:145-250: psnr / l1 over all 2*H*W floats in double; SSIM per
+ * channel (re, im) with an 11x11 Gaussian window (sigma 1.5, unit sum,
+ * spectrum.cpp:51-70), valid-region separable correlation (spectrum.cpp:72-101),
+ * statistics in double, mean over windows, average of the two channels.
+ * Returns 0, or 1 for a non-finite input (the reference throws domain_error,
+ * spectrum.cpp:44-49), 2 for a grid smaller than the window (invalid_argument). */
+#define SO_WIN 11
+
+static void so_window_taps(double g[SO_WIN])
+{
+    double sum = 0.0;
+    for (int i = 0; i < SO_WIN; i++)
+    {
+        const double d = i - SO_WIN / 2;
+        g[i] = exp(-0.5 * d * d / (1.5 * 1.5));
+        sum += g[i];
+    }
+    for (int i = 0; i < SO_WIN; i++)
+        g[i] /= sum;
+}
+
+/* spectrum.cpp:72-101 (src H x W -> dst (H-10) x (W-10)) */
+static void so_conv_valid(const double *src, int h, int w, double *tmp, double *dst, const double *g)
+{
+    const int vw = w - SO_WIN + 1, vh = h - SO_WIN + 1;
+    for (size_t k = 0; k < (size_t)h * vw; k++)
+        tmp[k] = 0.0;
+    for (int i = 0; i < h; i++)
+        for (int t = 0; t < SO_WIN; t++)
+            for (int j = 0; j < vw; j++)
+                tmp[(size_t)i * vw + j] += g[t] * src[(size_t)i * w + j + t];
+    for (int i = 0; i < vh; i++)
+    {
+        double *out = dst + (size_t)i * vw;
+        for (int j = 0; j < vw; j++)
+            out[j] = 0.0;
+        for (int t = 0; t < SO_WIN; t++)
+            for (int j = 0; j < vw; j++)
+                out[j] += g[t] * tmp[(size_t)(i + t) * vw + j];
+    }
+}
+
+/* spectrum.cpp:177-238 without the gradient */
+static double so_ssim_channel(const float *x, const float *y, int h, int w, int c, double peak)
+{
+    const int vh = h - SO_WIN + 1, vw = w - SO_WIN + 1;
+    const size_t cells = (size_t)h * w, wins = (size_t)vh * vw;
+    const double c1 = (0.01 * peak) * (0.01 * peak), c2 = (0.03 * peak) * (0.03 * peak);
+    double g[SO_WIN];
+    so_window_taps(g);
+    double *xs = malloc(sizeof(double) * cells), *ys = malloc(sizeof(double) * cells);
+    double *prod = malloc(sizeof(double) * cells), *tmp = malloc(sizeof(double) * (size_t)h * vw);
+    double *mx = malloc(sizeof(double) * wins), *my = malloc(sizeof(double) * wins);
+    double *sxx = malloc(sizeof(double) * wins), *syy = malloc(sizeof(double) * wins);
+    double *sxy = malloc(sizeof(double) * wins);
+    for (size_t k = 0; k < cells; k++)
+    {
+        xs[k] = (double)x[2 * k + c];
+        ys[k] = (double)y[2 * k + c];
+    }
+    so_conv_valid(xs, h, w, tmp, mx, g);
+    so_conv_valid(ys, h, w, tmp, my, g);
+    for (size_t k = 0; k < cells; k++)
+        prod[k] = xs[k] * xs[k];
+    so_conv_valid(prod, h, w, tmp, sxx, g);
+    for (size_t k = 0; k < cells; k++)
+        prod[k] = ys[k] * ys[k];
+    so_conv_valid(prod, h, w, tmp, syy, g);
+    for (size_t k = 0; k < cells; k++)
+        prod[k] = xs[k] * ys[k];
+    so_conv_valid(prod, h, w, tmp, sxy, g);
+    double total = 0.0;
+    for (size_t k = 0; k < wins; k++)
+    {
+        const double ux = mx[k], uy = my[k];
+        const double vx = sxx[k] - ux * ux, vy = syy[k] - uy * uy, vxy = sxy[k] - ux * uy;
+        const double a1 = 2.0 * ux * uy + c1, a2 = 2.0 * vxy + c2;
+        const double b1 = ux * ux + uy * uy + c1, b2 = vx + vy + c2;
+        total += (a1 * a2) / (b1 * b2);
+    }
+    free(xs), free(ys), free(prod), free(tmp), free(mx), free(my), free(sxx), free(syy), free(sxy);
+    return total / (double)wins;
+}
+
+int so_metrics(const float *a, const float *b, int H, int W, double peak, double *psnr, double *ssim, double *l1)
+{
+    const size_t n = (size_t)2 * H * W;
+    for (size_t k = 0; k < n; k++)
+        if (!isfinite((double)a[k]) || !isfinite((double)b[k]))
+            return 1;
+    double mse = 0.0, sad = 0.0;
+    for (size_t k = 0; k < n; k++)
+    {
+        const double d = (double)a[k] - (double)b[k];
+        mse += d * d;
+        sad += fabs((double)a[k] - (double)b[k]);
+    }
+    mse /= (double)n;
+    if (psnr)
+        *psnr = mse <= 0.0 ? 100.0 : fmin(100.0, 10.0 * log10(peak * peak / mse)); /* spectrum.cpp:145-161 */
+    if (l1)
+        *l1 = sad / (double)n; /* spectrum.cpp:163-172 */
+    if (ssim)
+    {
+        if (H < SO_WIN || W < SO_WIN)
+            return 2;
+        *ssim = 0.5 * (so_ssim_channel(a, b, H, W, 0, peak) + so_ssim_channel(a, b, H, W, 1, peak));
+    }
+    return 0;
+}

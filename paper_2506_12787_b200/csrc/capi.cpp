@@ -53,6 +53,11 @@ static int guarded(F &&f)
         g_err = e.what();
         return SWR_EINVAL;
     }
+    catch (const std::domain_error &e)
+    {
+        g_err = e.what();
+        return SWR_EDOMAIN;
+    }
     catch (const cuda_error &e)
     {
         g_err = e.what();
@@ -1099,6 +1104,156 @@ int swr_heads(swr_ctx *ctx, const float *spectra, int64_t B, double *pooled, int
 }
 
 int64_t swr_launch_count(swr_ctx *ctx) { return ctx->c.launches; }
+
+// ------------------------------------------------------------- metrics
+
+static void metrics_workspace(Ctx &c, int nb)
+{
+    Work &w = c.w;
+    if (nb <= w.met_cap)
+        return;
+    for (void *p : {(void *)w.met_tmp, (void *)w.met_bad, (void *)w.met_out, (void *)w.met_pred, (void *)w.met_target})
+        dfree(c, p);
+    const size_t per = size_t(2) * c.g.H * c.g.W;
+    w.met_tmp = dalloc<double>(c, metrics_tmp_doubles(c, nb));
+    w.met_bad = dalloc<int>(c, 1);
+    w.met_out = dalloc<double>(c, size_t(3) * nb);
+    w.met_pred = dalloc<float>(c, per * nb);
+    w.met_target = dalloc<float>(c, per * nb);
+    w.met_cap = nb;
+}
+
+static void check_metric_args(const Ctx &c, bool want_ssim)
+{
+    if (want_ssim && (c.g.H < 11 || c.g.W < 11))
+        throw std::invalid_argument("grid too small for the 11x11 SSIM window");
+}
+
+static void raise_if_nonfinite(Ctx &c, cudaStream_t st)
+{
+    int bad = 0;
+    check_cuda(cudaMemcpyAsync(&bad, c.w.met_bad, sizeof(int), cudaMemcpyDeviceToHost, st), "D2H metric flag");
+    check_cuda(cudaStreamSynchronize(st), "metrics");
+    if (bad)
+        throw std::domain_error("spectrum contains a non-finite value");
+}
+
+int swr_metrics_device(swr_ctx *ctx, const float *d_pred, const float *d_target, int64_t B, double peak,
+                       double *d_psnr, double *d_ssim, double *d_l1, void *stream)
+{
+    return guarded([&] {
+        Ctx &c = ctx->c;
+        if (B < 0)
+            throw std::invalid_argument("negative batch");
+        check_metric_args(c, d_ssim != nullptr);
+        if (B == 0)
+            return;
+        check_cuda(cudaSetDevice(c.device), "cudaSetDevice");
+        cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : c.stream;
+        const int64_t chunk = std::max<int64_t>(1, std::min<int64_t>(B, c.chunk));
+        metrics_workspace(c, int(chunk));
+        check_cuda(cudaMemsetAsync(c.w.met_bad, 0, sizeof(int), st), "memset");
+        const size_t per = size_t(2) * c.g.H * c.g.W;
+        for (int64_t b0 = 0; b0 < B; b0 += chunk)
+        {
+            const int nb = int(std::min<int64_t>(chunk, B - b0));
+            launch_metrics(c, d_pred + per * b0, d_target + per * b0, nb, peak, d_psnr ? d_psnr + b0 : nullptr,
+                           d_ssim ? d_ssim + b0 : nullptr, d_l1 ? d_l1 + b0 : nullptr, c.w.met_tmp, c.w.met_bad, st);
+        }
+        check_cuda(cudaGetLastError(), "metrics launch");
+        raise_if_nonfinite(c, st);
+    });
+}
+
+// host buffers: per chunk H2D of both spectra, metrics on device, D2H of 3 doubles per pair
+int swr_metrics(swr_ctx *ctx, const float *pred, const float *target, int64_t B, double peak, double *psnr,
+                double *ssim, double *l1)
+{
+    return guarded([&] {
+        Ctx &c = ctx->c;
+        if (B < 0)
+            throw std::invalid_argument("negative batch");
+        check_metric_args(c, ssim != nullptr);
+        if (B == 0)
+            return;
+        check_cuda(cudaSetDevice(c.device), "cudaSetDevice");
+        cudaStream_t st = c.stream;
+        const int64_t chunk = std::max<int64_t>(1, std::min<int64_t>(B, c.chunk));
+        metrics_workspace(c, int(chunk));
+        check_cuda(cudaMemsetAsync(c.w.met_bad, 0, sizeof(int), st), "memset");
+        const size_t per = size_t(2) * c.g.H * c.g.W;
+        double *o = c.w.met_out;
+        for (int64_t b0 = 0; b0 < B; b0 += chunk)
+        {
+            const int nb = int(std::min<int64_t>(chunk, B - b0));
+            check_cuda(cudaMemcpyAsync(c.w.met_pred, pred + per * b0, sizeof(float) * per * nb, cudaMemcpyHostToDevice,
+                                       st),
+                       "H2D prediction");
+            check_cuda(cudaMemcpyAsync(c.w.met_target, target + per * b0, sizeof(float) * per * nb,
+                                       cudaMemcpyHostToDevice, st),
+                       "H2D target");
+            launch_metrics(c, c.w.met_pred, c.w.met_target, nb, peak, o, ssim ? o + chunk : nullptr, o + 2 * chunk,
+                           c.w.met_tmp, c.w.met_bad, st);
+            for (int k = 0; k < 3; k++)
+            {
+                double *dst = k == 0 ? psnr : (k == 1 ? ssim : l1);
+                if (dst)
+                    check_cuda(cudaMemcpyAsync(dst + b0, o + k * chunk, sizeof(double) * nb, cudaMemcpyDeviceToHost, st),
+                               "D2H metrics");
+            }
+            check_cuda(cudaStreamSynchronize(st), "metrics chunk");
+        }
+        raise_if_nonfinite(c, st);
+    });
+}
+
+// train::evaluate (training.cpp:380-406) batched: render every position and
+// compare with its target spectrum on the device; only the 3 metrics per
+// sample come back (the spectra never leave the GPU)
+int swr_evaluate(swr_ctx *ctx, const float *pos_m, const float *target, int64_t B, double peak, double *psnr,
+                 double *ssim, double *l1)
+{
+    return guarded([&] {
+        Ctx &c = ctx->c;
+        if (B < 0)
+            throw std::invalid_argument("negative batch");
+        check_metric_args(c, ssim != nullptr);
+        if (B == 0)
+            return;
+        check_cuda(cudaSetDevice(c.device), "cudaSetDevice");
+        cudaStream_t st = c.stream;
+        const int64_t chunk = std::max<int64_t>(1, std::min<int64_t>(B, c.chunk));
+        ensure_work(c, chunk);
+        metrics_workspace(c, int(chunk));
+        check_cuda(cudaMemsetAsync(c.w.met_bad, 0, sizeof(int), st), "memset");
+        const size_t per = size_t(2) * c.g.H * c.g.W;
+        float *d_pos = dalloc<float>(c, size_t(3) * B);
+        check_cuda(cudaMemcpyAsync(d_pos, pos_m, sizeof(float) * 3 * B, cudaMemcpyHostToDevice, st), "H2D positions");
+        const bool use_mlp = c.has_net;
+        double *o = c.w.met_out;
+        for (int64_t b0 = 0; b0 < B; b0 += chunk)
+        {
+            const int nb = int(std::min<int64_t>(chunk, B - b0));
+            check_cuda(cudaMemcpyAsync(c.w.met_target, target + per * b0, sizeof(float) * per * nb,
+                                       cudaMemcpyHostToDevice, st),
+                       "H2D target");
+            run_chunk(c, d_pos + 3 * b0, nb, false, use_mlp, false, c.w.met_pred, false, 0, nullptr, nullptr, nullptr,
+                      nullptr, st);
+            launch_metrics(c, c.w.met_pred, c.w.met_target, nb, peak, o, ssim ? o + chunk : nullptr, o + 2 * chunk,
+                           c.w.met_tmp, c.w.met_bad, st);
+            for (int k = 0; k < 3; k++)
+            {
+                double *dst = k == 0 ? psnr : (k == 1 ? ssim : l1);
+                if (dst)
+                    check_cuda(cudaMemcpyAsync(dst + b0, o + k * chunk, sizeof(double) * nb, cudaMemcpyDeviceToHost, st),
+                               "D2H metrics");
+            }
+            check_cuda(cudaStreamSynchronize(st), "evaluate chunk");
+        }
+        dfree(c, d_pos);
+        raise_if_nonfinite(c, st);
+    });
+}
 
 // debug: clock64 trace of the tensor-core MLP (SWR_TC_DEBUG & 8), 3x8x80 stamps
 int swr_debug_mlp_trace(long long *out)

@@ -77,6 +77,11 @@ struct Work
     float4 *tile_part = nullptr; // [cap_b][tiles] (max |A|, argmax cell as float bits, sum |A| hi, lo)
     double *tile_sum = nullptr; // [cap_b][tiles]
     int64_t *stats = nullptr;      // device: (total pairs, longest segment) of the current chunk
+    // evaluation metrics (k_metrics.cu): SSIM scratch, non-finite flag, outputs, staging
+    int met_cap = 0;
+    double *met_tmp = nullptr, *met_out = nullptr;
+    int *met_bad = nullptr;
+    float *met_pred = nullptr, *met_target = nullptr;
     int64_t *host_pairs = nullptr; // pinned mirror of stats
 };
 
@@ -122,6 +127,9 @@ void prepare_tc_weights(Ctx &c, const std::vector<float> &whT, const std::vector
                         const std::vector<float> &heads, const std::vector<float> &cenc);
 void launch_mlp_tc(Ctx &c, int nb, cudaStream_t st);
 int mlp_tc_trace(long long *out);
+size_t metrics_tmp_doubles(const Ctx &c, int nb);
+void launch_metrics(Ctx &c, const float *d_pred, const float *d_target, int nb, double peak, double *d_psnr,
+                    double *d_ssim, double *d_l1, double *d_tmp, int *d_bad, cudaStream_t st);
 
 void check_cuda(cudaError_t e, const char *what);
 

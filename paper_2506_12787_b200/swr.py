@@ -64,6 +64,12 @@ def lib():
         L.swr_rasterize.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p]
         L.swr_heads.argtypes = [C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p, C.c_void_p, C.c_void_p]
         L.swr_stage_times.argtypes = [C.c_void_p, C.c_void_p]
+        L.swr_metrics.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64, C.c_double, C.c_void_p,
+                                  C.c_void_p, C.c_void_p]
+        L.swr_metrics_device.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64, C.c_double, C.c_void_p,
+                                         C.c_void_p, C.c_void_p, C.c_void_p]
+        L.swr_evaluate.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64, C.c_double, C.c_void_p,
+                                   C.c_void_p, C.c_void_p]
         L.swr_scene_get_info.argtypes = [C.c_void_p, C.c_void_p]
         L.swr_scene_create_wrfc.argtypes = [C.c_char_p, C.c_int, C.POINTER(C.c_void_p)]
         L.swr_scene_create.argtypes = [C.c_int, C.c_int, C.c_int, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
@@ -79,6 +85,8 @@ def _check(rc: int) -> None:
     msg = lib().swr_last_error().decode()
     if rc == 1:
         raise ValueError(msg)
+    if rc == 4:
+        raise ArithmeticError(msg)  # std::domain_error (non-finite metric input)
     raise SwrError(msg)
 
 
@@ -286,3 +294,31 @@ def pooled_magnitude(ck: Checkpoint, spectra) -> np.ndarray:
 def aoa_extract(ck: Checkpoint, spectra):
     _, rc, ang = heads(ck, spectra)
     return rc, ang
+
+
+def metrics(ck: Checkpoint, pred, target, peak: float = 1.0, ssim: bool = True):
+    """psnr / ssim / l1 per spectrum pair (spectrum.cpp:145-250), [B] each."""
+    a = _f32(pred).reshape(-1, ck.H, ck.W, 2)
+    b = _f32(target).reshape(-1, ck.H, ck.W, 2)
+    if a.shape != b.shape:
+        raise ValueError("spectrum shape mismatch")
+    B = a.shape[0]
+    out = {k: np.zeros(B, np.float64) for k in ("psnr", "ssim", "l1")}
+    _check(lib().swr_metrics(ck.handle, _p(a), _p(b), B, float(peak), _p(out["psnr"]),
+                             _p(out["ssim"]) if ssim else None, _p(out["l1"])))
+    if not ssim:
+        out.pop("ssim")
+    return out
+
+
+def evaluate(ck: Checkpoint, positions, targets, peak: float = 1.0):
+    """train::evaluate (training.cpp:380-406) on a batch: render + score on the device."""
+    pos = _f32(positions).reshape(-1, 3)
+    t = _f32(targets).reshape(-1, ck.H, ck.W, 2)
+    if t.shape[0] != pos.shape[0]:
+        raise ValueError("one target spectrum per position")
+    B = pos.shape[0]
+    out = {k: np.zeros(B, np.float64) for k in ("psnr", "ssim", "l1")}
+    _check(lib().swr_evaluate(ck.handle, _p(pos), _p(t), B, float(peak), _p(out["psnr"]), _p(out["ssim"]),
+                              _p(out["l1"])))
+    return out
