@@ -580,13 +580,14 @@ __device__ __forceinline__ float wrap_fast(float x)
 // For a chunk, each lane first prepares one pair (gathers its dynamic state,
 // shape and box, clips the box to the tile: rows [max(r0, tile), min(r1, tile)]
 // x the one or two wrapped column spans, splat.cpp:450-470) into a per-warp
-// record in shared memory; then the whole warp evaluates the records one by
-// one with its lanes mapped onto the clipped box only (lane -> (row, column)
-// from a small table, rows-per-sweep = 32 / columns), so no lane is spent on
-// cells the reference does not evaluate and the per-pair setup costs one lane,
-// not a warp. Each warp accumulates into its own shared-memory copy of the tile
-// (no atomics); the eight copies are summed in fixed warp order at the end, so
-// the result is bit-deterministic. The cutoff mask uses the reference's float q
+// record in shared memory, and the warp sorts its 32 records by sweep count
+// (bitonic, shuffles). Then each half-warp evaluates one record of a
+// similar-sized pair of records at a time, its 16 lanes mapped onto the clipped
+// box only (rows per sweep = 16 / columns), so no lane is spent on cells the
+// reference does not evaluate and the per-pair setup costs one lane. Each
+// half-warp accumulates into its own shared-memory copy of the tile (no
+// atomics); the copies are summed in fixed order at the end, so the result is
+// bit-deterministic. The cutoff mask uses the reference's float q
 // (same operation order, no FMA); exp(-q/2) is ex2.approx of a prescaled
 // argument.
 struct RasterRec
@@ -599,14 +600,16 @@ struct RasterRec
 // floor(x / d) == (x * m[d]) >> 12 for 0 <= x < 128, 1 <= d <= 32, m[d] = ceil(4096 / d)
 __host__ __device__ constexpr uint32_t magic12(int d) { return (4096u + d - 1) / d; }
 
-template <int kRasterWarps>
+// G = records evaluated side by side per warp: 2 (half-warps, tiles <= 16 wide) or
+// 1 (whole warp, tiles up to 32 wide)
+template <int kRasterWarps, int G>
 __global__ void __launch_bounds__(32 * kRasterWarps) raster_kernel(Grid g, SceneDev sd, const float4 *__restrict__ dyn,
                                                      const int4 *__restrict__ rng, const int64_t *__restrict__ seg,
                                                      const int *__restrict__ tile_off, const int *__restrict__ prims,
                                                      float *__restrict__ spec, float4 *__restrict__ tile_part,
                                                      double *__restrict__ tile_sum, int want_heads)
 {
-    extern __shared__ float2 acc[]; // [8][T*T], then RasterRec [8][32]
+    extern __shared__ float2 acc[]; // [2 * warps][T*T], then RasterRec [warps][32]
     __shared__ float elc[64], azc[32]; // elc zero-padded: a lane's last sweep may run past the tile
     __shared__ uint32_t magic[33];
     const int T = g.tile, TT = T * T;
@@ -614,8 +617,11 @@ __global__ void __launch_bounds__(32 * kRasterWarps) raster_kernel(Grid g, Scene
     const int tr0 = (t / g.tw) * T, tc0 = (t % g.tw) * T;
     const int tr1 = min(tr0 + T, g.H) - 1, tc1 = min(tc0 + T, g.W) - 1;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    RasterRec *recs = reinterpret_cast<RasterRec *>(acc + kRasterWarps * TT) + warp * 32;
-    for (int i = threadIdx.x; i < kRasterWarps * TT; i += blockDim.x)
+    constexpr int LPR = 32 / G; // lanes per record
+    RasterRec *recs = reinterpret_cast<RasterRec *>(acc + G * kRasterWarps * TT) + warp * 32;
+    __shared__ uint8_t order_all[kRasterWarps * 32]; // per warp: records sorted by sweep count
+    uint8_t *order = order_all + warp * 32;
+    for (int i = threadIdx.x; i < G * kRasterWarps * TT; i += blockDim.x)
         acc[i] = make_float2(0.f, 0.f);
     if (threadIdx.x < 64)
         elc[threadIdx.x] = (int)threadIdx.x < T && tr0 + (int)threadIdx.x <= tr1 ? sd.el_c[tr0 + threadIdx.x] : 0.f;
@@ -627,7 +633,8 @@ __global__ void __launch_bounds__(32 * kRasterWarps) raster_kernel(Grid g, Scene
     const int *tl = tile_off + (int64_t)s * (g.tiles + 1);
     const int64_t lb = seg[s] + tl[t], le = seg[s] + tl[t + 1];
     const int64_t sbase = (int64_t)s * g.np;
-    float2 *my = acc + warp * TT;
+    const int half = G == 2 ? lane >> 4 : 0, hl = lane & (LPR - 1); // record slot and its lane
+    float2 *my = acc + (G * warp + half) * TT;
     const uint32_t acc_base = (uint32_t)__cvta_generic_to_shared(my);
     const uint32_t el_base = (uint32_t)__cvta_generic_to_shared(elc);
     const float cut2 = g.cut2;
@@ -664,7 +671,7 @@ __global__ void __launch_bounds__(32 * kRasterWarps) raster_kernel(Grid g, Scene
             if (gi >= 0 && ncol > 0 && nrow > 0)
             {
                 mn = magic[ncol];
-                rpi = (int)((32u * mn) >> 12); // rows per sweep
+                rpi = (int)(((uint32_t)LPR * mn) >> 12); // rows per sweep of LPR lanes
                 mr = magic[rpi];
                 sweeps = (int)(((uint32_t)(nrow + rpi - 1) * mr) >> 12);
             }
@@ -675,6 +682,18 @@ __global__ void __launch_bounds__(32 * kRasterWarps) raster_kernel(Grid g, Scene
             r.box = make_int4(pr0 - tr0, pr1 - tr0, ncol | (na << 6) | (a0off << 12) | (rpi << 18) | (sweeps << 24),
                               (int)(mn | (mr << 13)));
             recs[lane] = r;
+            // sort (sweeps, lane) ascending across the warp: similar records pair up
+            uint32_t key = ((uint32_t)sweeps << 5) | (uint32_t)lane;
+#pragma unroll
+            for (int k = 2; k <= 32; k <<= 1)
+#pragma unroll
+                for (int jj = k >> 1; jj > 0; jj >>= 1)
+                {
+                    const uint32_t o = __shfl_xor_sync(0xffffffffu, key, jj);
+                    const bool up = (lane & k) == 0, lower = (lane & jj) == 0;
+                    key = (lower == up) ? min(key, o) : max(key, o);
+                }
+            order[lane] = (uint8_t)(key & 31);
         }
         // prefetch the pairs of this warp's next chunk
         const int cn = c0 + kRasterWarps * 32;
@@ -683,33 +702,34 @@ __global__ void __launch_bounds__(32 * kRasterWarps) raster_kernel(Grid g, Scene
         d = gi >= 0 ? dyn_s[gi] : make_float4(0.f, 0.f, 0.f, 0.f);
         sh = gi >= 0 ? sd.shape[gi] : make_float4(0.f, 0.f, 0.f, 0.f);
         __syncwarp();
-        const int nrec = min(32, cnt - c0);
 #pragma unroll 1
-        for (int j = 0; j < nrec; j++)
+        for (int j = 0; j < 32 / G; j++)
         {
-            const int4 bx = recs[j].box;
+            const RasterRec &R = recs[order[G * j + half]]; // this slot's record
+            const int4 bx = R.box;
             const int sweeps = bx.z >> 24;
-            if (sweeps == 0)
+            const int loop = G == 2 ? max(sweeps, __shfl_xor_sync(0xffffffffu, sweeps, 16)) : sweeps;
+            if (loop == 0)
                 continue;
-            const float4 A = recs[j].dyn, S = recs[j].shape;
+            const float4 A = R.dyn, S = R.shape;
             const int ncol = bx.z & 63, na = (bx.z >> 6) & 63, a0off = (bx.z >> 12) & 63, rpi = (bx.z >> 18) & 63;
             const uint32_t mn = (uint32_t)bx.w & 0x1fffu, mr = (uint32_t)bx.w >> 13;
-            const int lr = (int)(((uint32_t)lane * mn) >> 12), lc = lane - lr * ncol;
-            const bool lane_on = lr < rpi;
-            const int cc = lc < na ? a0off + lc : lc - na; // column inside the tile
+            const int lr = (int)(((uint32_t)hl * mn) >> 12), lc = hl - lr * ncol;
+            const bool lane_on = sweeps > 0 && lr < rpi;
+            const int cc = lane_on ? (lc < na ? a0off + lc : lc - na) : 0; // column inside the tile
             const float d_az = wrap_fast(__fsub_rn(azc[cc], A.y));
             const float w1 = __fmul_rn(__fmul_rn(S.z, d_az), d_az);
             const float w2 = __fmul_rn(S.y, d_az); // (2 * i01) * d_az
             // lane-private pointers (32-bit shared addresses): its row's el centre and
             // its cell; both advance by rpi rows per sweep
-            const int rr0 = bx.x + lr;
+            const int rr0 = lane_on ? bx.x + lr : 0;
             uint32_t elp = el_base + 4u * (uint32_t)rr0;
             uint32_t cp = acc_base + 8u * (uint32_t)(rr0 * T + cc);
-            const uint32_t el_step = 4u * (uint32_t)rpi, c_step = 8u * (uint32_t)(rpi * T);
+            const uint32_t el_step = lane_on ? 4u * (uint32_t)rpi : 0u, c_step = lane_on ? 8u * (uint32_t)(rpi * T) : 0u;
             // sweeps in which this lane's row is inside the box
             const int nvalid = lane_on ? (int)(((uint32_t)(bx.y - rr0 + rpi) * mr) >> 12) : 0;
 #pragma unroll 2
-            for (int it = 0; it < sweeps; it++, elp += el_step, cp += c_step)
+            for (int it = 0; it < loop; it++, elp += el_step, cp += c_step)
             {
                 float elv;
                 asm volatile("ld.shared.f32 %0, [%1];" : "=f"(elv) : "r"(elp));
@@ -745,7 +765,7 @@ __global__ void __launch_bounds__(32 * kRasterWarps) raster_kernel(Grid g, Scene
             continue;
         float re = 0.f, im = 0.f;
 #pragma unroll
-        for (int w = 0; w < kRasterWarps; w++)
+        for (int w = 0; w < G * kRasterWarps; w++)
         {
             const float2 v = acc[w * TT + cl];
             re = __fadd_rn(re, v.x);
@@ -769,34 +789,38 @@ __global__ void __launch_bounds__(32 * kRasterWarps) raster_kernel(Grid g, Scene
         heads_reduce(best, bidx, lsum, tile_part + (int64_t)s * g.tiles + t, tile_sum + (int64_t)s * g.tiles + t);
 }
 
-template <int WARPS>
+template <int WARPS, int G>
 static void launch_raster_w(Ctx &c, int nb, float *d_spec, bool want_heads, cudaStream_t st)
 {
     dim3 grid(c.g.tiles, nb);
-    const size_t smem = (size_t)WARPS * c.g.tile * c.g.tile * sizeof(float2) + WARPS * 32 * sizeof(RasterRec);
+    const size_t smem = (size_t)G * WARPS * c.g.tile * c.g.tile * sizeof(float2) + WARPS * 32 * sizeof(RasterRec);
     static size_t configured = 0;
     if (configured < smem)
     {
-        check_cuda(cudaFuncSetAttribute(raster_kernel<WARPS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem),
+        check_cuda(cudaFuncSetAttribute(raster_kernel<WARPS, G>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        (int)smem),
                    "raster smem attribute");
         // same L1/shared split as the MLP kernel, so raster CTAs can share its SMs
-        check_cuda(cudaFuncSetAttribute(raster_kernel<WARPS>, cudaFuncAttributePreferredSharedMemoryCarveout,
+        check_cuda(cudaFuncSetAttribute(raster_kernel<WARPS, G>, cudaFuncAttributePreferredSharedMemoryCarveout,
                                         (int)cudaSharedmemCarveoutMaxShared),
                    "raster carveout");
         configured = smem;
     }
-    raster_kernel<WARPS><<<grid, 32 * WARPS, smem, st>>>(c.g, c.s, c.w.dyn, c.w.rng, c.w.seg, c.w.tile_off, c.w.sorted,
-                                                         d_spec, c.w.tile_part, c.w.tile_sum, want_heads ? 1 : 0);
+    raster_kernel<WARPS, G><<<grid, 32 * WARPS, smem, st>>>(c.g, c.s, c.w.dyn, c.w.rng, c.w.seg, c.w.tile_off,
+                                                            c.w.sorted, d_spec, c.w.tile_part, c.w.tile_sum,
+                                                            want_heads ? 1 : 0);
     c.launches++;
 }
 
-// warps = 8 (standalone) or 4 (small enough to run beside the persistent MLP kernel)
+// warps = 8 (standalone) or 4 (small enough to run beside the persistent MLP kernel);
+// two records per warp when a tile row fits in 16 lanes
 void launch_raster(Ctx &c, int nb, float *d_spec, bool want_heads, cudaStream_t st, int warps)
 {
+    const bool narrow = c.g.tile <= 16;
     if (warps == 4)
-        launch_raster_w<4>(c, nb, d_spec, want_heads, st);
+        narrow ? launch_raster_w<4, 2>(c, nb, d_spec, want_heads, st) : launch_raster_w<4, 1>(c, nb, d_spec, want_heads, st);
     else
-        launch_raster_w<8>(c, nb, d_spec, want_heads, st);
+        narrow ? launch_raster_w<8, 2>(c, nb, d_spec, want_heads, st) : launch_raster_w<8, 1>(c, nb, d_spec, want_heads, st);
 }
 
 // Heads on given spectra: the same per-tile partials as the raster epilogue.

@@ -77,7 +77,8 @@ def test_bins_bit_exact(scene2k, ck2k):
 
 
 @pytest.mark.parametrize("cutoff,H,W,tile", [(0.0, 12, 24, 16), (3.0, 16, 32, 8), (1.0, 45, 90, 16),
-                                             (3.0, 90, 360, 16), (5.0, 30, 50, 7)])
+                                             (3.0, 90, 360, 16), (5.0, 30, 50, 7), (3.0, 90, 360, 32),
+                                             (2.0, 40, 100, 24)])
 def test_bins_bit_exact_grids(cutoff, H, W, tile):
     sc = make_scene(400, seed=5, H=H, W=W, width=16, cutoff=cutoff, tile=tile)
     ck = swr.Checkpoint.from_scene(sc)
