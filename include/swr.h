@@ -146,6 +146,38 @@ int swr_metrics_device(swr_ctx *ctx, const float *d_pred, const float *d_target,
 int swr_evaluate(swr_ctx *ctx, const float *pos_m, const float *target, int64_t B, double peak,
                  double *psnr, double *ssim, double *l1);
 
+/* ------------------------------------------------------------ datasets
+ * Reader of the reference's dataset directory (manifest.json + spectra.bin,
+ * wavesim.hpp:159-163; load_dataset, dataset.cpp:205-258): validates the
+ * manifest and the file size like load_dataset (SWR_ERUNTIME otherwise) and
+ * serves records by sample index without loading the whole file. Host only
+ * (no device needed). */
+typedef struct swr_dataset swr_dataset;
+typedef struct
+{
+    int n_elevation, n_azimuth;
+    int64_t samples, n_train, n_test, n_excluded;
+    uint64_t manifest_hash; /* FNV-1a 64 of the manifest bytes (common.cpp:40-48) */
+    double normalization;
+    double bbox_min[3], bbox_max[3];
+} swr_dataset_info;
+int swr_dataset_open(const char *dir, swr_dataset **out);
+void swr_dataset_close(swr_dataset *ds);
+int swr_dataset_get_info(swr_dataset *ds, swr_dataset_info *info);
+/* split: 0 train, 1 test, 2 all (training.cpp:145-160); indices may be NULL (count only) */
+int swr_dataset_split(swr_dataset *ds, int split, int32_t *indices, int64_t *count);
+/* records by index (NULL indices = the first `count`): pos [count][3], spectra [count][H][W][2] */
+int swr_dataset_read(swr_dataset *ds, const int32_t *indices, int64_t count, float *pos, float *spectra);
+/* train::evaluate (training.cpp:380-406): render every sample of the split and
+ * score it against its stored spectrum (peak 1). sample_ids / metrics are
+ * [split size]. SWR_ERUNTIME if the checkpoint's manifest_hash differs from the
+ * dataset's (train::hash_mismatch). */
+int swr_evaluate_dataset(swr_ctx *ctx, swr_dataset *ds, int split, int32_t *sample_ids, double *psnr,
+                         double *ssim, double *l1);
+/* the dataset fingerprint of a scene built from arrays (swr_scene_create_wrfc reads it
+ * from the checkpoint trailer, checkpoint.cpp:133) */
+int swr_scene_set_manifest_hash(swr_ctx *ctx, uint64_t hash);
+
 /* Kernel launches issued by this context since creation (for the bench). */
 int64_t swr_launch_count(swr_ctx *ctx);
 

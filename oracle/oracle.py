@@ -280,6 +280,23 @@ class Reference:
     def pooled(self, spec):
         return self.lib.wref_pooled(_f(_c32(spec)), spec.shape[0], spec.shape[1])
 
+    def set_dataset(self, manifest_hash, bbox6):
+        """Bind the checkpoint to a dataset: its manifest hash and normalisation box."""
+        b = np.asarray(bbox6, np.float64)
+        self.lib.wref_ck_set_dataset(self.h, C.c_uint64(manifest_hash), _d(b))
+
+    def evaluate(self, dataset_dir, split):
+        """train::evaluate (training.cpp:380-406): rows [n][4] = (sample id, psnr, ssim, l1)."""
+        L = self.lib
+        L.wref_evaluate.restype = C.c_longlong
+        rows = np.zeros((65536, 4))
+        n = L.wref_evaluate(self.h, dataset_dir.encode(), int(split), _d(rows), C.c_longlong(len(rows)))
+        if n == -2:
+            raise RuntimeError("hash mismatch: " + L.wref_last_error().decode())
+        if n < 0:
+            raise RuntimeError(L.wref_last_error().decode())
+        return rows[:n]
+
     def metrics(self, pred, target, peak=1.0):
         """(psnr, ssim, l1) through the reference's own psnr / ssim / l1."""
         pred, target = _c32(pred), _c32(target)
@@ -299,3 +316,30 @@ class Reference:
             el, az = C.c_float(), C.c_float()
             self.lib.wref_materialize_center_f(C.c_float(rel), C.c_float(raz), C.byref(el), C.byref(az))
         return el.value, az.value
+
+
+def make_dataset(dataset_dir, H, W, count, seed):
+    """Simulate + save a dataset with the reference's own wavesim / dataset code
+    (dataset.cpp:61-203); returns (manifest hash, bbox [6])."""
+    L = C.CDLL(REF_SO)
+    h = C.c_uint64()
+    bbox = np.zeros(6)
+    if L.wref_make_dataset(dataset_dir.encode(), H, W, count, C.c_uint64(seed), C.byref(h), _d(bbox)) != 0:
+        L.wref_last_error.restype = C.c_char_p
+        raise RuntimeError(L.wref_last_error().decode())
+    return h.value, bbox
+
+
+def load_dataset(dataset_dir, H, W):
+    """The reference's load_dataset (dataset.cpp:205-258): (hash, positions, spectra)."""
+    L = C.CDLL(REF_SO)
+    L.wref_dataset_load.restype = C.c_longlong
+    h = C.c_uint64()
+    n = L.wref_dataset_load(dataset_dir.encode(), C.byref(h), None, None, C.c_longlong(0))
+    if n < 0:
+        L.wref_last_error.restype = C.c_char_p
+        raise RuntimeError(L.wref_last_error().decode())
+    pos = np.zeros((n, 3), np.float32)
+    spec = np.zeros((n, H, W, 2), np.float32)
+    L.wref_dataset_load(dataset_dir.encode(), C.byref(h), _f(pos), _f(spec), C.c_longlong(n))
+    return h.value, pos, spec

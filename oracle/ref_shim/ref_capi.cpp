@@ -20,6 +20,7 @@
 #include "wrfsplat/splat.hpp"
 #include "wrfsplat/tasks.hpp"
 #include "wrfsplat/training.hpp"
+#include "wrfsplat/wavesim.hpp"
 
 using namespace wrfsplat;
 
@@ -427,6 +428,90 @@ void *wref_ck_init_random(int H, int W, int n, unsigned long long seed)
         return nullptr;
     }
     return ck;
+}
+
+// ----------------------------------------------------------- datasets
+// Simulate a dataset with the reference's own physics (default shoebox scene,
+// positions sampled 0.3 m from the walls) and save it (dataset.cpp:61-157, 184-203).
+int wref_make_dataset(const char *dir, int H, int W, int count, unsigned long long seed,
+                      unsigned long long *hash, double *bbox6)
+{
+    return guarded([&] {
+        sim::Scene scene;
+        Rng rng(seed);
+        const auto positions = sim::sample_positions(scene, count, 0.3, rng);
+        const auto ds = sim::generate_dataset(scene, AngularGrid{H, W}, positions, seed);
+        sim::save_dataset(ds, dir);
+        *hash = ds.manifest_hash;
+        for (int a = 0; a < 3; a++)
+        {
+            bbox6[a] = ds.bbox_min[std::size_t(a)];
+            bbox6[3 + a] = ds.bbox_max[std::size_t(a)];
+        }
+    });
+}
+
+// load_dataset (dataset.cpp:205-258): sample count, hash, and the records in file order
+long long wref_dataset_load(const char *dir, unsigned long long *hash, float *pos, float *spectra, long long cap)
+{
+    long long n = -1;
+    guarded([&] {
+        const auto ds = sim::load_dataset(dir);
+        *hash = ds.manifest_hash;
+        n = (long long)ds.samples.size();
+        if (pos && spectra)
+            for (long long i = 0; i < n && i < cap; i++)
+            {
+                const auto &smp = ds.samples[std::size_t(i)];
+                std::memcpy(pos + 3 * i, smp.position.data(), 12);
+                std::memcpy(spectra + i * smp.spectrum.data.size(), smp.spectrum.data.data(),
+                            4 * smp.spectrum.data.size());
+            }
+    });
+    return n;
+}
+
+void wref_ck_set_dataset(void *h, unsigned long long hash, const double *bbox6)
+{
+    auto &ck = *ck_of(h);
+    ck.manifest_hash = hash;
+    for (int a = 0; a < 3; a++)
+    {
+        ck.bbox_min[std::size_t(a)] = bbox6[a];
+        ck.bbox_max[std::size_t(a)] = bbox6[3 + a];
+    }
+}
+
+// train::evaluate (training.cpp:380-406) on a saved dataset: rows [n][4] =
+// (sample id, psnr, ssim, l1); returns the row count (-1 on error, -2 on hash mismatch)
+long long wref_evaluate(void *h, const char *dir, int split, double *rows, long long cap)
+{
+    long long n = -1;
+    try
+    {
+        const auto ds = sim::load_dataset(dir);
+        const auto r = train::evaluate(*ck_of(h), ds, split == 0 ? train::Split::train
+                                                                 : split == 1 ? train::Split::test : train::Split::all);
+        n = (long long)r.size();
+        for (long long i = 0; i < n && i < cap; i++)
+        {
+            rows[4 * i] = r[std::size_t(i)].sample_id;
+            rows[4 * i + 1] = r[std::size_t(i)].psnr_db;
+            rows[4 * i + 2] = r[std::size_t(i)].ssim;
+            rows[4 * i + 3] = r[std::size_t(i)].l1;
+        }
+    }
+    catch (const train::hash_mismatch &e)
+    {
+        g_err = e.what();
+        n = -2;
+    }
+    catch (const std::exception &e)
+    {
+        g_err = e.what();
+        n = -1;
+    }
+    return n;
 }
 
 } // extern "C"

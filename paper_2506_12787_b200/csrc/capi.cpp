@@ -75,6 +75,8 @@ static int guarded(F &&f)
     }
 }
 
+int swr_guarded(const std::function<void()> &f) { return guarded(f); }
+
 template <class T>
 static T *dalloc(Ctx &c, size_t count)
 {
@@ -109,6 +111,7 @@ struct HostScene
     float cutoff = 3.0f;
     int tile = 16;
     double bmin[3] = {0, 0, 0}, bmax[3] = {1, 1, 1};
+    uint64_t manifest_hash = 0; // checkpoint.cpp:40,133 (hex string in the trailer)
 };
 
 // ------------------------------------------------------------- scene build
@@ -156,6 +159,7 @@ static void build_scene(Ctx &c, const HostScene &hs, int device)
     c.cutoff = hs.cutoff;
     c.tile = hs.tile;
     std::memcpy(c.bbox_min, hs.bmin, sizeof(hs.bmin));
+    c.manifest_hash = hs.manifest_hash;
     std::memcpy(c.bbox_max, hs.bmax, sizeof(hs.bmax));
 
     const int n = hs.n, np = g.np;
@@ -672,6 +676,8 @@ static HostScene parse_wrfc(const char *path)
         hs.bmin[a] = bmin.at(a);
         hs.bmax[a] = bmax.at(a);
     }
+    if (j.contains("manifest_hash"))
+        hs.manifest_hash = std::stoull(j.at("manifest_hash").get<std::string>(), nullptr, 16);
     return hs;
 }
 
@@ -1253,6 +1259,49 @@ int swr_evaluate(swr_ctx *ctx, const float *pos_m, const float *target, int64_t 
         dfree(c, d_pos);
         raise_if_nonfinite(c, st);
     });
+}
+
+// train::evaluate (training.cpp:380-406) over a dataset split, streamed from
+// spectra.bin chunk by chunk (positions + targets of c.chunk samples at a time)
+int swr_evaluate_dataset(swr_ctx *ctx, swr_dataset *ds, int split, int32_t *sample_ids, double *psnr, double *ssim,
+                         double *l1)
+{
+    return guarded([&] {
+        Ctx &c = ctx->c;
+        const DatasetFile &d = ds->d;
+        if (c.manifest_hash != d.hash)
+            throw std::runtime_error("checkpoint was trained on a different dataset"); // train::hash_mismatch
+        if (d.H != c.g.H || d.W != c.g.W)
+            throw std::invalid_argument("spectrum shape mismatch");
+        if (split < 0 || split > 2)
+            throw std::invalid_argument("split must be 0 (train), 1 (test) or 2 (all)");
+        const std::vector<int> idx = d.split(split);
+        const int64_t B = int64_t(idx.size());
+        if (sample_ids)
+            std::memcpy(sample_ids, idx.data(), sizeof(int32_t) * idx.size());
+        if (B == 0)
+            return;
+        const int64_t chunk = std::max<int64_t>(1, std::min<int64_t>(B, c.chunk));
+        const size_t per = size_t(2) * c.g.H * c.g.W;
+        std::vector<float> pos(size_t(3) * chunk), tgt(per * chunk);
+        for (int64_t b0 = 0; b0 < B; b0 += chunk)
+        {
+            const int64_t nb = std::min<int64_t>(chunk, B - b0);
+            d.read(idx.data() + b0, nb, pos.data(), tgt.data());
+            const int rc = swr_evaluate(ctx, pos.data(), tgt.data(), nb, 1.0, psnr ? psnr + b0 : nullptr,
+                                        ssim ? ssim + b0 : nullptr, l1 ? l1 + b0 : nullptr);
+            if (rc == SWR_EDOMAIN)
+                throw std::domain_error(g_err);
+            if (rc != SWR_OK)
+                throw std::runtime_error(g_err);
+        }
+    });
+}
+
+int swr_scene_set_manifest_hash(swr_ctx *ctx, uint64_t hash)
+{
+    ctx->c.manifest_hash = hash;
+    return SWR_OK;
 }
 
 // debug: clock64 trace of the tensor-core MLP (SWR_TC_DEBUG & 8), 3x8x80 stamps

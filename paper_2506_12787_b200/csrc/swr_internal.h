@@ -6,6 +6,8 @@
 #include <cstdint>
 #include <string>
 #include <array>
+#include <functional>
+#include <string>
 #include <vector>
 
 namespace swr
@@ -93,6 +95,7 @@ struct Ctx
     NetDev net{};
     bool has_net = false;
     double bbox_min[3]{}, bbox_max[3]{};
+    uint64_t manifest_hash = 0; // FNV-1a of the training dataset manifest (training.hpp:124)
     float cutoff = 3.0f;
     int tile = 16;
     int mlp_precision = 0;
@@ -132,5 +135,29 @@ void launch_metrics(Ctx &c, const float *d_pred, const float *d_target, int nb, 
                     double *d_ssim, double *d_l1, double *d_tmp, int *d_bad, cudaStream_t st);
 
 void check_cuda(cudaError_t e, const char *what);
+// run f, mapping the reference's exception types to swr_status (capi.cpp)
+int swr_guarded(const std::function<void()> &f);
+
+// spectra.bin + manifest.json reader (dataset.cpp, dataset.cpp:159-258 of the reference)
+uint64_t fnv1a64(const void *data, size_t size);
+struct DatasetFile
+{
+    int H = 0, W = 0;
+    int64_t count = 0, record_floats = 0;
+    std::vector<int> train, test, excluded;
+    double bbox_min[3]{}, bbox_max[3]{}, normalization = 1.0;
+    uint64_t hash = 0;
+    void *fp = nullptr;
+    ~DatasetFile();
+    void open(const std::string &dir);
+    void read(const int32_t *idx, int64_t n, float *pos, float *spectra) const;
+    std::vector<int> split(int which) const;
+};
 
 } // namespace swr
+
+// opaque handle of the C ABI (swr.h)
+struct swr_dataset
+{
+    swr::DatasetFile d;
+};

@@ -70,6 +70,14 @@ def lib():
                                          C.c_void_p, C.c_void_p, C.c_void_p]
         L.swr_evaluate.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64, C.c_double, C.c_void_p,
                                    C.c_void_p, C.c_void_p]
+        L.swr_dataset_open.argtypes = [C.c_char_p, C.POINTER(C.c_void_p)]
+        L.swr_dataset_close.argtypes = [C.c_void_p]
+        L.swr_dataset_get_info.argtypes = [C.c_void_p, C.c_void_p]
+        L.swr_dataset_split.argtypes = [C.c_void_p, C.c_int, C.c_void_p, C.c_void_p]
+        L.swr_dataset_read.argtypes = [C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p, C.c_void_p]
+        L.swr_evaluate_dataset.argtypes = [C.c_void_p, C.c_void_p, C.c_int, C.c_void_p, C.c_void_p, C.c_void_p,
+                                           C.c_void_p]
+        L.swr_scene_set_manifest_hash.argtypes = [C.c_void_p, C.c_uint64]
         L.swr_scene_get_info.argtypes = [C.c_void_p, C.c_void_p]
         L.swr_scene_create_wrfc.argtypes = [C.c_char_p, C.c_int, C.POINTER(C.c_void_p)]
         L.swr_scene_create.argtypes = [C.c_int, C.c_int, C.c_int, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
@@ -146,6 +154,10 @@ class Checkpoint:
                                       C.cast(lb, C.c_void_p) if lb else None, C.c_float(sc.cutoff), sc.tile,
                                       bmin.ctypes.data, bmax.ctypes.data, device, C.byref(h)))
         return cls(h.value)
+
+    def set_manifest_hash(self, h: int) -> None:
+        """Fingerprint of the dataset this scene was trained on (checkpoint.cpp:133)."""
+        _check(lib().swr_scene_set_manifest_hash(self._h, C.c_uint64(h)))
 
     def close(self):
         if self._h:
@@ -321,4 +333,62 @@ def evaluate(ck: Checkpoint, positions, targets, peak: float = 1.0):
     out = {k: np.zeros(B, np.float64) for k in ("psnr", "ssim", "l1")}
     _check(lib().swr_evaluate(ck.handle, _p(pos), _p(t), B, float(peak), _p(out["psnr"]), _p(out["ssim"]),
                               _p(out["l1"])))
+    return out
+
+
+class _DsInfo(C.Structure):
+    _fields_ = [("n_elevation", C.c_int), ("n_azimuth", C.c_int), ("samples", C.c_int64), ("n_train", C.c_int64),
+                ("n_test", C.c_int64), ("n_excluded", C.c_int64), ("manifest_hash", C.c_uint64),
+                ("normalization", C.c_double), ("bbox_min", C.c_double * 3), ("bbox_max", C.c_double * 3)]
+
+
+class Dataset:
+    """manifest.json + spectra.bin reader (load_dataset, dataset.cpp:205-258), records on demand."""
+
+    TRAIN, TEST, ALL = 0, 1, 2
+
+    def __init__(self, path: str):
+        h = C.c_void_p()
+        _check(lib().swr_dataset_open(path.encode(), C.byref(h)))
+        self._h = h
+        info = _DsInfo()
+        _check(lib().swr_dataset_get_info(self._h, C.byref(info)))
+        self.H, self.W, self.samples = info.n_elevation, info.n_azimuth, info.samples
+        self.manifest_hash = info.manifest_hash
+        self.bbox = np.array(list(info.bbox_min) + list(info.bbox_max))
+        self.normalization = info.normalization
+
+    def split(self, which: int) -> np.ndarray:
+        n = C.c_int64()
+        _check(lib().swr_dataset_split(self._h, which, None, C.byref(n)))
+        idx = np.zeros(n.value, np.int32)
+        _check(lib().swr_dataset_split(self._h, which, _p(idx), C.byref(n)))
+        return idx
+
+    def read(self, indices=None, count=None):
+        idx = None if indices is None else np.ascontiguousarray(indices, np.int32)
+        n = len(idx) if idx is not None else (self.samples if count is None else count)
+        pos = np.zeros((n, 3), np.float32)
+        spec = np.zeros((n, self.H, self.W, 2), np.float32)
+        _check(lib().swr_dataset_read(self._h, _p(idx), n, _p(pos), _p(spec)))
+        return pos, spec
+
+    def close(self):
+        if self._h:
+            lib().swr_dataset_close(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def evaluate_dataset(ck: Checkpoint, ds: Dataset, split: int):
+    """train::evaluate (training.cpp:380-406): per sample of the split (ids, psnr, ssim, l1)."""
+    n = len(ds.split(split))
+    out = {"sample_id": np.zeros(n, np.int32), "psnr": np.zeros(n), "ssim": np.zeros(n), "l1": np.zeros(n)}
+    _check(lib().swr_evaluate_dataset(ck.handle, ds._h, split, _p(out["sample_id"]), _p(out["psnr"]),
+                                      _p(out["ssim"]), _p(out["l1"])))
     return out
