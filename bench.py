@@ -181,6 +181,8 @@ def main():
                     choices=["fp32", "bf16x3", "bf16"])
     ap.add_argument("--chunk", type=int, default=256)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--verify", action="store_true",
+                    help="N > 1: rank 0 re-renders every rank's positions and checks the gathered spectra bitwise")
     args = ap.parse_args()
 
     rank = int(os.environ.get("RANK", "0"))
@@ -212,17 +214,24 @@ def main():
         return
 
     import torch
+    # one process per GPU; SWR_BENCH_BACKEND=gloo lets the multi-rank plumbing be
+    # exercised on a single-GPU box (ranks then share the device; not a timing run)
+    backend = os.environ.get("SWR_BENCH_BACKEND", "nccl")
+    local = local % max(1, torch.cuda.device_count()) if backend != "nccl" else local
     torch.cuda.set_device(local)
     dist = None
     if world > 1:
         import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend)
     from paper_2506_12787_b200 import swr
 
     ck = swr.Checkpoint.from_scene(scene, device=local)
     ck.set_option("mlp_precision", {"fp32": 0, "bf16x3": 1, "bf16": 2}[args.precision])
     ck.set_option("chunk", args.chunk)
-    from paper_2506_12787_b200.shard import gather_to_root, max_over_ranks, shard_range
+    from paper_2506_12787_b200.shard import ChunkedGather, chunk_spans, gather_to_root, max_over_ranks, shard_range
     H, W = scene.H, scene.W
     if total_pos is None:                       # weak scaling: fixed positions per GPU
         B = args.batch
@@ -248,22 +257,54 @@ def main():
     flags = (swr.OUT_AOA | swr.OUT_POOLED) if aoa_only else (swr.OUT_SPECTRA | swr.OUT_POOLED | swr.OUT_RSSI)
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device="cuda")
 
+    # N > 1, full spectra: the one collective (outputs to rank 0 over NVLink, NCCL
+    # point-to-point) is issued chunk by chunk right behind each chunk's render,
+    # so the transfers overlap the rendering of the next chunks
+    overlapped = world > 1 and not aoa_only
+    if overlapped:
+        d_spec_out = torch.empty((total if rank == 0 else B, H, W, 2), dtype=torch.float32, device="cuda")
+        spans = chunk_spans(B, args.chunk)
+
     def step(timed_events=None):
         with torch.cuda.stream(stream):
+            if overlapped:
+                g = ChunkedGather(total, world, rank, args.chunk, d_spec_out)
+                view = g.local_view()
+                for k in range(g.n_chunks()):
+                    if k < len(spans):
+                        c0, n = spans[k]
+                        swr.render_device(ck, d_pos[c0].data_ptr(), n, flags, view[c0].data_ptr(),
+                                          d_pooled[c0].data_ptr(), d_rssi[c0].data_ptr(), d_rc[c0].data_ptr(),
+                                          d_ang[c0].data_ptr(), sptr)
+                    g.post(k)
+                g.wait()
+                gather_to_root(d_rssi, total, world, rank)
+                return
             swr.render_device(ck, d_pos.data_ptr(), B, flags, 0 if aoa_only else d_spec.data_ptr(),
                               d_pooled.data_ptr(), d_rssi.data_ptr(), d_rc.data_ptr(), d_ang.data_ptr(), sptr)
             if world > 1:
-                # the one collective: outputs gathered to rank 0 over NVLink (NCCL)
-                if aoa_only:
-                    gather_to_root(d_rc, total, world, rank)
-                    gather_to_root(d_ang, total, world, rank)
-                else:
-                    gather_to_root(d_spec, total, world, rank)
-                    gather_to_root(d_rssi, total, world, rank)
+                # AoA sweep: only 16 B per position travel to rank 0
+                gather_to_root(d_rc, total, world, rank)
+                gather_to_root(d_ang, total, world, rank)
 
     for _ in range(args.warmup):
         step()
     torch.cuda.synchronize()
+    if args.verify and overlapped and rank == 0:
+        # the kernels are deterministic per position, so the gathered shards must
+        # equal a local render of the same positions bit for bit
+        chk = torch.empty((total, H, W, 2), dtype=torch.float32, device="cuda")
+        d_all = torch.from_numpy(np.ascontiguousarray(pos_all[:total])).cuda()
+        tmp_p = torch.empty(total, dtype=torch.float64, device="cuda")
+        tmp_rc = torch.empty((total, 2), dtype=torch.int32, device="cuda")
+        tmp_a = torch.empty((total, 2), dtype=torch.float64, device="cuda")
+        with torch.cuda.stream(stream):
+            swr.render_device(ck, d_all.data_ptr(), total, flags, chk.data_ptr(), tmp_p.data_ptr(),
+                              tmp_p.data_ptr(), tmp_rc.data_ptr(), tmp_a.data_ptr(), sptr)
+        torch.cuda.synchronize()
+        if not torch.equal(chk, d_spec_out):
+            raise SystemExit("verify: gathered spectra differ from a local render")
+        print("verify: gathered spectra of all ranks match a local render bitwise", file=sys.stderr, flush=True)
 
     # ---------------- device-timed region: K steps, L2 flushed between steps (untimed).
     # Per-stage CUDA events ride along (recorded on the render stream, read after
