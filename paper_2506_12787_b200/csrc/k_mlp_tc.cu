@@ -91,7 +91,11 @@ constexpr int XC_OP = TM * XCK * 2;     // one xc A operand (hi or lo) of a CTA 
 constexpr int XC_BLOCK = TG * XCK * 2;  // per 32-Gaussian block, one operand: 3 KB
 constexpr int A_LBO = (TM / 8) * 128;   // xc A tile: K-direction core-matrix stride (2 KB)
 constexpr int A_SBO = 128;
-constexpr int EPI_WARPS = 20;           // 5 column groups x 4 TMEM lane quarters
+#ifndef SWR_TC_GROUPS
+#define SWR_TC_GROUPS 5
+#endif
+constexpr int NGRP = SWR_TC_GROUPS;     // epilogue column groups (5 or 6)
+constexpr int EPI_WARPS = 4 * NGRP;     // column groups x 4 TMEM lane quarters
 constexpr int EPI_THREADS = 32 * EPI_WARPS;
 constexpr int THREADS = 32 * (2 + EPI_WARPS);
 constexpr int NREG = 3;                 // TMEM regions of 160 columns
@@ -109,10 +113,10 @@ constexpr int SMEM_CONST = (8 * WPC + 8) * 4;
 constexpr int NBARS = 2 * NSTAGE + 4 + 4 + 1 + 2;
 constexpr int SMEM_BYTES = SMEM_RING + SMEM_XC + SMEM_P + SMEM_CONST + NBARS * 8 + 16 + 1024;
 static_assert(SMEM_BYTES <= 227 * 1024, "shared memory budget");
-// epilogue column group g converts 16-column chunks g and g + 5: part 0 (chunks
-// 0-5) is converted by all 20 warps (group 0 takes two chunks), part 1 (chunks
-// 6-9) by groups 1-4
-__host__ __device__ constexpr int part_warps(int p) { return p == 0 ? 20 : 16; }
+// epilogue column group g converts 16-column chunks g and g + NGRP. With 6 groups
+// part 0 (chunks 0-5) is one chunk per warp (24 warps) and part 1 (chunks 6-9) is
+// converted by groups 0-3; with 5 groups group 0 takes chunks 0 and 5.
+__host__ __device__ constexpr int part_warps(int p) { return p == 0 ? 4 * NGRP : 16; }
 
 __host__ __device__ constexpr bool has_xc(int l) { return l == 0 || l == 2 || l == 4 || l == 6; }
 // weight stream per tile: one stage per (trunk layer, part): the xc K steps
@@ -520,12 +524,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1) mlp_tc_k
     }
     else
     {
-        const int e = warp;           // 0..19
+        const int e = warp;           // 0 .. EPI_WARPS - 1
         const int et = threadIdx.x;
         const int q = warp & 3;       // TMEM lane quarter = position of the tile
-        const int grp = 4 - (e >> 2); // column group: chunks grp (part 0) and grp + 5 (part 0 for group 0, else 1)
+        const int grp = NGRP - 1 - (e >> 2); // column group: chunks grp (part 0) and grp + NGRP (if < 10)
         const uint32_t lane_off = (uint32_t)(q * 32) << 16;
-        const int pc0 = part_of_chunk(grp), pc1 = part_of_chunk(grp + 5);
+        const int c1 = grp + NGRP; // second chunk (none when >= 10)
+        const int pc0 = part_of_chunk(grp), pc1 = c1 < KSTEPS ? part_of_chunk(c1) : -1;
         uint32_t fph = 0; // phase bits of acc[set][part] (this warp waits every completion of its parts)
         int ct = 0;       // trunk layers converted (= the issuer's trunk count): set = ct & 1
 
@@ -542,7 +547,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1) mlp_tc_k
                 fph ^= 1u << bit;
                 tc::tc_fence_after();
             }
-            if (lane == 0 && chunk < 5)
+            if (lane == 0 && chunk < NGRP)
                 stamp(a, it, l, 16 + e);
             if (!(a.debug & 2))
             {
@@ -569,13 +574,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1) mlp_tc_k
             if (lane == 0)
             {
                 tc::mbar_arrive_remote_relaxed(tc::mapa(&a_ready[(ct & 1) * NPART + p], 0)); // read by the next consumer
-                if (chunk < 5)
-                    stamp(a, it, l, 36 + e);
+                if (chunk < NGRP)
+                    stamp(a, it, l, 40 + e);
             }
         };
         auto convert_layer = [&](int it, int l) {
             convert(it, l, grp, pc0, true, pc1 != pc0);
-            convert(it, l, grp + 5, pc1, pc1 != pc0, true);
+            if (pc1 >= 0)
+                convert(it, l, c1, pc1, pc1 != pc0, true);
             ct++;
         };
         // heads of local tile `it` (group 0 warps: one lane quarter each)

@@ -13,6 +13,7 @@ for d in sys.argv[1:]:
     ck.set_option("stage_timing", 1)
     ts = []
     for _ in range(3):
+        ck.set_option("stage_reset", 1)
         swr.render(ck, pos, spectra=False)
         ts.append(round(float(ck.stage_times()[1]), 3))
     ck.set_option("stage_timing", 0)
