@@ -8,6 +8,14 @@ __global__ void spin_a(long long cycles)
         ;
     if (threadIdx.x == 9999) sm[0] = 1;
 }
+__global__ void __cluster_dims__(2, 1, 1) spin_c(long long cycles)
+{
+    extern __shared__ char sm[];
+    long long t0 = clock64();
+    while (clock64() - t0 < cycles)
+        ;
+    if (threadIdx.x == 9999) sm[0] = 1;
+}
 __global__ void spin_b(long long cycles)
 {
     extern __shared__ char sm[];
@@ -37,6 +45,25 @@ int main()
         {704, 195784, 200000, 128, 14336, -1, "A 191KB carve100, B default", 100},
         {704, 150000, 200000, 128, 14336, 100, "A 146KB carve100, B carve100", 100},
     };
+    {
+        // cluster kernel A (2-CTA clusters), 704 threads, 191 KB, carveout 100
+        cudaFuncSetAttribute(spin_c, cudaFuncAttributeMaxDynamicSharedMemorySize, 200000);
+        cudaFuncSetAttribute(spin_c, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+        cudaFuncSetAttribute(spin_b, cudaFuncAttributeMaxDynamicSharedMemorySize, 48 * 1024);
+        cudaFuncSetAttribute(spin_b, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+        cudaDeviceSynchronize();
+        cudaEventRecord(e0, 0);
+        cudaDeviceSynchronize();
+        spin_c<<<148, 704, 195784, a>>>(10000000);
+        spin_b<<<148, 128, 14336, b>>>(10000000);
+        cudaDeviceSynchronize();
+        cudaEventRecord(e1, 0);
+        cudaEventSynchronize(e1);
+        float ms;
+        cudaEventElapsedTime(&ms, e0, e1);
+        printf("%-40s: %.2f ms (%s) %s\n", "CLUSTER A 191KB carve100, B carve100", ms, ms < 7 ? "concurrent" : "serial",
+               cudaGetErrorString(cudaGetLastError()));
+    }
     for (auto &c : cs)
     {
         cudaFuncSetAttribute(spin_a, cudaFuncAttributeMaxDynamicSharedMemorySize, c.a_attr ? c.a_attr : 48 * 1024);
