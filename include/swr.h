@@ -178,6 +178,22 @@ int swr_evaluate_dataset(swr_ctx *ctx, swr_dataset *ds, int split, int32_t *samp
  * from the checkpoint trailer, checkpoint.cpp:133) */
 int swr_scene_set_manifest_hash(swr_ctx *ctx, uint64_t hash);
 
+/* ------------------------------------------------------------ backward
+ * splat::rasterize_backward (splat.cpp:494-669) per position: residuals as for
+ * swr_rasterize (NULL = canonical render), upstream = dL/dA [B][H][W][2];
+ * outputs in the reference's RenderGrads layout (splat.hpp:77-89), [B][n][2|3|1]:
+ * center_raw, cholesky, atten_logit, response (raw fields, chain rule applied)
+ * and d_center, d_response, d_atten (wrt the residuals). Any output may be NULL. */
+int swr_rasterize_backward(swr_ctx *ctx, const float *d_center, const float *d_response,
+                           const float *d_atten, int64_t B, const float *upstream, float *g_center_raw,
+                           float *g_cholesky, float *g_atten_logit, float *g_response, float *g_d_center,
+                           float *g_d_response, float *g_d_atten);
+/* train::hybrid_loss (training.cpp:62-106): lambda1 * L1 + (1 - lambda1) * (1 - SSIM)
+ * per (prediction, target) pair; terms [B][3] = (loss, l1_term, ssim_term),
+ * grad [B][H][W][2] = dLoss/dprediction (NULL: value only). */
+int swr_hybrid_loss(swr_ctx *ctx, const float *pred, const float *target, int64_t B, double lambda1,
+                    double *terms, float *grad);
+
 /* Kernel launches issued by this context since creation (for the bench). */
 int64_t swr_launch_count(swr_ctx *ctx);
 

@@ -308,6 +308,31 @@ class Reference:
             raise ValueError("grid too small for the 11x11 SSIM window")
         return tuple(out)
 
+    def rasterize_backward(self, upstream, res=None):
+        """splat::rasterize_backward -> dict of the seven RenderGrads fields."""
+        n = self.sc.n
+        dc, dr, da = _split_res(res)
+        widths = (2, 3, 1, 2, 2, 2, 1)
+        flat = np.zeros(n * sum(widths), np.float32)
+        self._check(self.lib.wref_rasterize_backward(self.h, _f(dc), _f(dr), _f(da), _f(_c32(upstream)), _f(flat)))
+        out, at = {}, 0
+        names = ("center_raw", "cholesky", "atten_logit", "response", "d_center", "d_response", "d_atten")
+        for k, w in zip(names, widths):
+            v = flat[at:at + n * w]
+            out[k] = v.reshape(n, w) if w > 1 else v.copy()
+            at += n * w
+        return out
+
+    def hybrid_loss(self, pred, target, lambda1, grad=True):
+        pred, target = _c32(pred), _c32(target)
+        terms = np.zeros(3)
+        g = np.zeros_like(pred) if grad else None
+        rc = self.lib.wref_hybrid_loss(_f(pred), _f(target), pred.shape[0], pred.shape[1], C.c_double(lambda1),
+                                       _d(terms), _f(g) if grad else None)
+        if rc:
+            raise ArithmeticError("hybrid loss: non-finite input or loss")
+        return terms, g
+
     def materialize_center(self, rel, raz, double=False):
         if double:
             el, az = C.c_double(), C.c_double()

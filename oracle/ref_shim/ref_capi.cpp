@@ -254,6 +254,62 @@ int wref_rasterize(void *h, const float *d_center, const float *d_response, cons
     });
 }
 
+// rasterize_backward(set, residuals-or-null, params, upstream): the seven
+// RenderGrads fields, concatenated in declaration order into `grads`
+// (n * (2+3+1+2+2+2+1) floats).
+int wref_rasterize_backward(void *h, const float *d_center, const float *d_response, const float *d_atten,
+                            const float *upstream, float *grads)
+{
+    return guarded([&] {
+        const auto &ck = *ck_of(h);
+        splat::Residuals res;
+        const splat::Residuals *rp = nullptr;
+        if (d_center)
+        {
+            res.resize(ck.set.n);
+            std::memcpy(res.d_center.data(), d_center, sizeof(float) * res.d_center.size());
+            std::memcpy(res.d_response.data(), d_response, sizeof(float) * res.d_response.size());
+            std::memcpy(res.d_atten.data(), d_atten, sizeof(float) * res.d_atten.size());
+            rp = &res;
+        }
+        const Spectrum up = wrap_spectrum(upstream, ck.set.grid.n_elevation, ck.set.grid.n_azimuth);
+        const auto g = splat::rasterize_backward<float>(ck.set, rp, ck.config.raster, up);
+        float *dst = grads;
+        for (const auto *v : {&g.center_raw, &g.cholesky, &g.atten_logit, &g.response, &g.d_center, &g.d_response,
+                              &g.d_atten})
+        {
+            std::memcpy(dst, v->data(), sizeof(float) * v->size());
+            dst += v->size();
+        }
+    });
+}
+
+// hybrid_loss(prediction, target, lambda1, grad-or-null): terms = (loss,
+// l1_term, ssim_term); returns 1 on the reference's non-finite error.
+int wref_hybrid_loss(const float *pred, const float *target, int H, int W, double lambda1, double *terms, float *grad)
+{
+    try
+    {
+        const auto p = wrap_spectrum(pred, H, W), t = wrap_spectrum(target, H, W);
+        Spectrum g;
+        const auto lt = train::hybrid_loss<float>(p, t, lambda1, grad ? &g : nullptr);
+        terms[0] = lt.loss;
+        terms[1] = lt.l1_term;
+        terms[2] = lt.ssim_term;
+        if (grad)
+            fill_spectrum(g, grad);
+        return 0;
+    }
+    catch (const std::runtime_error &)
+    {
+        return 1;
+    }
+    catch (const std::exception &)
+    {
+        return 2;
+    }
+}
+
 int wref_render_at(void *h, const float *pos_m, float *spectrum)
 {
     return guarded([&] {

@@ -165,7 +165,7 @@ static void build_scene(Ctx &c, const HostScene &hs, int device)
     const int n = hs.n, np = g.np;
     std::vector<float> el0(np, 0.f), az0(np, 0.f), d0(np, 0.f), re0(np, 0.f), im0(np, 0.f), il3(np, 0.f),
         l2v(np, 0.f);
-    std::vector<float4> shape(np, make_float4(0, 0, 0, 0));
+    std::vector<float4> shape(np, make_float4(0, 0, 0, 0)), bwd(np, make_float4(0, 0, 0, 0));
     std::vector<double2> half(np, make_double2(0, 0));
     for (int p = 0; p < n; p++)
     {
@@ -186,6 +186,9 @@ static void build_scene(Ctx &c, const HostScene &hs, int device)
         l2v[p] = l2;
         half[p] = make_double2(double(g.radius) * double(l1),
                                double(g.radius) * std::sqrt(double(l2) * l2 + double(l3) * l3));
+        const float th_el = std::tanh(rel), th_az = std::tanh(raz);
+        bwd[p] = make_float4(1.0f - th_el * th_el, 1.0f - th_az * th_az, c1 >= 1e-4f ? 1.0f : 0.0f,
+                             c3 >= 1e-4f ? 1.0f : 0.0f);
     }
     std::vector<float> elc(hs.H), azc(hs.W);
     for (int r = 0; r < hs.H; r++)
@@ -202,6 +205,7 @@ static void build_scene(Ctx &c, const HostScene &hs, int device)
     s.inv_l3 = upload(c, il3);
     s.l2 = upload(c, l2v);
     s.half = upload(c, half);
+    s.bwd = upload(c, bwd);
     s.el_c = upload(c, elc);
     s.az_c = upload(c, azc);
 
@@ -343,12 +347,16 @@ static void ensure_pairs(Ctx &c, int64_t pairs, int nb, int64_t max_seg)
         dfree(c, w.keys);
         dfree(c, w.vals);
         dfree(c, w.sorted);
+        dfree(c, w.perm);
+        w.perm = nullptr;
         const int64_t cap = std::max<int64_t>(pairs + pairs / 8, 1024);
         w.keys = dalloc<uint16_t>(c, cap);
         w.vals = dalloc<int>(c, cap);
         w.sorted = dalloc<int>(c, cap);
         w.cap_pairs = cap;
     }
+    if (w.want_perm && !w.perm)
+        w.perm = dalloc<int>(c, w.cap_pairs);
     const int need = int(std::max<int64_t>(1, (max_seg + kSort - 1) / kSort));
     if (need > w.max_chunks || !w.chunk_hist)
     {
@@ -1295,6 +1303,134 @@ int swr_evaluate_dataset(swr_ctx *ctx, swr_dataset *ds, int split, int32_t *samp
             if (rc != SWR_OK)
                 throw std::runtime_error(g_err);
         }
+    });
+}
+
+// ------------------------------------------------------------ backward
+
+// splat::rasterize_backward (splat.cpp:494-669) per position: residuals as
+// swr_rasterize (nullable), upstream [B][H][W][2]; outputs [B][n][...] in the
+// reference's RenderGrads layout (splat.hpp:77-89), any may be NULL
+int swr_rasterize_backward(swr_ctx *ctx, const float *dc, const float *dr, const float *da, int64_t B,
+                           const float *upstream, float *g_center_raw, float *g_cholesky, float *g_atten_logit,
+                           float *g_response, float *g_d_center, float *g_d_response, float *g_d_atten)
+{
+    return guarded([&] {
+        Ctx &c = ctx->c;
+        if (B < 0)
+            throw std::invalid_argument("negative batch");
+        if (B == 0)
+            return;
+        check_cuda(cudaSetDevice(c.device), "cudaSetDevice");
+        cudaStream_t st = c.stream;
+        const int64_t chunk = std::max<int64_t>(1, std::min<int64_t>(B, c.chunk));
+        ensure_work(c, chunk);
+        const bool with_res = dc != nullptr;
+        const int n = c.g.n;
+        const size_t per = size_t(2) * c.g.H * c.g.W;
+        float *d_state = dalloc<float>(c, size_t(chunk) * std::max(n, 1) * 11);
+        float *d_up = dalloc<float>(c, per * chunk);
+        const int widths[7] = {2, 3, 1, 2, 2, 2, 1};
+        float *host_out[7] = {g_center_raw, g_cholesky, g_atten_logit, g_response, g_d_center, g_d_response, g_d_atten};
+        float *d_out[7];
+        for (int k = 0; k < 7; k++)
+            d_out[k] = dalloc<float>(c, size_t(chunk) * std::max(n, 1) * widths[k]);
+        float *d_slots = nullptr;
+        int64_t slots_cap = 0;
+        c.w.want_perm = true;
+        try
+        {
+            for (int64_t b0 = 0; b0 < B; b0 += chunk)
+            {
+                const int nb = int(std::min<int64_t>(chunk, B - b0));
+                if (with_res)
+                    upload_residuals(c, dc, dr, da, b0, nb);
+                check_cuda(cudaMemcpyAsync(d_up, upstream + per * b0, sizeof(float) * per * nb, cudaMemcpyHostToDevice,
+                                           st),
+                           "H2D upstream");
+                // the forward's setup + bins (state, boxes, CSR lists) with the sort permutation
+                launch_setup(c, nb, with_res, st);
+                launch_bin_count(c, nb, st);
+                check_cuda(cudaMemcpyAsync(c.w.host_pairs, c.w.stats, 2 * sizeof(int64_t), cudaMemcpyDeviceToHost, st),
+                           "D2H pair count");
+                check_cuda(cudaStreamSynchronize(st), "pair count");
+                const int64_t pairs = c.w.host_pairs[0], max_seg = c.w.host_pairs[1];
+                ensure_pairs(c, pairs, nb, max_seg);
+                launch_bin_sort(c, nb, pairs, int(max_seg), st);
+                launch_state_out(c, nb, with_res, d_state, st);
+                if (pairs > slots_cap)
+                {
+                    dfree(c, d_slots);
+                    slots_cap = std::max<int64_t>(pairs, 1);
+                    d_slots = dalloc<float>(c, size_t(slots_cap) * 8);
+                }
+                launch_raster_backward(c, nb, d_state, d_up, d_slots, st);
+                launch_bwd_merge(c, nb, with_res, d_slots, d_out, st);
+                check_cuda(cudaGetLastError(), "backward launch");
+                for (int k = 0; k < 7; k++)
+                    if (host_out[k])
+                        check_cuda(cudaMemcpyAsync(host_out[k] + size_t(b0) * n * widths[k], d_out[k],
+                                                   sizeof(float) * size_t(nb) * n * widths[k], cudaMemcpyDeviceToHost,
+                                                   st),
+                                   "D2H grads");
+                check_cuda(cudaStreamSynchronize(st), "backward");
+            }
+        }
+        catch (...)
+        {
+            c.w.want_perm = false;
+            throw;
+        }
+        c.w.want_perm = false;
+        for (void *p : {(void *)d_state, (void *)d_up, (void *)d_slots})
+            dfree(c, p);
+        for (float *p : d_out)
+            dfree(c, p);
+    });
+}
+
+// hybrid_loss (training.cpp:62-106) for B (prediction, target) pairs: terms
+// [B][3] = (loss, l1_term, ssim_term); grad [B][H][W][2] (NULL: value only)
+int swr_hybrid_loss(swr_ctx *ctx, const float *pred, const float *target, int64_t B, double lambda1, double *terms,
+                    float *grad)
+{
+    return guarded([&] {
+        Ctx &c = ctx->c;
+        if (B < 0)
+            throw std::invalid_argument("negative batch");
+        check_metric_args(c, true);
+        if (B == 0)
+            return;
+        check_cuda(cudaSetDevice(c.device), "cudaSetDevice");
+        cudaStream_t st = c.stream;
+        const int64_t chunk = std::max<int64_t>(1, std::min<int64_t>(B, c.chunk));
+        metrics_workspace(c, int(chunk));
+        const size_t per = size_t(2) * c.g.H * c.g.W;
+        double *d_tmp = dalloc<double>(c, loss_tmp_doubles(c, int(chunk)));
+        double *d_terms = dalloc<double>(c, size_t(3) * chunk);
+        float *d_grad = grad ? dalloc<float>(c, per * chunk) : nullptr;
+        check_cuda(cudaMemsetAsync(c.w.met_bad, 0, sizeof(int), st), "memset");
+        for (int64_t b0 = 0; b0 < B; b0 += chunk)
+        {
+            const int nb = int(std::min<int64_t>(chunk, B - b0));
+            check_cuda(cudaMemcpyAsync(c.w.met_pred, pred + per * b0, sizeof(float) * per * nb, cudaMemcpyHostToDevice,
+                                       st),
+                       "H2D prediction");
+            check_cuda(cudaMemcpyAsync(c.w.met_target, target + per * b0, sizeof(float) * per * nb,
+                                       cudaMemcpyHostToDevice, st),
+                       "H2D target");
+            launch_hybrid_loss(c, c.w.met_pred, c.w.met_target, nb, lambda1, d_terms, d_grad, d_tmp, c.w.met_bad, st);
+            if (terms)
+                check_cuda(cudaMemcpyAsync(terms + 3 * b0, d_terms, sizeof(double) * 3 * nb, cudaMemcpyDeviceToHost, st),
+                           "D2H loss");
+            if (grad)
+                check_cuda(cudaMemcpyAsync(grad + per * b0, d_grad, sizeof(float) * per * nb, cudaMemcpyDeviceToHost, st),
+                           "D2H loss gradient");
+            check_cuda(cudaStreamSynchronize(st), "loss");
+        }
+        for (void *p : {(void *)d_tmp, (void *)d_terms, (void *)d_grad})
+            dfree(c, p);
+        raise_if_nonfinite(c, st);
     });
 }
 

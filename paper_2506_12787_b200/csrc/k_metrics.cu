@@ -161,6 +161,135 @@ __global__ void ssim_final_kernel(const double *__restrict__ part, int nb, int v
     }
     ssim[s] = 0.5 * (ch[0] + ch[1]);
 }
+
+// ------------------------------------------------- hybrid loss + gradient
+// training.cpp:62-106: loss = lambda1 * L1 + (1 - lambda1) * (1 - SSIM), and its
+// gradient wrt the prediction; the SSIM gradient follows ssim_channel's
+// f1/f2/f3 window terms scattered back with the adjoint correlation
+// (spectrum.cpp:103-131, 209-235), all in double, rounded to float where the
+// reference stores floats.
+
+// per window: SSIM and the three gradient terms; F layout [pair][channel][3][vh][vw]
+__global__ void __launch_bounds__(256) ssim_vgrad_kernel(const double *__restrict__ tmp, int H, int W,
+                                                         double *__restrict__ part, double *__restrict__ F)
+{
+    __shared__ double sh[32];
+    const int i = blockIdx.x, c = blockIdx.y;
+    const int64_t s = blockIdx.z;
+    const int vw = W - kWin + 1, vh = H - kWin + 1;
+    const int64_t qs = (int64_t)H * vw, fs = (int64_t)vh * vw;
+    const double *in = tmp + ((s * 2 + c) * 5) * qs;
+    double *f = F + ((s * 2 + c) * 3) * fs + (int64_t)i * vw;
+    const double c1 = 0.01 * 0.01, c2 = 0.03 * 0.03; // peak 1 (training.cpp:79-80)
+    double acc = 0.0;
+    for (int j = threadIdx.x; j < vw; j += blockDim.x)
+    {
+        double m[5];
+#pragma unroll
+        for (int q = 0; q < 5; q++)
+        {
+            double v = 0.0;
+#pragma unroll
+            for (int t = 0; t < kWin; t++)
+                v = __fma_rn(c_taps[t], in[q * qs + (int64_t)(i + t) * vw + j], v);
+            m[q] = v;
+        }
+        const double ux = m[0], uy = m[1];
+        const double vx = m[2] - ux * ux, vy = m[3] - uy * uy, vxy = m[4] - ux * uy;
+        const double a1 = 2.0 * ux * uy + c1, a2 = 2.0 * vxy + c2;
+        const double b1 = ux * ux + uy * uy + c1, b2 = vx + vy + c2;
+        const double sv = (a1 * a2) / (b1 * b2);
+        acc += sv;
+        f[j] = 2.0 * uy * (a2 - a1) / (b1 * b2) - 2.0 * sv * ux / b1 + 2.0 * sv * ux / b2;
+        f[fs + j] = 2.0 * a1 / (b1 * b2);
+        f[2 * fs + j] = -2.0 * sv / b2;
+    }
+    acc = block_sum(acc, sh);
+    if (threadIdx.x == 0)
+        part[(s * 2 + c) * vh + i] = acc;
+}
+
+// adjoint correlation, horizontal: T[q][i][col] = sum_t g[t] F[q][i][col - t]
+__global__ void __launch_bounds__(256) scatter_h_kernel(const double *__restrict__ F, int H, int W,
+                                                        double *__restrict__ T)
+{
+    const int i = blockIdx.x, cq = blockIdx.y; // cq = channel * 3 + q
+    const int64_t s = blockIdx.z;
+    const int vw = W - kWin + 1, vh = H - kWin + 1;
+    const double *src = F + ((s * 6 + cq) * vh + i) * (int64_t)vw;
+    double *dst = T + ((s * 6 + cq) * vh + i) * (int64_t)W;
+    for (int col = threadIdx.x; col < W; col += blockDim.x)
+    {
+        double v = 0.0;
+        for (int t = 0; t < kWin; t++) // scatter order: t ascending for a fixed column
+        {
+            const int j = col - t;
+            if (j >= 0 && j < vw)
+                v = __fma_rn(c_taps[t], src[j], v);
+        }
+        dst[col] = v;
+    }
+}
+
+// adjoint, vertical, then the loss gradient per cell and channel
+__global__ void __launch_bounds__(256) loss_grad_kernel(const double *__restrict__ T, const float *__restrict__ pred,
+                                                        const float *__restrict__ target, int H, int W,
+                                                        double lambda1, float *__restrict__ grad)
+{
+    const int r = blockIdx.x;
+    const int64_t s = blockIdx.z;
+    const int vw = W - kWin + 1, vh = H - kWin + 1;
+    const double inv_w = 1.0 / ((double)vh * vw);
+    const double inv = lambda1 / (2.0 * H * W), sw = 0.5 * (1.0 - lambda1);
+    for (int col = threadIdx.x; col < W; col += blockDim.x)
+    {
+        const int64_t k = ((s * H) + r) * (int64_t)W + col;
+        float out[2];
+        for (int c = 0; c < 2; c++)
+        {
+            double gq[3];
+            for (int q = 0; q < 3; q++)
+            {
+                const double *src = T + ((s * 6 + c * 3 + q) * vh) * (int64_t)W;
+                double v = 0.0;
+                for (int t = kWin - 1; t >= 0; t--) // scatter order: source rows ascending
+                {
+                    const int i = r - t;
+                    if (i >= 0 && i < vh)
+                        v = __fma_rn(c_taps[t], src[(int64_t)i * W + col], v);
+                }
+                gq[q] = v;
+            }
+            const double x = (double)pred[2 * k + c], y = (double)target[2 * k + c];
+            const float g_ssim = (float)((gq[0] + gq[1] * y + gq[2] * x) * inv_w); // ssim_channel's T grad
+            const float d = pred[2 * k + c] - target[2 * k + c];
+            const double sgn = d > 0.f ? 1.0 : (d < 0.f ? -1.0 : 0.0);
+            out[c] = (float)(inv * sgn - sw * (double)g_ssim);
+        }
+        reinterpret_cast<float2 *>(grad)[k] = make_float2(out[0], out[1]);
+    }
+}
+
+__global__ void loss_final_kernel(const double *__restrict__ part, const double *__restrict__ l1v, int nb, int vh,
+                                  int vw, double lambda1, double *__restrict__ terms)
+{
+    const int s = blockIdx.x * blockDim.x + threadIdx.x;
+    if (s >= nb)
+        return;
+    double ch[2];
+    for (int c = 0; c < 2; c++)
+    {
+        double t = 0.0;
+        for (int i = 0; i < vh; i++)
+            t += part[((int64_t)s * 2 + c) * vh + i];
+        ch[c] = t / ((double)vh * vw);
+    }
+    const double ssim = 0.5 * (ch[0] + ch[1]);
+    const double l1t = lambda1 * l1v[s], st = (1.0 - lambda1) * (1.0 - ssim);
+    terms[3 * s] = l1t + st;
+    terms[3 * s + 1] = l1t;
+    terms[3 * s + 2] = st;
+}
 } // namespace
 
 // host: the window taps exactly as spectrum.cpp:51-70 computes them
@@ -209,4 +338,43 @@ void launch_metrics(Ctx &c, const float *d_pred, const float *d_target, int nb, 
     check_cuda(cudaGetLastError(), "metrics kernels");
 }
 
+} // namespace swr
+
+namespace swr
+{
+size_t loss_tmp_doubles(const Ctx &c, int nb)
+{
+    const int H = c.g.H, W = c.g.W, vw = std::max(W - kWin + 1, 0), vh = std::max(H - kWin + 1, 0);
+    // h-correlations (5 q) | partial sums | F (3 q x windows) | adjoint rows (3 q x vh x W) | l1 per pair
+    return std::max<size_t>((size_t)nb * 2 * (5 * (size_t)H * vw + vh + 3 * (size_t)vh * vw + 3 * (size_t)vh * W) + nb,
+                            1);
+}
+
+// hybrid_loss (training.cpp:62-106) for nb pairs: terms [nb][3] = (loss, l1_term,
+// ssim_term) in double, grad [nb][H][W][2] float (null: value only)
+void launch_hybrid_loss(Ctx &c, const float *d_pred, const float *d_target, int nb, double lambda1, double *d_terms,
+                        float *d_grad, double *d_tmp, int *d_bad, cudaStream_t st)
+{
+    upload_taps();
+    const int H = c.g.H, W = c.g.W, vw = W - kWin + 1, vh = H - kWin + 1;
+    const int64_t n = (int64_t)2 * H * W;
+    double *hcor = d_tmp;
+    double *part = hcor + (size_t)nb * 2 * 5 * H * vw;
+    double *F = part + (size_t)nb * 2 * vh;
+    double *T = F + (size_t)nb * 2 * 3 * vh * vw;
+    double *l1v = T + (size_t)nb * 2 * 3 * vh * W;
+    const int threads = std::min(256, ((std::max(std::max(vw, W), 32) + 31) / 32) * 32);
+    metrics_point_kernel<<<nb, 512, 0, st>>>(d_pred, d_target, n, 1.0, nullptr, l1v, d_bad);
+    ssim_h_kernel<<<dim3(H, 2, nb), threads, 2 * W * sizeof(double), st>>>(d_pred, d_target, H, W, hcor);
+    ssim_vgrad_kernel<<<dim3(vh, 2, nb), threads, 0, st>>>(hcor, H, W, part, F);
+    loss_final_kernel<<<(nb + 127) / 128, 128, 0, st>>>(part, l1v, nb, vh, vw, lambda1, d_terms);
+    c.launches += 4;
+    if (d_grad)
+    {
+        scatter_h_kernel<<<dim3(vh, 6, nb), threads, 0, st>>>(F, H, W, T);
+        loss_grad_kernel<<<dim3(H, 1, nb), threads, 0, st>>>(T, d_pred, d_target, H, W, lambda1, d_grad);
+        c.launches += 2;
+    }
+    check_cuda(cudaGetLastError(), "hybrid loss kernels");
+}
 } // namespace swr

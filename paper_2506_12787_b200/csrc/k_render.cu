@@ -437,7 +437,7 @@ __global__ void __launch_bounds__(kSortThreads) sort_scatter_kernel(const uint16
                                                                     const int *__restrict__ vals,
                                                                     const int64_t *__restrict__ seg,
                                                                     const int *__restrict__ hist, int *__restrict__ out,
-                                                                    int max_chunks, int tiles)
+                                                                    int *__restrict__ perm, int max_chunks, int tiles)
 {
     extern __shared__ int whist[]; // [8][tiles]
     constexpr int kWarps = kSortThreads / 32, kRounds = kSort / kSortThreads;
@@ -489,7 +489,12 @@ __global__ void __launch_bounds__(kSortThreads) sort_scatter_kernel(const uint16
     {
         const int64_t i = b + (int64_t)w * (kSort / kWarps) + k * 32 + lane;
         if (i < e)
-            out[seg[s] + wh[ky[k]] + rk[k]] = vals[i];
+        {
+            const int dst = (int)(seg[s] + wh[ky[k]] + rk[k]);
+            out[dst] = vals[i];
+            if (perm) // CSR slot of each emitted pair (the backward merges per primitive)
+                perm[i] = dst;
+        }
     }
 }
 
@@ -505,6 +510,7 @@ void launch_bin_sort(Ctx &c, int nb, int64_t pairs, int max_seg, cudaStream_t st
     sort_scan_kernel<<<nb, 1024, 0, st>>>(c.w.seg, c.w.chunk_hist, c.w.tile_off, c.w.max_chunks, tiles);
     sort_scatter_kernel<<<gs, kSortThreads, 8 * tiles * sizeof(int), st>>>(c.w.keys, c.w.vals, c.w.seg,
                                                                            c.w.chunk_hist, c.w.sorted,
+                                                                           c.w.want_perm ? c.w.perm : nullptr,
                                                                            c.w.max_chunks, tiles);
     c.launches += 4;
 }

@@ -39,6 +39,8 @@ struct SceneDev
     float *inv_l3, *l2;    // remaining state fields (parity output only)
     double2 *half;         // FP64 bbox half widths (radius*l1, radius*sqrt(l2^2+l3^2)), splat.cpp:223-225
     float *el_c, *az_c;    // float(cell centres) (splat.cpp:180-185)
+    float4 *bwd;           // backward chain-rule constants (splat.cpp:633-664): (1 - tanh^2 el, az raw),
+                           // l1 >= floor, l3 >= floor (1 / 0)
 };
 
 // Deformation MLP on the device.
@@ -76,6 +78,8 @@ struct Work
     uint16_t *keys = nullptr;   // [cap_pairs] tile of each pair (primitive order)
     int *vals = nullptr;        // [cap_pairs] primitive of each pair (primitive order)
     int *sorted = nullptr;      // [cap_pairs] tile_prims (tile-major, primitive order inside)
+    int *perm = nullptr;        // [cap_pairs] CSR slot of each emitted pair (backward only)
+    bool want_perm = false;
     float4 *tile_part = nullptr; // [cap_b][tiles] (max |A|, argmax cell as float bits, sum |A| hi, lo)
     double *tile_sum = nullptr; // [cap_b][tiles]
     int64_t *stats = nullptr;      // device: (total pairs, longest segment) of the current chunk
@@ -133,6 +137,12 @@ int mlp_tc_trace(long long *out);
 size_t metrics_tmp_doubles(const Ctx &c, int nb);
 void launch_metrics(Ctx &c, const float *d_pred, const float *d_target, int nb, double peak, double *d_psnr,
                     double *d_ssim, double *d_l1, double *d_tmp, int *d_bad, cudaStream_t st);
+size_t loss_tmp_doubles(const Ctx &c, int nb);
+void launch_raster_backward(Ctx &c, int nb, const float *d_state, const float *d_upstream, float *d_slots,
+                            cudaStream_t st);
+void launch_bwd_merge(Ctx &c, int nb, bool with_res, const float *d_slots, float *const out[7], cudaStream_t st);
+void launch_hybrid_loss(Ctx &c, const float *d_pred, const float *d_target, int nb, double lambda1, double *d_terms,
+                        float *d_grad, double *d_tmp, int *d_bad, cudaStream_t st);
 
 void check_cuda(cudaError_t e, const char *what);
 // run f, mapping the reference's exception types to swr_status (capi.cpp)

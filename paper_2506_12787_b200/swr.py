@@ -77,6 +77,10 @@ def lib():
         L.swr_dataset_read.argtypes = [C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p, C.c_void_p]
         L.swr_evaluate_dataset.argtypes = [C.c_void_p, C.c_void_p, C.c_int, C.c_void_p, C.c_void_p, C.c_void_p,
                                            C.c_void_p]
+        L.swr_rasterize_backward.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64,
+                                             C.c_void_p] + [C.c_void_p] * 7
+        L.swr_hybrid_loss.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64, C.c_double, C.c_void_p,
+                                      C.c_void_p]
         L.swr_scene_set_manifest_hash.argtypes = [C.c_void_p, C.c_uint64]
         L.swr_scene_get_info.argtypes = [C.c_void_p, C.c_void_p]
         L.swr_scene_create_wrfc.argtypes = [C.c_char_p, C.c_int, C.POINTER(C.c_void_p)]
@@ -287,6 +291,40 @@ def rasterize(ck: Checkpoint, res: Residuals | None = None, B: int = 1) -> np.nd
     sp = np.zeros((B, ck.H, ck.W, 2), np.float32)
     _check(lib().swr_rasterize(ck.handle, _p(dc), _p(dr), _p(da), B, _p(sp)))
     return sp
+
+
+# RenderGrads field order and widths (splat.hpp:77-89)
+GRAD_FIELDS = (("center_raw", 2), ("cholesky", 3), ("atten_logit", 1), ("response", 2), ("d_center", 2),
+               ("d_response", 2), ("d_atten", 1))
+
+
+def rasterize_backward(ck: Checkpoint, upstream, res: Residuals | None = None) -> dict:
+    """splat::rasterize_backward (splat.cpp:494-669) per position: upstream
+    dL/dA [B][H][W][2] (+ residuals [B]...) -> the RenderGrads fields, [B][n][w]."""
+    up = _f32(upstream).reshape(-1, ck.H, ck.W, 2)
+    dc, dr, da, B = _res_args(res, up.shape[0])
+    if res is None:
+        B = up.shape[0]
+    elif B != up.shape[0]:
+        raise ValueError("residual and upstream batch sizes differ")
+    out = {k: np.zeros((B, ck.n, w) if w > 1 else (B, ck.n), np.float32) for k, w in GRAD_FIELDS}
+    _check(lib().swr_rasterize_backward(ck.handle, _p(dc), _p(dr), _p(da), B, _p(up),
+                                        *[_p(out[k]) for k, _ in GRAD_FIELDS]))
+    return out
+
+
+def hybrid_loss(ck: Checkpoint, pred, target, lambda1: float = 0.8, grad: bool = True):
+    """train::hybrid_loss (training.cpp:62-106) per pair: (terms [B][3] =
+    (loss, l1_term, ssim_term), dLoss/dprediction [B][H][W][2] or None)."""
+    a = _f32(pred).reshape(-1, ck.H, ck.W, 2)
+    b = _f32(target).reshape(-1, ck.H, ck.W, 2)
+    if a.shape != b.shape:
+        raise ValueError("spectrum shape mismatch")
+    B = a.shape[0]
+    terms = np.zeros((B, 3), np.float64)
+    g = np.zeros_like(a) if grad else None
+    _check(lib().swr_hybrid_loss(ck.handle, _p(a), _p(b), B, float(lambda1), _p(terms), _p(g)))
+    return terms, g
 
 
 def heads(ck: Checkpoint, spectra):

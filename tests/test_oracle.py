@@ -185,3 +185,27 @@ def dense_oracle(s, res=None):
         out[..., 0] += re * k
         out[..., 1] += im * k
     return out
+
+
+@pytest.mark.skipif(not has_ref(), reason="reference build absent (GPU box)")
+def test_reference_backward_shim_field_order():
+    """Pins the wref_rasterize_backward wiring: A is linear in response, so
+    dL/dresponse_n = sum(upstream * (A(response_n + e) - A)) for L = <upstream, A>,
+    and d_response equals response (splat.cpp:494-669)."""
+    sc = make_scene(40, seed=2, H=16, W=32, width=24)
+    ref = O.Reference(scene=sc)
+    rng = np.random.default_rng(0)
+    up = rng.standard_normal((16, 32, 2)).astype(np.float32)
+    g = ref.rasterize_backward(up)
+    assert set(g) == {"center_raw", "cholesky", "atten_logit", "response", "d_center", "d_response", "d_atten"}
+    np.testing.assert_array_equal(g["response"], g["d_response"])
+    base = ref.rasterize().astype(np.float64)
+    for n in (0, 7, 31):
+        for c in range(2):
+            dr = np.zeros((sc.n, 2), np.float32)
+            dr[n, c] = 1.0
+            pert = ref.rasterize((np.zeros((sc.n, 2), np.float32), dr, np.zeros(sc.n, np.float32)))
+            fd = float(np.sum(up.astype(np.float64) * (pert - base)))
+            assert abs(fd - g["response"][n, c]) <= 1e-4 * max(1.0, abs(fd)), (n, c)
+    terms, grad = ref.hybrid_loss(base.astype(np.float32), np.zeros((16, 32, 2), np.float32), 0.8)
+    assert abs(terms[0] - terms[1] - terms[2]) <= 1e-12 and grad.shape == (16, 32, 2)
