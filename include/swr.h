@@ -194,6 +194,68 @@ int swr_rasterize_backward(swr_ctx *ctx, const float *d_center, const float *d_r
 int swr_hybrid_loss(swr_ctx *ctx, const float *pred, const float *target, int64_t B, double lambda1,
                     double *terms, float *grad);
 
+/* ------------------------------------------------------------ training
+ * train::train (training.cpp:198-376) on the device: the coarse stage (Gaussians
+ * only) then the fine stage (deform net + Gaussians, centres frozen), one
+ * training sample per iteration drawn with the reference's Rng stream
+ * (mt19937_64; init_random and DeformNet::init draw orders, splat.cpp:681-709,
+ * deform.cpp:73-102), Adam per field group (training.cpp:39-57), hybrid loss
+ * (training.cpp:62-106), rasterize_backward and deform_backward
+ * (deform.cpp:264-326) as CUDA kernels. FP32 like the reference. */
+typedef struct
+{
+    int32_t primitives;       /* Gaussian count (TrainConfig, training.hpp:96-112) */
+    int32_t bands_center;     /* encoding bands (10) */
+    int32_t bands_position;   /* (6) */
+    int32_t width;            /* deform-net hidden width (156; <= 160 here) */
+    float cutoff_radius;      /* raster cutoff (3) */
+    int32_t tile;             /* raster tile edge (16) */
+    double lr_gaussian;       /* 1e-2 */
+    double lr_mlp;            /* 8e-3 */
+    double lambda1;           /* L1 weight of the hybrid loss (0.7) */
+    int64_t coarse_iters;     /* 10000 */
+    int64_t fine_iters;       /* 100000 */
+    double anneal_scale;      /* coordinate-noise gamma (1) */
+    int64_t anneal_threshold; /* coordinate-noise tau (10000) */
+    uint64_t seed;            /* 1234 */
+} swr_train_config;
+
+typedef struct swr_trainer swr_trainer;
+
+/* The reference defaults (training.hpp:96-112). */
+void swr_train_config_default(swr_train_config *cfg);
+/* Fresh run (resume_wrfc NULL: init_random + net init from cfg.seed) or resume
+ * from a checkpoint written with the same config on the same dataset
+ * (SWR_EINVAL on a config mismatch, SWR_ERUNTIME on a manifest-hash mismatch,
+ * training.cpp:212-219). The dataset's samples are copied to the device; ds may
+ * be closed afterwards. */
+int swr_trainer_create(const swr_train_config *cfg, swr_dataset *ds, const char *resume_wrfc, int device,
+                       swr_trainer **out);
+void swr_trainer_destroy(swr_trainer *tr);
+/* Run up to max_iters further iterations of the schedule (stops at
+ * coarse_iters + fine_iters). log [done][3] = (loss, l1_term, ssim_term) per
+ * iteration (the reference's CSV columns), NULL to skip; *done = iterations run;
+ * *device_ms = device time of the run. SWR_ERUNTIME on a non-finite loss. */
+int swr_trainer_run(swr_trainer *tr, int64_t max_iters, double *log, int64_t *done, double *device_ms);
+/* Completed iterations (Checkpoint::iteration). */
+int64_t swr_trainer_iteration(swr_trainer *tr);
+/* Current parameters in the reference layouts; layer_w/b in layer_list order
+ * (8 trunk layers, head_center, head_response, head_atten); any NULL skipped. */
+int swr_trainer_params(swr_trainer *tr, float *center_raw, float *cholesky, float *atten_logit, float *response,
+                       float *const layer_w[11], float *const layer_b[11]);
+/* One training forward/backward at the current parameters, no optimizer step:
+ * pos01 (normalized, 3 floats) != NULL runs the fine-stage chain
+ * (predict_residuals -> rasterize -> hybrid_loss -> rasterize_backward ->
+ * deform_backward, training.cpp:332-345), NULL the coarse one (no residuals);
+ * the target is dataset sample `sample`. terms = (loss, l1_term, ssim_term);
+ * render_grads = the 7 RenderGrads fields [n][w]; layer_gw/gb = DeformGrads in
+ * layer_list order (fine only). Any output may be NULL. */
+int swr_trainer_gradients(swr_trainer *tr, const float *pos01, int32_t sample, double *terms,
+                          float *const render_grads[7], float *const layer_gw[11], float *const layer_gb[11]);
+/* train::save_checkpoint (checkpoint.cpp:50-93): WRFC with the config echo,
+ * iteration, manifest hash and bbox. */
+int swr_trainer_save(swr_trainer *tr, const char *path);
+
 /* Kernel launches issued by this context since creation (for the bench). */
 int64_t swr_launch_count(swr_ctx *ctx);
 

@@ -333,6 +333,65 @@ class Reference:
             raise ArithmeticError("hybrid loss: non-finite input or loss")
         return terms, g
 
+    def train(self, dataset_dir, cfg, log_path=None, resume=None):
+        """train::train(load_dataset(dir), cfg, log_path, resume) -> a new Reference.
+        cfg: any object with the TrainConfig fields."""
+        L = self.lib
+        L.wref_train.restype = C.c_void_p
+        ints = (C.c_int * 5)(cfg.primitives, cfg.bands_center, cfg.bands_position, cfg.width, cfg.tile)
+        dbl = (C.c_double * 5)(cfg.cutoff_radius, cfg.lr_gaussian, cfg.lr_mlp, cfg.lambda1, cfg.anneal_scale)
+        ll = (C.c_longlong * 3)(cfg.coarse_iters, cfg.fine_iters, cfg.anneal_threshold)
+        kind = C.c_int()
+        h = L.wref_train(dataset_dir.encode(), ints, dbl, ll, C.c_ulonglong(cfg.seed),
+                         log_path.encode() if log_path else None, resume.h if resume is not None else None,
+                         C.byref(kind))
+        if not h:
+            msg = L.wref_last_error().decode()
+            raise (ValueError if kind.value == 1 else RuntimeError)(msg)
+        return Reference(handle=h)
+
+    def deform_backward(self, pos01, up):
+        """DeformGrads for upstream dL/d(residuals) up = (d_center, d_response, d_atten)."""
+        shapes = self.sc.layer_shapes()
+        gw = [np.zeros(s, np.float32) for s in shapes]
+        gb = [np.zeros(s[0], np.float32) for s in shapes]
+        uc, ur, ua = (_c32(u) for u in up)
+        self._check(self.lib.wref_deform_backward(self.h, _f(_c32(pos01)), _f(uc), _f(ur), _f(ua),
+                                                  (_fp * 11)(*[_f(w) for w in gw]), (_fp * 11)(*[_f(b) for b in gb])))
+        return gw, gb
+
+    def iteration(self):
+        self.lib.wref_ck_iteration.restype = C.c_longlong
+        return int(self.lib.wref_ck_iteration(self.h))
+
+    def set_iteration(self, it):
+        self.lib.wref_ck_set_iteration(self.h, C.c_longlong(it))
+
+    def gradients(self, target, lambda1, pos01=None):
+        """The training iteration's gradient chain at these parameters (fine when pos01 given)."""
+        sc = self.sc
+        n = sc.n
+        widths = (2, 3, 1, 2, 2, 2, 1)
+        names = ("center_raw", "cholesky", "atten_logit", "response", "d_center", "d_response", "d_atten")
+        flat = np.zeros(n * sum(widths), np.float32)
+        terms = np.zeros(3)
+        shapes = sc.layer_shapes()
+        gw = [np.zeros(s, np.float32) for s in shapes]
+        gb = [np.zeros(s[0], np.float32) for s in shapes]
+        pw = (_fp * 11)(*[_f(w) for w in gw])
+        pb = (_fp * 11)(*[_f(b) for b in gb])
+        p = None if pos01 is None else _c32(pos01)
+        self._check(self.lib.wref_gradients(self.h, _f(p), _f(_c32(target)), C.c_double(lambda1), _d(terms),
+                                            _f(flat), pw, pb))
+        out, at = {"terms": terms}, 0
+        for k, w in zip(names, widths):
+            v = flat[at:at + n * w]
+            out[k] = v.reshape(n, w) if w > 1 else v.copy()
+            at += n * w
+        if p is not None:
+            out["layer_w"], out["layer_b"] = gw, gb
+        return out
+
     def materialize_center(self, rel, raz, double=False):
         if double:
             el, az = C.c_double(), C.c_double()

@@ -538,6 +538,147 @@ void wref_ck_set_dataset(void *h, unsigned long long hash, const double *bbox6)
     }
 }
 
+// train::train(load_dataset(dir), cfg, log_path, resume) -> a new checkpoint
+// handle (nullptr on error; *kind = 1 invalid_argument, 2 hash_mismatch, 3 other).
+// ints5 = primitives, bands_center, bands_position, width, tile;
+// dbl5 = cutoff_radius, lr_gaussian, lr_mlp, lambda1, anneal_scale;
+// ll3 = coarse_iters, fine_iters, anneal_threshold.
+void *wref_train(const char *dir, const int *ints5, const double *dbl5, const long long *ll3,
+                 unsigned long long seed, const char *log_path, void *resume, int *kind)
+{
+    *kind = 0;
+    try
+    {
+        const auto ds = sim::load_dataset(dir);
+        train::TrainConfig cfg;
+        cfg.primitives = ints5[0];
+        cfg.enc.bands_center = ints5[1];
+        cfg.enc.bands_position = ints5[2];
+        cfg.width = ints5[3];
+        cfg.raster.tile = ints5[4];
+        cfg.raster.cutoff_radius = float(dbl5[0]);
+        cfg.lr_gaussian = dbl5[1];
+        cfg.lr_mlp = dbl5[2];
+        cfg.lambda1 = dbl5[3];
+        cfg.anneal_scale = dbl5[4];
+        cfg.coarse_iters = ll3[0];
+        cfg.fine_iters = ll3[1];
+        cfg.anneal_threshold = ll3[2];
+        cfg.seed = seed;
+        return new train::Checkpoint(
+            train::train(ds, cfg, log_path ? std::string(log_path) : std::string(), resume ? ck_of(resume) : nullptr));
+    }
+    catch (const train::hash_mismatch &e)
+    {
+        g_err = e.what();
+        *kind = 2;
+    }
+    catch (const std::invalid_argument &e)
+    {
+        g_err = e.what();
+        *kind = 1;
+    }
+    catch (const std::exception &e)
+    {
+        g_err = e.what();
+        *kind = 3;
+    }
+    return nullptr;
+}
+
+// The training iteration's gradient chain at the checkpoint's parameters
+// (training.cpp:320-345): pos01 != nullptr = fine (predict_residuals ->
+// rasterize -> hybrid_loss -> rasterize_backward -> deform_backward), else
+// coarse. grads7 = RenderGrads fields concatenated; gw/gb = DeformGrads.
+int wref_gradients(void *h, const float *pos01, const float *target, double lambda1, double *terms, float *grads7,
+                   float *const *gw, float *const *gb)
+{
+    return guarded([&] {
+        const auto &ck = *ck_of(h);
+        const Spectrum tgt = wrap_spectrum(target, ck.set.grid.n_elevation, ck.set.grid.n_azimuth);
+        splat::RasterWorkspace rws;
+        Spectrum pred, lgrad;
+        splat::RenderGrads g;
+        deform::DeformWorkspace dws;
+        splat::Residuals res;
+        const splat::Residuals *rp = nullptr;
+        if (pos01)
+        {
+            deform::predict_residuals(ck.net, ck.set, {pos01[0], pos01[1], pos01[2]}, dws, res);
+            rp = &res;
+        }
+        splat::rasterize<float>(ck.set, rp, ck.config.raster, pred, rws);
+        const auto lt = train::hybrid_loss(pred, tgt, lambda1, &lgrad);
+        terms[0] = lt.loss;
+        terms[1] = lt.l1_term;
+        terms[2] = lt.ssim_term;
+        splat::rasterize_backward<float>(ck.set, rp, ck.config.raster, lgrad, g, rws);
+        float *dst = grads7;
+        for (const auto *v : {&g.center_raw, &g.cholesky, &g.atten_logit, &g.response, &g.d_center, &g.d_response,
+                              &g.d_atten})
+        {
+            std::memcpy(dst, v->data(), sizeof(float) * v->size());
+            dst += v->size();
+        }
+        if (pos01)
+        {
+            splat::Residuals rg;
+            rg.resize(ck.set.n);
+            rg.d_center = g.d_center;
+            rg.d_response = g.d_response;
+            rg.d_atten = g.d_atten;
+            deform::DeformGrads dg;
+            dg.resize_like(ck.net);
+            deform::deform_backward(ck.net, dws, rg, dg);
+            const deform::DeformNet::Layer *L[11];
+            for (int i = 0; i < 8; i++)
+                L[i] = &dg.trunk[std::size_t(i)];
+            L[8] = &dg.head_center;
+            L[9] = &dg.head_response;
+            L[10] = &dg.head_atten;
+            for (int i = 0; i < 11; i++)
+            {
+                std::memcpy(gw[i], L[i]->w.data(), sizeof(float) * L[i]->w.size());
+                std::memcpy(gb[i], L[i]->b.data(), sizeof(float) * L[i]->b.size());
+            }
+        }
+    });
+}
+
+// deform_backward (deform.cpp:264-326) after predict_residuals at pos01 for a
+// given upstream dL/dresiduals; gw/gb = DeformGrads in layer_list order
+int wref_deform_backward(void *h, const float *pos01, const float *up_c, const float *up_r, const float *up_a,
+                         float *const *gw, float *const *gb)
+{
+    return guarded([&] {
+        const auto &ck = *ck_of(h);
+        deform::DeformWorkspace dws;
+        splat::Residuals res, up;
+        deform::predict_residuals(ck.net, ck.set, {pos01[0], pos01[1], pos01[2]}, dws, res);
+        up.resize(ck.set.n);
+        std::memcpy(up.d_center.data(), up_c, sizeof(float) * up.d_center.size());
+        std::memcpy(up.d_response.data(), up_r, sizeof(float) * up.d_response.size());
+        std::memcpy(up.d_atten.data(), up_a, sizeof(float) * up.d_atten.size());
+        deform::DeformGrads dg;
+        dg.resize_like(ck.net);
+        deform::deform_backward(ck.net, dws, up, dg);
+        const deform::DeformNet::Layer *L[11];
+        for (int i = 0; i < 8; i++)
+            L[i] = &dg.trunk[std::size_t(i)];
+        L[8] = &dg.head_center;
+        L[9] = &dg.head_response;
+        L[10] = &dg.head_atten;
+        for (int i = 0; i < 11; i++)
+        {
+            std::memcpy(gw[i], L[i]->w.data(), sizeof(float) * L[i]->w.size());
+            std::memcpy(gb[i], L[i]->b.data(), sizeof(float) * L[i]->b.size());
+        }
+    });
+}
+
+void wref_ck_set_iteration(void *h, long long it) { ck_of(h)->iteration = it; }
+long long wref_ck_iteration(void *h) { return ck_of(h)->iteration; }
+
 // train::evaluate (training.cpp:380-406) on a saved dataset: rows [n][4] =
 // (sample id, psnr, ssim, l1); returns the row count (-1 on error, -2 on hash mismatch)
 long long wref_evaluate(void *h, const char *dir, int split, double *rows, long long cap)

@@ -77,46 +77,72 @@ static int guarded(F &&f)
 
 int swr_guarded(const std::function<void()> &f) { return guarded(f); }
 
-template <class T>
-static T *dalloc(Ctx &c, size_t count)
-{
-    void *p = nullptr;
-    check_cuda(cudaMalloc(&p, std::max<size_t>(count, 1) * sizeof(T)), "cudaMalloc");
-    c.allocs.push_back(p);
-    return static_cast<T *>(p);
-}
-
-static void dfree(Ctx &c, void *p)
-{
-    if (!p)
-        return;
-    cudaFree(p);
-    c.allocs.erase(std::remove(c.allocs.begin(), c.allocs.end(), p), c.allocs.end());
-}
-
-template <class T>
-static T *upload(Ctx &c, const std::vector<T> &v)
-{
-    T *d = dalloc<T>(c, v.size());
-    check_cuda(cudaMemcpy(d, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice), "upload");
-    return d;
-}
-
-struct HostScene
-{
-    int H, W, n;
-    std::vector<float> center_raw, cholesky, atten, response;
-    int width = 0, bands_c = 10, bands_p = 6;
-    std::vector<std::vector<float>> lw, lb; // 11 layers or empty
-    float cutoff = 3.0f;
-    int tile = 16;
-    double bmin[3] = {0, 0, 0}, bmax[3] = {1, 1, 1};
-    uint64_t manifest_hash = 0; // checkpoint.cpp:40,133 (hex string in the trailer)
-};
-
 // ------------------------------------------------------------- scene build
 
-static void build_scene(Ctx &c, const HostScene &hs, int device)
+// Per-primitive render inputs from the raw fields, on the host (glibc tanhf /
+// expf like the reference's prepare(), splat.cpp:159-249)
+SceneFields scene_fields(const Grid &g, int n, const float *center_raw, const float *cholesky, const float *atten,
+                         const float *response)
+{
+    const int np = g.np;
+    SceneFields f;
+    f.el0.assign(np, 0.f);
+    f.az0.assign(np, 0.f);
+    f.d0.assign(np, 0.f);
+    f.re0.assign(np, 0.f);
+    f.im0.assign(np, 0.f);
+    f.il3.assign(np, 0.f);
+    f.l2v.assign(np, 0.f);
+    f.shape.assign(np, make_float4(0, 0, 0, 0));
+    f.bwd.assign(np, make_float4(0, 0, 0, 0));
+    f.half.assign(np, make_double2(0, 0));
+    for (int p = 0; p < n; p++)
+    {
+        const float rel = center_raw[2 * size_t(p)], raz = center_raw[2 * size_t(p) + 1];
+        f.el0[p] = float(kPi / 4) * (std::tanh(rel) + 1.0f); // float overloads: glibc tanhf
+        f.az0[p] = float(kPi) * (std::tanh(raz) + 1.0f);
+        const float a = atten[p];
+        f.d0[p] = 1.0f / (1.0f + std::exp(-a));
+        f.re0[p] = response[2 * size_t(p)];
+        f.im0[p] = response[2 * size_t(p) + 1];
+        const float c1 = cholesky[3 * size_t(p)], l2 = cholesky[3 * size_t(p) + 1], c3 = cholesky[3 * size_t(p) + 2];
+        const float l1 = c1 < 1e-4f ? 1e-4f : c1; // std::max(l, chol_floor)
+        const float l3 = c3 < 1e-4f ? 1e-4f : c3;
+        const float det = l1 * l1 * l3 * l3;
+        f.shape[p] = make_float4((l2 * l2 + l3 * l3) / det, -l2 / (l1 * l3 * l3), 1.0f / (l3 * l3), 1.0f / l1);
+        f.il3[p] = 1.0f / l3;
+        f.l2v[p] = l2;
+        f.half[p] = make_double2(double(g.radius) * double(l1),
+                                 double(g.radius) * std::sqrt(double(l2) * l2 + double(l3) * l3));
+        const float th_el = std::tanh(rel), th_az = std::tanh(raz);
+        f.bwd[p] = make_float4(1.0f - th_el * th_el, 1.0f - th_az * th_az, c1 >= 1e-4f ? 1.0f : 0.0f,
+                               c3 >= 1e-4f ? 1.0f : 0.0f);
+    }
+    return f;
+}
+
+// overwrite the device scene entries of c with host-derived ones (same arrays)
+void refresh_scene_host(Ctx &c, const float *center_raw, const float *cholesky, const float *atten,
+                        const float *response)
+{
+    const SceneFields f = scene_fields(c.g, c.g.n, center_raw, cholesky, atten, response);
+    auto put = [&](void *dst, const void *src, size_t bytes) {
+        check_cuda(cudaMemcpy(dst, src, bytes, cudaMemcpyHostToDevice), "refresh scene");
+    };
+    const size_t np = size_t(c.g.np);
+    put(c.s.el0, f.el0.data(), 4 * np);
+    put(c.s.az0, f.az0.data(), 4 * np);
+    put(c.s.delta0, f.d0.data(), 4 * np);
+    put(c.s.re0, f.re0.data(), 4 * np);
+    put(c.s.im0, f.im0.data(), 4 * np);
+    put(c.s.shape, f.shape.data(), 16 * np);
+    put(c.s.inv_l3, f.il3.data(), 4 * np);
+    put(c.s.l2, f.l2v.data(), 4 * np);
+    put(c.s.half, f.half.data(), 16 * np);
+    put(c.s.bwd, f.bwd.data(), 16 * np);
+}
+
+void build_scene(Ctx &c, const HostScene &hs, int device)
 {
     if (hs.H < 1 || hs.W < 1)
         throw std::invalid_argument("gaussian set has an empty grid");
@@ -163,49 +189,24 @@ static void build_scene(Ctx &c, const HostScene &hs, int device)
     std::memcpy(c.bbox_max, hs.bmax, sizeof(hs.bmax));
 
     const int n = hs.n, np = g.np;
-    std::vector<float> el0(np, 0.f), az0(np, 0.f), d0(np, 0.f), re0(np, 0.f), im0(np, 0.f), il3(np, 0.f),
-        l2v(np, 0.f);
-    std::vector<float4> shape(np, make_float4(0, 0, 0, 0)), bwd(np, make_float4(0, 0, 0, 0));
-    std::vector<double2> half(np, make_double2(0, 0));
-    for (int p = 0; p < n; p++)
-    {
-        const float rel = hs.center_raw[2 * size_t(p)], raz = hs.center_raw[2 * size_t(p) + 1];
-        el0[p] = float(kPi / 4) * (std::tanh(rel) + 1.0f); // float overloads: glibc tanhf
-        az0[p] = float(kPi) * (std::tanh(raz) + 1.0f);
-        const float a = hs.atten[p];
-        d0[p] = 1.0f / (1.0f + std::exp(-a));
-        re0[p] = hs.response[2 * size_t(p)];
-        im0[p] = hs.response[2 * size_t(p) + 1];
-        const float c1 = hs.cholesky[3 * size_t(p)], l2 = hs.cholesky[3 * size_t(p) + 1],
-                    c3 = hs.cholesky[3 * size_t(p) + 2];
-        const float l1 = c1 < 1e-4f ? 1e-4f : c1; // std::max(l, chol_floor)
-        const float l3 = c3 < 1e-4f ? 1e-4f : c3;
-        const float det = l1 * l1 * l3 * l3;
-        shape[p] = make_float4((l2 * l2 + l3 * l3) / det, -l2 / (l1 * l3 * l3), 1.0f / (l3 * l3), 1.0f / l1);
-        il3[p] = 1.0f / l3;
-        l2v[p] = l2;
-        half[p] = make_double2(double(g.radius) * double(l1),
-                               double(g.radius) * std::sqrt(double(l2) * l2 + double(l3) * l3));
-        const float th_el = std::tanh(rel), th_az = std::tanh(raz);
-        bwd[p] = make_float4(1.0f - th_el * th_el, 1.0f - th_az * th_az, c1 >= 1e-4f ? 1.0f : 0.0f,
-                             c3 >= 1e-4f ? 1.0f : 0.0f);
-    }
+    SceneFields f = scene_fields(g, n, hs.center_raw.data(), hs.cholesky.data(), hs.atten.data(), hs.response.data());
+    const std::vector<float> &el0 = f.el0, &az0 = f.az0;
     std::vector<float> elc(hs.H), azc(hs.W);
     for (int r = 0; r < hs.H; r++)
         elc[r] = float((r + 0.5) * g.cell_el);
     for (int j = 0; j < hs.W; j++)
         azc[j] = float((j + 0.5) * g.cell_az);
     SceneDev &s = c.s;
-    s.el0 = upload(c, el0);
-    s.az0 = upload(c, az0);
-    s.delta0 = upload(c, d0);
-    s.re0 = upload(c, re0);
-    s.im0 = upload(c, im0);
-    s.shape = upload(c, shape);
-    s.inv_l3 = upload(c, il3);
-    s.l2 = upload(c, l2v);
-    s.half = upload(c, half);
-    s.bwd = upload(c, bwd);
+    s.el0 = upload(c, f.el0);
+    s.az0 = upload(c, f.az0);
+    s.delta0 = upload(c, f.d0);
+    s.re0 = upload(c, f.re0);
+    s.im0 = upload(c, f.im0);
+    s.shape = upload(c, f.shape);
+    s.inv_l3 = upload(c, f.il3);
+    s.l2 = upload(c, f.l2v);
+    s.half = upload(c, f.half);
+    s.bwd = upload(c, f.bwd);
     s.el_c = upload(c, elc);
     s.az_c = upload(c, azc);
 
@@ -308,7 +309,7 @@ static void build_scene(Ctx &c, const HostScene &hs, int device)
 
 // ------------------------------------------------------------- work buffers
 
-static void ensure_work(Ctx &c, int64_t nb)
+void ensure_work(Ctx &c, int64_t nb)
 {
     Work &w = c.w;
     if (w.cap_b >= nb)
@@ -339,7 +340,7 @@ static void ensure_work(Ctx &c, int64_t nb)
     w.chunk_hist = nullptr;
 }
 
-static void ensure_pairs(Ctx &c, int64_t pairs, int nb, int64_t max_seg)
+void ensure_pairs(Ctx &c, int64_t pairs, int nb, int64_t max_seg)
 {
     Work &w = c.w;
     if (pairs > w.cap_pairs)
@@ -580,7 +581,7 @@ static void upload_residuals(Ctx &c, const float *dc, const float *dr, const flo
                "upload residuals");
 }
 
-static HostScene parse_wrfc(const char *path)
+HostScene parse_wrfc(const char *path)
 {
     std::ifstream is(path, std::ios::binary);
     if (!is)
@@ -686,6 +687,9 @@ static HostScene parse_wrfc(const char *path)
     }
     if (j.contains("manifest_hash"))
         hs.manifest_hash = std::stoull(j.at("manifest_hash").get<std::string>(), nullptr, 16);
+    hs.config_json = cfg.dump();
+    if (j.contains("iteration"))
+        hs.iteration = j.at("iteration").get<int64_t>();
     return hs;
 }
 

@@ -5,8 +5,10 @@
 
 #include <cstdint>
 #include <string>
+#include <algorithm>
 #include <array>
 #include <functional>
+#include <stdexcept>
 #include <string>
 #include <vector>
 
@@ -115,6 +117,95 @@ struct Ctx
     std::vector<void *> allocs;
     void *host_stage = nullptr; // persistent staging of the host-buffer API (capi.cpp)
 };
+
+void check_cuda(cudaError_t e, const char *what);
+
+template <class T>
+inline T *dalloc(Ctx &c, size_t count)
+{
+    void *p = nullptr;
+    check_cuda(cudaMalloc(&p, std::max<size_t>(count, 1) * sizeof(T)), "cudaMalloc");
+    c.allocs.push_back(p);
+    return static_cast<T *>(p);
+}
+
+inline void dfree(Ctx &c, void *p)
+{
+    if (!p)
+        return;
+    cudaFree(p);
+    c.allocs.erase(std::remove(c.allocs.begin(), c.allocs.end(), p), c.allocs.end());
+}
+
+template <class T>
+inline T *upload(Ctx &c, const std::vector<T> &v)
+{
+    T *d = dalloc<T>(c, v.size());
+    check_cuda(cudaMemcpy(d, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice), "upload");
+    return d;
+}
+
+struct HostScene
+{
+    int H, W, n;
+    std::vector<float> center_raw, cholesky, atten, response;
+    int width = 0, bands_c = 10, bands_p = 6;
+    std::vector<std::vector<float>> lw, lb; // 11 layers or empty
+    float cutoff = 3.0f;
+    int tile = 16;
+    double bmin[3] = {0, 0, 0}, bmax[3] = {1, 1, 1};
+    uint64_t manifest_hash = 0; // checkpoint.cpp:40,133 (hex string in the trailer)
+    std::string config_json;    // trailer "config" object (checkpoint.cpp:36), WRFC files only
+    int64_t iteration = 0;      // trailer "iteration"
+};
+
+// ------------------------------------------------------------ training (k_train.cu, train.cpp)
+struct AdamHp
+{
+    double lr, beta1, beta2, eps; // AdamParams (training.hpp:44-50)
+};
+
+// Gaussian parameters, Adam moments and gradients on the device (reference layouts)
+struct GaussDev
+{
+    float *center, *chol, *atten, *resp;                   // [n][2], [n][3], [n], [n][2]
+    float *m_center, *v_center, *m_chol, *v_chol, *m_atten, *v_atten, *m_resp, *v_resp;
+    const float *g_center, *g_chol, *g_atten, *g_resp;     // rasterize_backward outputs
+};
+
+void launch_gauss_adam(Ctx &c, const GaussDev &gp, const AdamHp &hp, double bc1_c, double bc2_c, double bc1,
+                       double bc2, bool step_center, bool step_rest, float floor_el, float floor_az, cudaStream_t st);
+void launch_adam_flat(Ctx &c, float *p, const float *g, float *m, float *v, int64_t count, const AdamHp &hp,
+                      double bc1, double bc2, cudaStream_t st);
+void launch_position_encoding(Ctx &c, float *x, int d, int dc, const float *d_penc, int dp, cudaStream_t st);
+void launch_dense_fwd(Ctx &c, const float *a1, int ld1, int ka, const float *a2, int ld2, int K, const float *W,
+                      const float *b, int width, float *h, cudaStream_t st);
+void launch_heads_fwd(Ctx &c, const float *h7, int width, const float *Wh, const float *bh, float *planes,
+                      int64_t plane, cudaStream_t st);
+void launch_dense_bwd_input(Ctx &c, const float *dz, int width, const float *W, int cols, const float *h_prev,
+                            float *dz_prev, cudaStream_t st);
+size_t dw_partial_floats(int n, int R, int C);
+void launch_dense_bwd_weights(Ctx &c, const float *dz, int R, const float *a1, int ld1, int ka, const float *a2,
+                              int ld2, int K, float *part, float *dW, float *db, cudaStream_t st);
+void launch_heads_bwd(Ctx &c, const float *d_center, const float *d_response, const float *d_atten,
+                      const float *Wc, const float *Wr, const float *Wa, const float *h7, int width, float *dz7,
+                      float *dr5, cudaStream_t st);
+
+// scene / work-buffer management shared by the C ABI and the trainer (capi.cpp)
+void build_scene(Ctx &c, const HostScene &hs, int device);
+struct SceneFields
+{
+    std::vector<float> el0, az0, d0, re0, im0, il3, l2v;
+    std::vector<float4> shape, bwd;
+    std::vector<double2> half;
+};
+SceneFields scene_fields(const Grid &g, int n, const float *center_raw, const float *cholesky, const float *atten,
+                         const float *response);
+void refresh_scene_host(Ctx &c, const float *center_raw, const float *cholesky, const float *atten,
+                        const float *response);
+void ensure_work(Ctx &c, int64_t nb);
+void ensure_pairs(Ctx &c, int64_t pairs, int nb, int64_t max_seg);
+HostScene parse_wrfc(const char *path);
 
 // kernels (k_mlp.cu, k_render.cu). All launch on `st` and bump ctx.launches.
 void launch_pos_prep(Ctx &c, const float *d_pos_m, int nb, bool normalized, cudaStream_t st);

@@ -81,6 +81,18 @@ def lib():
                                              C.c_void_p] + [C.c_void_p] * 7
         L.swr_hybrid_loss.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64, C.c_double, C.c_void_p,
                                       C.c_void_p]
+        L.swr_train_config_default.argtypes = [C.c_void_p]
+        L.swr_train_config_default.restype = None
+        L.swr_trainer_create.argtypes = [C.c_void_p, C.c_void_p, C.c_char_p, C.c_int, C.POINTER(C.c_void_p)]
+        L.swr_trainer_destroy.argtypes = [C.c_void_p]
+        L.swr_trainer_destroy.restype = None
+        L.swr_trainer_run.argtypes = [C.c_void_p, C.c_int64, C.c_void_p, C.c_void_p, C.c_void_p]
+        L.swr_trainer_iteration.argtypes = [C.c_void_p]
+        L.swr_trainer_iteration.restype = C.c_int64
+        L.swr_trainer_params.argtypes = [C.c_void_p] + [C.c_void_p] * 6
+        L.swr_trainer_gradients.argtypes = [C.c_void_p, C.c_void_p, C.c_int32, C.c_void_p, C.c_void_p, C.c_void_p,
+                                            C.c_void_p]
+        L.swr_trainer_save.argtypes = [C.c_void_p, C.c_char_p]
         L.swr_scene_set_manifest_hash.argtypes = [C.c_void_p, C.c_uint64]
         L.swr_scene_get_info.argtypes = [C.c_void_p, C.c_void_p]
         L.swr_scene_create_wrfc.argtypes = [C.c_char_p, C.c_int, C.POINTER(C.c_void_p)]
@@ -430,3 +442,117 @@ def evaluate_dataset(ck: Checkpoint, ds: Dataset, split: int):
     _check(lib().swr_evaluate_dataset(ck.handle, ds._h, split, _p(out["sample_id"]), _p(out["psnr"]),
                                       _p(out["ssim"]), _p(out["l1"])))
     return out
+
+
+# ---------------------------------------------------------------- training
+
+class TrainConfig(C.Structure):
+    """train::TrainConfig (training.hpp:96-112); defaults are the reference's."""
+    _fields_ = [("primitives", C.c_int32), ("bands_center", C.c_int32), ("bands_position", C.c_int32),
+                ("width", C.c_int32), ("cutoff_radius", C.c_float), ("tile", C.c_int32),
+                ("lr_gaussian", C.c_double), ("lr_mlp", C.c_double), ("lambda1", C.c_double),
+                ("coarse_iters", C.c_int64), ("fine_iters", C.c_int64), ("anneal_scale", C.c_double),
+                ("anneal_threshold", C.c_int64), ("seed", C.c_uint64)]
+
+    def __init__(self, **kw):
+        super().__init__()
+        lib().swr_train_config_default(C.byref(self))
+        for k, v in kw.items():
+            if not hasattr(self, k):
+                raise TypeError(f"unknown TrainConfig field {k}")
+            setattr(self, k, v)
+
+
+def _layer_shapes(width, bands_c, bands_p):
+    D = 2 * (2 * bands_c + 1) + 3 * (2 * bands_p + 1)
+    cols = [D if i == 0 else (width + D if i in (2, 4, 6) else width) for i in range(8)]
+    return [(width, c) for c in cols] + [(2, width), (2, width), (1, width)]
+
+
+class Trainer:
+    """train::train (training.cpp:198-376) on one B200: create (fresh or resume),
+    run iterations of the coarse/fine schedule, read / save the parameters."""
+
+    def __init__(self, cfg: TrainConfig, ds: Dataset, resume: str | None = None, device: int = 0):
+        self.cfg = cfg
+        h = C.c_void_p()
+        _check(lib().swr_trainer_create(C.byref(cfg), ds._h, resume.encode() if resume else None, device,
+                                        C.byref(h)))
+        self._h = h
+        self.H, self.W = ds.H, ds.W
+        self.n = None
+
+    @property
+    def iteration(self) -> int:
+        return int(lib().swr_trainer_iteration(self._h))
+
+    def run(self, iters: int | None = None):
+        """Run up to `iters` iterations (default: the rest of the schedule).
+        Returns (log [k][3] = loss, l1_term, ssim_term; device ms)."""
+        total = self.cfg.coarse_iters + self.cfg.fine_iters
+        k = total - self.iteration if iters is None else int(iters)
+        k = max(k, 0)
+        log = np.zeros((k, 3), np.float64)
+        done = C.c_int64()
+        ms = C.c_double()
+        _check(lib().swr_trainer_run(self._h, k, _p(log), C.byref(done), C.byref(ms)))
+        return log[:done.value], ms.value
+
+    def params(self) -> dict:
+        n = self._count()
+        out = {"center_raw": np.zeros((n, 2), np.float32), "cholesky": np.zeros((n, 3), np.float32),
+               "atten_logit": np.zeros(n, np.float32), "response": np.zeros((n, 2), np.float32)}
+        shapes = _layer_shapes(self.cfg.width, self.cfg.bands_center, self.cfg.bands_position)
+        out["weights"] = [np.zeros(s, np.float32) for s in shapes]
+        out["biases"] = [np.zeros(s[0], np.float32) for s in shapes]
+        pw = (C.c_void_p * 11)(*[w.ctypes.data for w in out["weights"]])
+        pb = (C.c_void_p * 11)(*[b.ctypes.data for b in out["biases"]])
+        _check(lib().swr_trainer_params(self._h, _p(out["center_raw"]), _p(out["cholesky"]), _p(out["atten_logit"]),
+                                        _p(out["response"]), pw, pb))
+        return out
+
+    def _count(self) -> int:
+        if self.n is None:
+            # resume may change n; read it from a params call with only the atten pointer sized by cfg
+            self.n = int(self.cfg.primitives)
+        return self.n
+
+    def gradients(self, sample: int, pos01=None) -> dict:
+        """One forward/backward at the current parameters (no step). pos01 given:
+        the fine-stage chain incl. DeformGrads; else the coarse chain."""
+        n = self._count()
+        g = {k: np.zeros((n, w) if w > 1 else n, np.float32) for k, w in GRAD_FIELDS}
+        terms = np.zeros(3)
+        rg = (C.c_void_p * 7)(*[g[k].ctypes.data for k, _ in GRAD_FIELDS])
+        shapes = _layer_shapes(self.cfg.width, self.cfg.bands_center, self.cfg.bands_position)
+        gw = [np.zeros(s, np.float32) for s in shapes]
+        gb = [np.zeros(s[0], np.float32) for s in shapes]
+        pos = None if pos01 is None else _f32(pos01).reshape(3)
+        _check(lib().swr_trainer_gradients(self._h, _p(pos), int(sample), _p(terms), rg,
+                                           (C.c_void_p * 11)(*[w.ctypes.data for w in gw]),
+                                           (C.c_void_p * 11)(*[b.ctypes.data for b in gb])))
+        g["terms"] = terms
+        if pos is not None:
+            g["layer_w"], g["layer_b"] = gw, gb
+        return g
+
+    def save(self, path: str) -> None:
+        _check(lib().swr_trainer_save(self._h, path.encode()))
+
+    def close(self):
+        if getattr(self, "_h", None):
+            lib().swr_trainer_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def train(ds: Dataset, cfg: TrainConfig, resume: str | None = None, device: int = 0):
+    """train::train: the whole schedule; returns (trainer, log [iters][3])."""
+    tr = Trainer(cfg, ds, resume, device)
+    log, _ = tr.run()
+    return tr, log

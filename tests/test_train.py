@@ -1,0 +1,186 @@
+"""Device training against the reference's own
+train::train compiled from its sources (oracle/_ref):
+
+  * initial state (init_random + DeformNet::init draws from the seed): bit-exact;
+  * one iteration's gradients (coarse chain, and fine chain incl. DeformGrads) at
+    identical parameters: max |GPU - ref| <= 1e-5 * max |ref| per RenderGrads
+    field, <= 1e-4 * max |ref| per network tensor (FP32 both; summation orders
+    differ: per-lane cell sums, split-K GEMMs vs the reference's loops);
+  * the schedule (sample draws, stage switch, Adam, width floors): the first
+    iteration's loss matches to 1e-6, the coarse-stage log to 1e-3 (the fine
+    stage only statistically: see test_schedule_tracks_reference);
+  * the reference's own training tests restated (test_training.cpp:228-350):
+    reproducible, loss decreases, fine stage freezes the centres, resume.
+"""
+import csv
+
+import numpy as np
+import pytest
+
+import oracle as O
+from paper_2506_12787_b200 import swr
+from paper_2506_12787_b200.scene import make_scene
+
+pytestmark = pytest.mark.gpu
+FIELDS = ("center_raw", "cholesky", "atten_logit", "response")
+
+
+def cfg(**kw):
+    base = dict(primitives=6, coarse_iters=12, fine_iters=8, anneal_threshold=5, seed=99)
+    base.update(kw)
+    return swr.TrainConfig(**base)
+
+
+@pytest.fixture(scope="module")
+def tiny(tmp_path_factory):
+    d = str(tmp_path_factory.mktemp("tiny"))
+    O.make_dataset(d, 12, 16, 8, 5)
+    return d
+
+
+@pytest.fixture(scope="module")
+def full(tmp_path_factory):
+    d = str(tmp_path_factory.mktemp("full"))
+    O.make_dataset(d, 90, 360, 6, 7)
+    return d
+
+
+@pytest.fixture(scope="module")
+def refapi():
+    return O.Reference(scene=make_scene(4, seed=1, H=12, W=16, width=24))
+
+
+def _close(got, want, tol, name):
+    scale = max(1e-12, float(np.abs(want).max()))
+    err = float(np.abs(got - want).max())
+    assert err <= tol * scale, f"{name}: max err {err:.3e} vs scale {scale:.3e}"
+
+
+def test_init_matches_reference_bitwise(full, refapi):
+    c = cfg(primitives=500, coarse_iters=0, fine_iters=0)
+    tr = swr.Trainer(c, swr.Dataset(full))
+    got = tr.params()
+    want = refapi.train(full, c)
+    for k in FIELDS:
+        np.testing.assert_array_equal(got[k], getattr(want.sc, k), err_msg=k)
+    for i, (a, b) in enumerate(zip(got["weights"], want.sc.weights)):
+        np.testing.assert_array_equal(a, b, err_msg=f"layer {i}")
+    for a, b in zip(got["biases"], want.sc.biases):
+        np.testing.assert_array_equal(a, b)
+
+
+def test_coarse_and_fine_gradients_match_reference(full, tmp_path):
+    c = cfg(primitives=1500, coarse_iters=3, fine_iters=3, anneal_threshold=100)
+    ds = swr.Dataset(full)
+    tr = swr.Trainer(c, ds)
+    tr.run()  # 3 coarse + 3 fine steps: heads non-zero, trunk gradients live
+    path = str(tmp_path / "state.wrfc")
+    tr.save(path)
+    ref = O.Reference(path=path)
+    _, spec = ds.read([1])
+    pos01 = np.array([0.31, 0.52, 0.77], np.float32)
+    for p in (None, pos01):
+        got = tr.gradients(1, p)
+        want = ref.gradients(spec[0], c.lambda1, p)
+        assert np.abs(got["terms"] - want["terms"]).max() <= 1e-6 * abs(want["terms"][0]) + 1e-9
+        for k, _ in swr.GRAD_FIELDS:
+            _close(got[k], want[k], 1e-5, k)
+        if p is not None:
+            for i in range(11):
+                _close(got["layer_w"][i], want["layer_w"][i], 1e-4, f"dW{i}")
+                _close(got["layer_b"][i], want["layer_b"][i], 1e-4, f"db{i}")
+            assert any(np.abs(w).max() > 0 for w in got["layer_w"][:8])  # trunk actually exercised
+
+
+def test_schedule_tracks_reference(full, refapi, tmp_path):
+    c = cfg(primitives=1500, coarse_iters=20, fine_iters=10, anneal_threshold=6)
+    tr = swr.Trainer(c, swr.Dataset(full))
+    log, _ = tr.run()
+    path = str(tmp_path / "ref_log.csv")
+    refapi.train(full, c, log_path=path)
+    want = np.array([[float(x) for x in r[2:5]] for r in list(csv.reader(open(path)))[1:]])
+    assert log.shape == want.shape == (30, 3)
+    assert abs(log[0, 0] - want[0, 0]) <= 1e-6 * want[0, 0]
+    rel = np.abs(log[:, 0] - want[:, 0]) / want[:, 0]
+    print("relative loss-log deviation per iteration:", np.array2string(rel, precision=2))
+    # coarse stage: rounding-level drift only (Adam on the Gaussians is smooth here)
+    assert rel[:20].max() <= 1e-3
+    # first fine iteration: same sample, residuals from the identical fresh net
+    assert rel[20] <= 1e-2
+    # later fine iterations: Adam's first network steps are ~lr * sign(g) for all
+    # 223k weights, so gradients that differ by rounding near zero flip whole
+    # +-lr steps; the trajectories stay statistically alike, not bitwise
+    assert np.all(np.isfinite(log)) and abs(log[21:, 0].mean() / want[21:, 0].mean() - 1) <= 0.25
+    np.testing.assert_allclose(log[:, 0], log[:, 1] + log[:, 2], rtol=1e-12)
+
+
+def test_training_reproducible_and_stages(tiny):
+    ds = swr.Dataset(tiny)
+    a = swr.Trainer(cfg(), ds)
+    b = swr.Trainer(cfg(), ds)
+    la, _ = a.run()
+    lb, _ = b.run()
+    assert a.iteration == 20
+    np.testing.assert_array_equal(la, lb)
+    pa, pb = a.params(), b.params()
+    for k in FIELDS:
+        np.testing.assert_array_equal(pa[k], pb[k])
+    for wa, wb in zip(pa["weights"], pb["weights"]):
+        np.testing.assert_array_equal(wa, wb)
+    # fine stage freezes the centres bit for bit and moves the rest (test_training.cpp:294-322)
+    before = swr.Trainer(cfg(coarse_iters=0, fine_iters=0), ds).params()
+    after_t = swr.Trainer(cfg(coarse_iters=0, fine_iters=10), ds)
+    after_t.run()
+    after = after_t.params()
+    np.testing.assert_array_equal(after["center_raw"], before["center_raw"])
+    assert not np.array_equal(after["cholesky"], before["cholesky"])
+    assert not np.array_equal(after["response"], before["response"])
+    assert not np.array_equal(after["weights"][8], before["weights"][8])
+    coarse_t = swr.Trainer(cfg(coarse_iters=10, fine_iters=0), ds)
+    coarse_t.run()
+    coarse = coarse_t.params()
+    assert not np.array_equal(coarse["center_raw"], before["center_raw"])
+    np.testing.assert_array_equal(coarse["weights"][8], before["weights"][8])
+
+
+def test_loss_decreases_on_overfittable_scene(tiny):
+    tr = swr.Trainer(cfg(primitives=24, coarse_iters=150, fine_iters=0), swr.Dataset(tiny))
+    log, _ = tr.run()
+    assert log.shape == (150, 3) and log[0, 0] > 0
+    assert log[:15, 0].sum() > log[-15:, 0].sum()
+
+
+def test_resume_and_validation(tiny, tmp_path):
+    ds = swr.Dataset(tiny)
+    full_run = swr.Trainer(cfg(), ds)
+    full_run.run(10)
+    p = str(tmp_path / "mid.wrfc")
+    full_run.save(p)
+    res = swr.Trainer(cfg(), ds, resume=p)
+    assert res.iteration == 10
+    log, _ = res.run()
+    assert res.iteration == 20 and log.shape == (10, 3)
+    with pytest.raises(ValueError):
+        swr.Trainer(cfg(lr_gaussian=2e-2), ds, resume=p)
+    with pytest.raises(ValueError):
+        swr.Trainer(cfg(lambda1=1.5), ds)
+    with pytest.raises(ValueError):
+        swr.Trainer(cfg(coarse_iters=-1), ds)
+    other = str(tmp_path / "other")
+    O.make_dataset(other, 12, 16, 8, 6)
+    with pytest.raises(RuntimeError):
+        swr.Trainer(cfg(), swr.Dataset(other), resume=p)
+
+
+def test_saved_checkpoint_renders_like_reference(tiny, tmp_path):
+    tr = swr.Trainer(cfg(primitives=40), swr.Dataset(tiny))
+    tr.run()
+    p = str(tmp_path / "done.wrfc")
+    tr.save(p)
+    ref = O.Reference(path=p)
+    assert ref.iteration() == 20
+    ck = swr.load_checkpoint(p)
+    pos = np.array([[1.0, 2.0, 1.5]], np.float32)
+    got = swr.render(ck, pos, pooled=False, aoa=False)["spectra"][0]
+    want = ref.render_at(pos[0])
+    assert np.abs(got - want).max() <= 1e-5 * max(1.0, np.abs(want).max())
