@@ -43,13 +43,14 @@ __device__ __forceinline__ void adam1(float &p, float g, float &m, float &v, con
 namespace
 {
 
-__global__ void gauss_adam_kernel(Grid g, SceneDev sd, GaussDev gp, AdamHp hp, double bc1_c, double bc2_c,
-                                  double bc1, double bc2, int step_center, int step_rest, float floor_el,
-                                  float floor_az)
+__global__ void gauss_adam_kernel(Grid g, SceneDev sd, GaussDev gp, AdamHp hp, TrainSched sc, int step_center,
+                                  int step_rest, float floor_el, float floor_az)
 {
     const int p = blockIdx.x * blockDim.x + threadIdx.x;
     if (p >= g.n)
         return;
+    const double *bc = sc.bc + 6 * *sc.it; // (center bc1, bc2, rest bc1, bc2, net bc1, bc2)
+    const double bc1_c = bc[0], bc2_c = bc[1], bc1 = bc[2], bc2 = bc[3];
     float cr[2] = {gp.center[2 * p], gp.center[2 * p + 1]};
     float ch[3] = {gp.chol[3 * p], gp.chol[3 * p + 1], gp.chol[3 * p + 2]};
     float at = gp.atten[p];
@@ -103,8 +104,9 @@ __global__ void gauss_adam_kernel(Grid g, SceneDev sd, GaussDev gp, AdamHp hp, d
 }
 
 __global__ void adam_flat_kernel(float *__restrict__ p, const float *__restrict__ gr, float *__restrict__ m,
-                                 float *__restrict__ v, int64_t count, AdamHp hp, double bc1, double bc2)
+                                 float *__restrict__ v, int64_t count, AdamHp hp, TrainSched sc)
 {
+    const double bc1 = sc.bc[6 * *sc.it + 4], bc2 = sc.bc[6 * *sc.it + 5];
     for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < count; i += int64_t(gridDim.x) * blockDim.x)
     {
         float x = p[i], mm = m[i], vv = v[i];
@@ -346,41 +348,74 @@ __global__ void pack_dr_kernel(const float *__restrict__ d_center, const float *
 }
 
 // input rows x[m] = [encode(centre_m) (static), encode(position)] (deform.cpp:157-168)
-__global__ void penc_kernel(float *__restrict__ x, int n, int d, int dc, const float *__restrict__ penc, int dp)
+__global__ void penc_kernel(float *__restrict__ x, int n, int d, int dc, TrainSched sc, int dp)
 {
     const int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
     if (e >= int64_t(n) * dp)
         return;
     const int m = int(e / dp), k = int(e % dp);
-    x[int64_t(m) * d + dc + k] = penc[k];
+    x[int64_t(m) * d + dc + k] = sc.penc[*sc.it * dp + k];
+}
+
+// this iteration's training target (the drawn sample's spectrum) into a fixed buffer
+__global__ void gather_target_kernel(const float4 *__restrict__ spectra, int64_t per4, TrainSched sc,
+                                     float4 *__restrict__ out)
+{
+    const float4 *src = spectra + per4 * sc.idx[*sc.it];
+    for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < per4; i += int64_t(gridDim.x) * blockDim.x)
+        out[i] = src[i];
+}
+
+// the loss-log row of this iteration, then advance the schedule cursor
+__global__ void log_advance_kernel(const double *__restrict__ terms, double *__restrict__ log, TrainSched sc)
+{
+    const int64_t it = *sc.it;
+    log[3 * it + 0] = terms[0];
+    log[3 * it + 1] = terms[1];
+    log[3 * it + 2] = terms[2];
+    *sc.it = it + 1;
 }
 
 inline int blocks(int64_t n, int t) { return int((n + t - 1) / t); }
 
 } // namespace
 
-void launch_gauss_adam(Ctx &c, const GaussDev &gp, const AdamHp &hp, double bc1_c, double bc2_c, double bc1,
-                       double bc2, bool step_center, bool step_rest, float floor_el, float floor_az, cudaStream_t st)
+void launch_gauss_adam(Ctx &c, const GaussDev &gp, const AdamHp &hp, const TrainSched &sc, bool step_center,
+                       bool step_rest, float floor_el, float floor_az, cudaStream_t st)
 {
     if (c.g.n == 0)
         return;
-    gauss_adam_kernel<<<blocks(c.g.n, 256), 256, 0, st>>>(c.g, c.s, gp, hp, bc1_c, bc2_c, bc1, bc2, step_center,
-                                                           step_rest, floor_el, floor_az);
+    gauss_adam_kernel<<<blocks(c.g.n, 256), 256, 0, st>>>(c.g, c.s, gp, hp, sc, step_center, step_rest, floor_el,
+                                                           floor_az);
     c.launches++;
 }
 
 void launch_adam_flat(Ctx &c, float *p, const float *g, float *m, float *v, int64_t count, const AdamHp &hp,
-                      double bc1, double bc2, cudaStream_t st)
+                      const TrainSched &sc, cudaStream_t st)
 {
     if (count == 0)
         return;
-    adam_flat_kernel<<<std::min<int64_t>(blocks(count, 256), 148 * 8), 256, 0, st>>>(p, g, m, v, count, hp, bc1, bc2);
+    adam_flat_kernel<<<std::min<int64_t>(blocks(count, 256), 148 * 8), 256, 0, st>>>(p, g, m, v, count, hp, sc);
     c.launches++;
 }
 
-void launch_position_encoding(Ctx &c, float *x, int d, int dc, const float *d_penc, int dp, cudaStream_t st)
+void launch_position_encoding(Ctx &c, float *x, int d, int dc, const TrainSched &sc, int dp, cudaStream_t st)
 {
-    penc_kernel<<<blocks(int64_t(c.g.n) * dp, 256), 256, 0, st>>>(x, c.g.n, d, dc, d_penc, dp);
+    penc_kernel<<<blocks(int64_t(c.g.n) * dp, 256), 256, 0, st>>>(x, c.g.n, d, dc, sc, dp);
+    c.launches++;
+}
+
+void launch_gather_target(Ctx &c, const float *spectra, const TrainSched &sc, float *out, cudaStream_t st)
+{
+    const int64_t per4 = int64_t(c.g.H) * c.g.W / 2; // 2 H W floats
+    gather_target_kernel<<<std::min<int64_t>(blocks(per4, 256), 148 * 2), 256, 0, st>>>(
+        reinterpret_cast<const float4 *>(spectra), per4, sc, reinterpret_cast<float4 *>(out));
+    c.launches++;
+}
+
+void launch_log_advance(Ctx &c, const double *terms, double *log, const TrainSched &sc, cudaStream_t st)
+{
+    log_advance_kernel<<<1, 1, 0, st>>>(terms, log, sc);
     c.launches++;
 }
 

@@ -173,11 +173,23 @@ struct GaussDev
     const float *g_center, *g_chol, *g_atten, *g_resp;     // rasterize_backward outputs
 };
 
-void launch_gauss_adam(Ctx &c, const GaussDev &gp, const AdamHp &hp, double bc1_c, double bc2_c, double bc1,
-                       double bc2, bool step_center, bool step_rest, float floor_el, float floor_az, cudaStream_t st);
+// Per-iteration arguments read on the device (so one captured iteration replays
+// as a CUDA graph): entry *it of each table; log_advance bumps *it.
+struct TrainSched
+{
+    const int *idx;     // [iters] training sample
+    const float *penc;  // [iters][dp] position encoding (fine stage)
+    const double *bc;   // [iters][6] Adam bias corrections (centre, rest, network)
+    int64_t *it;        // device cursor
+};
+
+void launch_gauss_adam(Ctx &c, const GaussDev &gp, const AdamHp &hp, const TrainSched &sc, bool step_center,
+                       bool step_rest, float floor_el, float floor_az, cudaStream_t st);
 void launch_adam_flat(Ctx &c, float *p, const float *g, float *m, float *v, int64_t count, const AdamHp &hp,
-                      double bc1, double bc2, cudaStream_t st);
-void launch_position_encoding(Ctx &c, float *x, int d, int dc, const float *d_penc, int dp, cudaStream_t st);
+                      const TrainSched &sc, cudaStream_t st);
+void launch_position_encoding(Ctx &c, float *x, int d, int dc, const TrainSched &sc, int dp, cudaStream_t st);
+void launch_gather_target(Ctx &c, const float *spectra, const TrainSched &sc, float *out, cudaStream_t st);
+void launch_log_advance(Ctx &c, const double *terms, double *log, const TrainSched &sc, cudaStream_t st);
 void launch_dense_fwd(Ctx &c, const float *a1, int ld1, int ka, const float *a2, int ld2, int K, const float *W,
                       const float *b, int width, float *h, cudaStream_t st);
 void launch_heads_fwd(Ctx &c, const float *h7, int width, const float *Wh, const float *bh, float *planes,

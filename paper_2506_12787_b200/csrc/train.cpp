@@ -25,6 +25,7 @@
 
 #include <chrono>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <fstream>
 #include <memory>
@@ -161,14 +162,24 @@ struct Trainer
     float *net_p = nullptr, *net_g = nullptr, *net_m = nullptr, *net_v = nullptr;
     int64_t t_net = 0;
     float *x0 = nullptr, *h[kTrunkLayers]{}, *dz_a = nullptr, *dz_b = nullptr, *dr5 = nullptr, *part = nullptr;
-    float *d_penc = nullptr, *h_penc = nullptr; // pinned ring of per-iteration position encodings
-    int penc_ring = 0;
-    // render / loss scratch
-    float *d_pred = nullptr, *d_lgrad = nullptr, *d_state = nullptr, *d_slots = nullptr;
-    int64_t slots_cap = 0;
+    // per-iteration plan (device tables indexed by iteration - it_base) + cursor
+    int64_t it_base = 0;
+    int *d_sidx = nullptr;
+    float *d_spenc = nullptr;
+    double *d_sbc = nullptr, *d_log = nullptr;
+    TrainSched sched{};
+    int *g_sidx = nullptr; // one-entry plan of gradients()
+    float *g_spenc = nullptr;
+    double *g_sbc = nullptr;
+    int64_t *g_it = nullptr;
+    bool use_graphs = true;
+    cudaGraphExec_t graph[2]{};
+    int64_t graph_launches[2]{};
+    // render / loss scratch (worst-case sized)
+    int64_t pair_cap = 0;
+    float *d_pred = nullptr, *d_lgrad = nullptr, *d_target = nullptr, *d_state = nullptr, *d_slots = nullptr;
     float *grads[7]{};
-    double *d_tmp = nullptr, *d_log = nullptr;
-    int64_t log_cap = 0;
+    double *d_tmp = nullptr, *d_terms = nullptr;
     int *d_bad = nullptr;
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
 
@@ -183,15 +194,16 @@ struct Trainer
             cudaFree(p);
         if (c.w.host_pairs)
             cudaFreeHost(c.w.host_pairs);
-        if (h_penc)
-            cudaFreeHost(h_penc);
+        for (auto &gx : graph)
+            if (gx)
+                cudaGraphExecDestroy(gx);
         if (c.stream)
             cudaStreamDestroy(c.stream);
     }
 
     void reset_opt()
     {
-        // training.cpp:257-268: fresh moments, step counters back to zero
+        // training.cpp:257-268: fresh moments (the step counters restart in run()'s plan)
         cudaStream_t st = c.stream;
         for (float *p : {gp.m_center, gp.v_center})
             check_cuda(cudaMemsetAsync(p, 0, sizeof(float) * 2 * std::max(n, 1), st), "memset");
@@ -203,7 +215,6 @@ struct Trainer
             check_cuda(cudaMemsetAsync(p, 0, sizeof(float) * 2 * std::max(n, 1), st), "memset");
         for (float *p : {net_m, net_v})
             check_cuda(cudaMemsetAsync(p, 0, sizeof(float) * P, st), "memset");
-        t_center = t_rest = t_net = 0;
     }
 
     void setup_net_layout()
@@ -308,15 +319,31 @@ struct Trainer
         dz_b = dalloc<float>(c, nn * width);
         dr5 = dalloc<float>(c, nn * 5);
         part = dalloc<float>(c, dw_partial_floats(n, width, width + D + 1));
-        penc_ring = 1024;
-        d_penc = dalloc<float>(c, size_t(penc_ring) * Dp);
-        check_cuda(cudaHostAlloc((void **)&h_penc, sizeof(float) * penc_ring * Dp, cudaHostAllocDefault), "host alloc");
         const size_t per = size_t(2) * H * W;
         d_pred = dalloc<float>(c, per);
         d_lgrad = dalloc<float>(c, per);
+        d_target = dalloc<float>(c, per);
         d_state = dalloc<float>(c, nn * 11);
         d_tmp = dalloc<double>(c, loss_tmp_doubles(c, 1));
+        d_terms = dalloc<double>(c, 3);
         d_bad = dalloc<int>(c, 1);
+        // every (tile, primitive) pair of one position at most: no pair-count sync
+        pair_cap = std::max<int64_t>(int64_t(n) * c.g.tiles, 1024);
+        ensure_pairs(c, pair_cap, 1, pair_cap);
+        d_slots = dalloc<float>(c, size_t(pair_cap) * 8);
+        const int64_t cap = std::max<int64_t>(total - iteration, 1);
+        it_base = iteration;
+        d_sidx = dalloc<int>(c, size_t(cap));
+        d_spenc = dalloc<float>(c, size_t(cap) * Dp);
+        d_sbc = dalloc<double>(c, size_t(cap) * 6);
+        d_log = dalloc<double>(c, size_t(cap) * 3);
+        sched = TrainSched{d_sidx, d_spenc, d_sbc, dalloc<int64_t>(c, 1)};
+        g_sidx = dalloc<int>(c, 1);
+        g_spenc = dalloc<float>(c, size_t(Dp));
+        g_sbc = dalloc<double>(c, 6);
+        g_it = dalloc<int64_t>(c, 1);
+        const char *env = std::getenv("SWR_TRAIN_GRAPHS");
+        use_graphs = !(env && env[0] == '0');
         check_cuda(cudaEventCreate(&ev0), "event");
         check_cuda(cudaEventCreate(&ev1), "event");
     }
@@ -366,36 +393,31 @@ struct Trainer
         }
     }
 
-    void render_and_backward(int idx, bool with_res, double *log_row)
+    // ---------------------------------------------------------------- device step
+    // Everything an iteration enqueues reads its per-iteration arguments through
+    // a TrainSched (device tables + cursor), and every buffer is sized for the
+    // worst case at creation (pairs <= n * tiles per position), so one iteration
+    // is a fixed launch sequence: captured once per stage and replayed as a CUDA
+    // graph, with no host round trip inside the loop.
+
+    void render_and_backward(const TrainSched &sc, bool with_res)
     {
         cudaStream_t st = c.stream;
-        const size_t per = size_t(2) * H * W;
+        launch_gather_target(c, d_spectra, sc, d_target, st);
         launch_setup(c, 1, with_res, st);
         launch_bin_count(c, 1, st);
-        check_cuda(cudaMemcpyAsync(c.w.host_pairs, c.w.stats, 2 * sizeof(int64_t), cudaMemcpyDeviceToHost, st),
-                   "D2H pair count");
-        check_cuda(cudaStreamSynchronize(st), "pair count");
-        const int64_t pairs = c.w.host_pairs[0], max_seg = c.w.host_pairs[1];
-        ensure_pairs(c, pairs, 1, max_seg);
-        launch_bin_sort(c, 1, pairs, int(max_seg), st);
+        launch_bin_sort(c, 1, pair_cap, int(pair_cap), st);
         launch_raster(c, 1, d_pred, false, st);
-        launch_hybrid_loss(c, d_pred, d_spectra + per * size_t(idx), 1, cfg.lambda1, log_row, d_lgrad, d_tmp, d_bad,
-                           st);
+        launch_hybrid_loss(c, d_pred, d_target, 1, cfg.lambda1, d_terms, d_lgrad, d_tmp, d_bad, st);
         launch_state_out(c, 1, with_res, d_state, st);
-        if (pairs > slots_cap)
-        {
-            dfree(c, d_slots);
-            slots_cap = std::max<int64_t>(pairs + pairs / 4, 1024);
-            d_slots = dalloc<float>(c, size_t(slots_cap) * 8);
-        }
         launch_raster_backward(c, 1, d_state, d_lgrad, d_slots, st);
         launch_bwd_merge(c, 1, with_res, d_slots, grads, st);
     }
 
-    void net_forward(int ring_slot)
+    void net_forward(const TrainSched &sc)
     {
         cudaStream_t st = c.stream;
-        launch_position_encoding(c, x0, D, Dc, d_penc + size_t(ring_slot) * Dp, Dp, st);
+        launch_position_encoding(c, x0, D, Dc, sc, Dp, st);
         const float *prev = x0;
         for (int i = 0; i < kTrunkLayers; i++)
         {
@@ -408,16 +430,16 @@ struct Trainer
                 launch_dense_fwd(c, prev, width, width, nullptr, 0, width, Wl, bl, width, h[i], st);
             prev = h[i];
         }
-        launch_heads_fwd(c, h[kTrunkLayers - 1], width, net_p + off_w[kTrunkLayers], net_p + off_b[kTrunkLayers], c.w.res,
-                         int64_t(c.w.cap_b) * c.g.np, st);
+        launch_heads_fwd(c, h[kTrunkLayers - 1], width, net_p + off_w[kTrunkLayers], net_p + off_b[kTrunkLayers],
+                         c.w.res, int64_t(c.w.cap_b) * c.g.np, st);
     }
 
     void net_backward()
     {
         cudaStream_t st = c.stream;
         const float *Wh = net_p + off_w[kTrunkLayers];
-        launch_heads_bwd(c, grads[4], grads[5], grads[6], Wh, Wh + 2 * width, Wh + 4 * width, h[kTrunkLayers - 1], width,
-                         dz_a, dr5, st);
+        launch_heads_bwd(c, grads[4], grads[5], grads[6], Wh, Wh + 2 * width, Wh + 4 * width, h[kTrunkLayers - 1],
+                         width, dz_a, dr5, st);
         launch_dense_bwd_weights(c, dr5, 5, h[kTrunkLayers - 1], width, width, nullptr, 0, width, part,
                                  net_g + off_w[kTrunkLayers], net_g + off_b[kTrunkLayers], st);
         float *dz = dz_a, *dz_next = dz_b;
@@ -438,37 +460,60 @@ struct Trainer
         }
     }
 
-    void step(int64_t it, double *log_row, int ring_slot_if_fine, int idx)
+    // one full training iteration (training.cpp:312-376) on the stream
+    void enqueue_step(bool coarse)
     {
         cudaStream_t st = c.stream;
         const AdamHp hp_g{cfg.lr_gaussian, 0.9, 0.999, 1e-8}, hp_n{cfg.lr_mlp, 0.9, 0.999, 1e-8};
-        const bool coarse = it < cfg.coarse_iters;
         if (coarse)
         {
-            render_and_backward(idx, false, log_row);
-            t_center++;
-            t_rest++;
-            const double b1c = 1.0 - std::pow(0.9, double(t_center)), b2c = 1.0 - std::pow(0.999, double(t_center));
-            const double b1 = 1.0 - std::pow(0.9, double(t_rest)), b2 = 1.0 - std::pow(0.999, double(t_rest));
-            launch_gauss_adam(c, gp, hp_g, b1c, b2c, b1, b2, true, true, floor_el(), floor_az(), st);
+            render_and_backward(sched, false);
+            launch_gauss_adam(c, gp, hp_g, sched, true, true, floor_el(), floor_az(), st);
+        }
+        else
+        {
+            net_forward(sched);
+            render_and_backward(sched, true);
+            net_backward();
+            launch_adam_flat(c, net_p, net_g, net_m, net_v, P, hp_n, sched, st);
+            launch_gauss_adam(c, gp, hp_g, sched, false, true, floor_el(), floor_az(), st);
+        }
+        launch_log_advance(c, d_terms, d_log, sched, st);
+    }
+
+    // replay `count` iterations of one stage: the first eagerly (lazy kernel
+    // attributes, and a check), the rest through the stage's captured graph
+    void enqueue_iterations(bool coarse, int64_t count)
+    {
+        cudaStream_t st = c.stream;
+        if (count <= 0)
+            return;
+        const int gi = coarse ? 0 : 1;
+        enqueue_step(coarse);
+        check_cuda(cudaGetLastError(), "training launch");
+        if (count == 1)
+            return;
+        if (!use_graphs)
+        {
+            for (int64_t k = 1; k < count; k++)
+                enqueue_step(coarse);
             return;
         }
-        if (!cenc_ready)
+        if (!graph[gi])
         {
-            // centres are frozen in the fine stage: their encodings (and the scene's
-            // centre-derived inputs) are computed once, on the host like the reference
-            host_center_inputs();
-            cenc_ready = true;
+            const int64_t l0 = c.launches;
+            cudaGraph_t g = nullptr;
+            check_cuda(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal), "begin capture");
+            enqueue_step(coarse);
+            check_cuda(cudaStreamEndCapture(st, &g), "end capture");
+            check_cuda(cudaGraphInstantiate(&graph[gi], g, 0), "graph instantiate");
+            cudaGraphDestroy(g);
+            graph_launches[gi] = c.launches - l0;
+            c.launches = l0;
         }
-        net_forward(ring_slot_if_fine);
-        render_and_backward(idx, true, log_row);
-        net_backward();
-        t_net++;
-        t_rest++;
-        const double nb1 = 1.0 - std::pow(0.9, double(t_net)), nb2 = 1.0 - std::pow(0.999, double(t_net));
-        launch_adam_flat(c, net_p, net_g, net_m, net_v, P, hp_n, nb1, nb2, st);
-        const double b1 = 1.0 - std::pow(0.9, double(t_rest)), b2 = 1.0 - std::pow(0.999, double(t_rest));
-        launch_gauss_adam(c, gp, hp_g, 1.0, 1.0, b1, b2, false, true, floor_el(), floor_az(), st);
+        for (int64_t k = 1; k < count; k++)
+            check_cuda(cudaGraphLaunch(graph[gi], st), "graph launch");
+        c.launches += graph_launches[gi] * (count - 1);
     }
 
     // one forward/backward at the current parameters without an optimizer step:
@@ -477,26 +522,26 @@ struct Trainer
     void gradients(const float *pos01, int idx, double *terms)
     {
         cudaStream_t st = c.stream;
-        if (log_cap < 1)
-        {
-            dfree(c, d_log);
-            log_cap = 1;
-            d_log = dalloc<double>(c, 3);
-        }
         check_cuda(cudaMemsetAsync(d_bad, 0, sizeof(int), st), "memset");
         host_center_inputs(); // the reference's exact render / encoding inputs
+        std::vector<float> penc(static_cast<size_t>(Dp), 0.f);
+        if (pos01)
+            encode_host(pos01, 3, cfg.bands_position, penc.data());
+        const int64_t zero = 0;
+        check_cuda(cudaMemcpy(g_sidx, &idx, sizeof(int), cudaMemcpyHostToDevice), "H2D");
+        check_cuda(cudaMemcpy(g_spenc, penc.data(), sizeof(float) * Dp, cudaMemcpyHostToDevice), "H2D");
+        check_cuda(cudaMemcpy(g_it, &zero, sizeof(int64_t), cudaMemcpyHostToDevice), "H2D");
+        const TrainSched gs{g_sidx, g_spenc, g_sbc, g_it};
         if (pos01)
         {
-            encode_host(pos01, 3, cfg.bands_position, h_penc);
-            check_cuda(cudaMemcpyAsync(d_penc, h_penc, sizeof(float) * Dp, cudaMemcpyHostToDevice, st), "H2D");
-            net_forward(0);
-            render_and_backward(idx, true, d_log);
+            net_forward(gs);
+            render_and_backward(gs, true);
             net_backward();
         }
         else
-            render_and_backward(idx, false, d_log);
+            render_and_backward(gs, false);
         check_cuda(cudaGetLastError(), "gradient launch");
-        check_cuda(cudaMemcpyAsync(terms, d_log, sizeof(double) * 3, cudaMemcpyDeviceToHost, st), "D2H");
+        check_cuda(cudaMemcpyAsync(terms, d_terms, sizeof(double) * 3, cudaMemcpyDeviceToHost, st), "D2H");
         check_cuda(cudaStreamSynchronize(st), "gradients");
     }
 
@@ -504,60 +549,104 @@ struct Trainer
     {
         cudaStream_t st = c.stream;
         const int64_t todo = std::max<int64_t>(0, std::min(max_iters, total - iteration));
-        if (todo > log_cap)
+        if (todo == 0)
         {
-            dfree(c, d_log);
-            log_cap = todo;
-            d_log = dalloc<double>(c, size_t(3) * todo);
+            if (ms)
+                *ms = 0.0;
+            return 0;
         }
-        check_cuda(cudaMemsetAsync(d_bad, 0, sizeof(int), st), "memset");
-        check_cuda(cudaEventRecord(ev0, st), "event");
-        NoiseSched sched{cfg.anneal_scale, cfg.anneal_threshold, int(train_idx.size())};
-        int ring = 0;
+        // host plan: the reference's Rng stream, stage switches and Adam step
+        // counters (training.cpp:298-376) -> device tables
+        const int64_t slot0 = iteration - it_base;
+        std::vector<int> sidx(static_cast<size_t>(todo));
+        std::vector<float> spenc(size_t(todo) * Dp, 0.f);
+        std::vector<double> sbc(size_t(todo) * 6, 1.0);
+        const double count = double(std::max<size_t>(train_idx.size(), 1));
+        bool fine_seen = in_fine;
+        int64_t first_fine = todo; // index of the first fine iteration of this run
         for (int64_t k = 0; k < todo; k++)
         {
             const int64_t it = iteration + k;
             const bool coarse = it < cfg.coarse_iters;
-            if (!coarse && !in_fine)
+            if (!coarse && !fine_seen)
             {
-                reset_opt(); // training.cpp:305-310
-                in_fine = true;
+                fine_seen = true; // moments and step counters restart (training.cpp:305-310)
+                t_center = t_rest = t_net = 0;
             }
+            if (!coarse && first_fine == todo)
+                first_fine = k;
             const int idx = train_idx[size_t(rng.index(train_idx.size()))];
-            int slot = 0;
-            if (!coarse)
+            sidx[size_t(k)] = idx;
+            double *bc = &sbc[size_t(k) * 6];
+            if (coarse)
+            {
+                t_center++;
+                t_rest++;
+                bc[0] = 1.0 - std::pow(0.9, double(t_center));
+                bc[1] = 1.0 - std::pow(0.999, double(t_center));
+            }
+            else
             {
                 float pos[3];
                 normalized_position(idx, pos);
                 const int64_t fine_it = it - cfg.coarse_iters;
-                if (!(sched.scale == 0.0 || fine_it >= sched.threshold)) // training.cpp:116-128
+                if (!(cfg.anneal_scale == 0.0 || fine_it >= cfg.anneal_threshold)) // training.cpp:116-128
                 {
-                    const double amp = sched.scale * (2.0 / std::cbrt(double(std::max(sched.count, 1)))) *
-                                       (1.0 - double(fine_it) / double(sched.threshold));
+                    const double amp = cfg.anneal_scale * (2.0 / std::cbrt(count)) *
+                                       (1.0 - double(fine_it) / double(cfg.anneal_threshold));
                     for (int a = 0; a < 3; a++)
                         pos[a] = pos[a] + float(rng.normal() * amp);
                 }
-                slot = ring;
-                ring = (ring + 1) % penc_ring;
-                // the ring slot is free again once the pair-count sync of a later
-                // iteration has drained the stream (one sync per iteration)
-                encode_host(pos, 3, cfg.bands_position, h_penc + size_t(slot) * Dp);
-                check_cuda(cudaMemcpyAsync(d_penc + size_t(slot) * Dp, h_penc + size_t(slot) * Dp, sizeof(float) * Dp,
-                                           cudaMemcpyHostToDevice, st),
-                           "H2D position encoding");
+                encode_host(pos, 3, cfg.bands_position, &spenc[size_t(k) * Dp]);
+                t_net++;
+                t_rest++;
+                bc[4] = 1.0 - std::pow(0.9, double(t_net));
+                bc[5] = 1.0 - std::pow(0.999, double(t_net));
             }
-            step(it, d_log + 3 * k, slot, idx);
+            bc[2] = 1.0 - std::pow(0.9, double(t_rest));
+            bc[3] = 1.0 - std::pow(0.999, double(t_rest));
         }
-        check_cuda(cudaEventRecord(ev1, st), "event");
-        check_cuda(cudaGetLastError(), "training launch");
-        check_cuda(cudaStreamSynchronize(st), "training");
-        float f = 0.f;
-        check_cuda(cudaEventElapsedTime(&f, ev0, ev1), "event time");
+        check_cuda(cudaMemcpy(d_sidx + slot0, sidx.data(), sizeof(int) * todo, cudaMemcpyHostToDevice), "H2D plan");
+        check_cuda(cudaMemcpy(d_spenc + slot0 * Dp, spenc.data(), sizeof(float) * spenc.size(), cudaMemcpyHostToDevice),
+                   "H2D plan");
+        check_cuda(cudaMemcpy(d_sbc + slot0 * 6, sbc.data(), sizeof(double) * sbc.size(), cudaMemcpyHostToDevice),
+                   "H2D plan");
+        check_cuda(cudaMemcpy(sched.it, &slot0, sizeof(int64_t), cudaMemcpyHostToDevice), "H2D cursor");
+        check_cuda(cudaMemsetAsync(d_bad, 0, sizeof(int), st), "memset");
+
+        float f_total = 0.f;
+        auto timed = [&](bool coarse, int64_t cnt) {
+            check_cuda(cudaEventRecord(ev0, st), "event");
+            enqueue_iterations(coarse, cnt);
+            check_cuda(cudaEventRecord(ev1, st), "event");
+            check_cuda(cudaStreamSynchronize(st), "training");
+            float f = 0.f;
+            check_cuda(cudaEventElapsedTime(&f, ev0, ev1), "event time");
+            f_total += f;
+        };
+        if (first_fine > 0)
+            timed(true, first_fine);
+        if (first_fine < todo)
+        {
+            if (!in_fine)
+            {
+                reset_opt();
+                in_fine = true;
+            }
+            if (!cenc_ready)
+            {
+                // centres are frozen in the fine stage: their encodings (and the
+                // scene's centre-derived inputs) are computed once, on the host
+                host_center_inputs();
+                cenc_ready = true;
+            }
+            timed(false, todo - first_fine);
+        }
         if (ms)
-            *ms = f;
+            *ms = f_total;
         std::vector<double> host(size_t(3) * todo);
-        if (todo)
-            check_cuda(cudaMemcpy(host.data(), d_log, sizeof(double) * host.size(), cudaMemcpyDeviceToHost), "D2H log");
+        check_cuda(cudaMemcpy(host.data(), d_log + 3 * slot0, sizeof(double) * host.size(), cudaMemcpyDeviceToHost),
+                   "D2H log");
         if (log)
             std::memcpy(log, host.data(), sizeof(double) * host.size());
         iteration += todo;
@@ -570,13 +659,6 @@ struct Trainer
             throw std::runtime_error("hybrid loss is not finite"); // training.cpp:89-90
         return todo;
     }
-
-    struct NoiseSched
-    {
-        double scale;
-        int64_t threshold;
-        int count;
-    };
 
     void save(const std::string &path)
     {
