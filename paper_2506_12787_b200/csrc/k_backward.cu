@@ -20,6 +20,8 @@
 // differ from the reference's sequential sums by rounding only (deterministic).
 #include "swr_internal.h"
 
+#include <cstdlib>
+
 namespace swr
 {
 
@@ -57,12 +59,14 @@ __device__ __forceinline__ float wrap_pm_pi_f(float x)
 __global__ void __launch_bounds__(32 * kBwdWarps)
     raster_bwd_kernel(Grid g, SceneDev sd, const float *__restrict__ state, const int4 *__restrict__ rng,
                       const int64_t *__restrict__ seg, const int *__restrict__ tile_off, const int *__restrict__ prims,
-                      const float *__restrict__ upstream, float *__restrict__ slots)
+                      const float *__restrict__ upstream, float *__restrict__ slots, int split)
 {
     extern __shared__ float2 up[]; // [T*T] upstream gradient of the tile, then BwdRec [warps][32]
     __shared__ float elc[64], azc[32];
     const int T = g.tile, TT = T * T;
-    const int t = blockIdx.x, s = blockIdx.y;
+    // blockIdx.y = position * split + part: `split` CTAs share a tile's pairs
+    // (every pair owns its slot, so the split changes no arithmetic)
+    const int t = blockIdx.x, s = blockIdx.y / split, part = blockIdx.y % split;
     const int tr0 = (t / g.tw) * T, tc0 = (t % g.tw) * T;
     const int tr1 = min(tr0 + T, g.H) - 1, tc1 = min(tc0 + T, g.W) - 1;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -85,7 +89,7 @@ __global__ void __launch_bounds__(32 * kBwdWarps)
     const int tcw = tc1 - tc0 + 1;
     const float cut2 = g.cut2;
 
-    for (int c0 = warp * 32; c0 < cnt; c0 += kBwdWarps * 32)
+    for (int c0 = (part * kBwdWarps + warp) * 32; c0 < cnt; c0 += split * kBwdWarps * 32)
     {
         {
             const int j = c0 + lane;
@@ -263,7 +267,12 @@ __global__ void bwd_merge_kernel(Grid g, SceneDev sd, const float *__restrict__ 
 void launch_raster_backward(Ctx &c, int nb, const float *d_state, const float *d_upstream, float *d_slots,
                             cudaStream_t st)
 {
-    dim3 grid(c.g.tiles, nb);
+    // few positions (training: one) leave most SMs idle with a CTA per tile: split
+    // each tile's pair list over enough CTAs for ~4 per SM
+    int split = std::max(1, std::min(8, (4 * 148 + c.g.tiles * nb - 1) / (c.g.tiles * nb)));
+    if (const char *e = std::getenv("SWR_BWD_SPLIT"))
+        split = std::max(1, std::atoi(e));
+    dim3 grid(c.g.tiles, nb * split);
     const size_t smem = (size_t)c.g.tile * c.g.tile * sizeof(float2) + kBwdWarps * 32 * sizeof(BwdRec);
     static size_t configured = 0;
     if (configured < smem)
@@ -273,7 +282,7 @@ void launch_raster_backward(Ctx &c, int nb, const float *d_state, const float *d
         configured = smem;
     }
     raster_bwd_kernel<<<grid, 32 * kBwdWarps, smem, st>>>(c.g, c.s, d_state, c.w.rng, c.w.seg, c.w.tile_off,
-                                                          c.w.sorted, d_upstream, d_slots);
+                                                          c.w.sorted, d_upstream, d_slots, split);
     c.launches++;
 }
 

@@ -3,10 +3,11 @@
 // train::evaluate (training.cpp:380-406). All statistics in double like the
 // reference ("float/double instantiations agree to roundoff", spectrum.cpp:176).
 //
-//   metrics_point_kernel  one CTA per spectrum pair: sum (a-b)^2 and |a-b| over
-//                         the 2*H*W floats -> PSNR (clamped at 100 dB) and L1;
-//                         counts non-finite inputs (the reference throws
+//   metrics_part_kernel   one CTA per (pair, 8192-float chunk): sum (a-b)^2 and
+//                         |a-b|; counts non-finite inputs (the reference throws
 //                         domain_error, spectrum.cpp:44-49)
+//   metrics_final_kernel  per pair, the chunk sums in order -> PSNR (clamped at
+//                         100 dB) and L1
 //   ssim_h_kernel         one CTA per (pair, channel, row): the 11-tap horizontal
 //                         correlation of x, y, x^2, y^2, xy (valid columns)
 //   ssim_v_kernel         one CTA per (pair, channel, valid row): vertical taps,
@@ -43,15 +44,21 @@ __device__ double block_sum(double v, double *sh)
     return t; // valid in thread 0
 }
 
-__global__ void __launch_bounds__(512) metrics_point_kernel(const float *__restrict__ a, const float *__restrict__ b, int64_t n, double peak,
-                                     double *__restrict__ psnr, double *__restrict__ l1, int *__restrict__ bad)
+constexpr int kPtChunk = 8192; // floats per partial of the point metrics
+inline int pt_chunks(int64_t n) { return (int)((n + kPtChunk - 1) / kPtChunk); }
+
+// (sum (a-b)^2, sum |a-b|) of one chunk of one pair, fixed-order block sums
+__global__ void __launch_bounds__(256) metrics_part_kernel(const float *__restrict__ a, const float *__restrict__ b,
+                                                           int64_t n, int chunks, double2 *__restrict__ part,
+                                                           int *__restrict__ bad)
 {
     __shared__ double sh[32];
-    const int64_t s = blockIdx.x;
+    const int64_t s = blockIdx.y;
+    const int64_t lo = (int64_t)blockIdx.x * kPtChunk, hi = min(n, lo + kPtChunk);
     const float *x = a + s * n, *y = b + s * n;
     double sq = 0.0, ab = 0.0;
     int nf = 0;
-    for (int64_t k = threadIdx.x; k < n; k += blockDim.x)
+    for (int64_t k = lo + threadIdx.x; k < hi; k += blockDim.x)
     {
         const float xv = x[k], yv = y[k];
         if (!isfinite(xv) || !isfinite(yv))
@@ -67,12 +74,29 @@ __global__ void __launch_bounds__(512) metrics_point_kernel(const float *__restr
     {
         if (nf)
             atomicAdd(bad, 1);
-        const double mse = sq / (double)n;
-        if (psnr)
-            psnr[s] = mse <= 0.0 ? 100.0 : fmin(100.0, 10.0 * log10(peak * peak / mse));
-        if (l1)
-            l1[s] = ab / (double)n;
+        part[s * chunks + blockIdx.x] = make_double2(sq, ab);
     }
+}
+
+// per pair: chunk partials in ascending order -> PSNR (clamped at 100 dB) and L1
+__global__ void metrics_final_kernel(const double2 *__restrict__ part, int chunks, int nb, int64_t n, double peak,
+                                     double *__restrict__ psnr, double *__restrict__ l1)
+{
+    const int s = blockIdx.x * blockDim.x + threadIdx.x;
+    if (s >= nb)
+        return;
+    double sq = 0.0, ab = 0.0;
+    for (int c = 0; c < chunks; c++)
+    {
+        const double2 v = part[(int64_t)s * chunks + c];
+        sq += v.x;
+        ab += v.y;
+    }
+    const double mse = sq / (double)n;
+    if (psnr)
+        psnr[s] = mse <= 0.0 ? 100.0 : fmin(100.0, 10.0 * log10(peak * peak / mse));
+    if (l1)
+        l1[s] = ab / (double)n;
 }
 
 // tmp layout: [pair][channel][5 quantities][H][vw]
@@ -236,7 +260,7 @@ __global__ void __launch_bounds__(256) loss_grad_kernel(const double *__restrict
                                                         const float *__restrict__ target, int H, int W,
                                                         double lambda1, float *__restrict__ grad)
 {
-    const int r = blockIdx.x;
+    const int r = blockIdx.x, c = blockIdx.y; // one CTA per (row, channel)
     const int64_t s = blockIdx.z;
     const int vw = W - kWin + 1, vh = H - kWin + 1;
     const double inv_w = 1.0 / ((double)vh * vw);
@@ -244,29 +268,24 @@ __global__ void __launch_bounds__(256) loss_grad_kernel(const double *__restrict
     for (int col = threadIdx.x; col < W; col += blockDim.x)
     {
         const int64_t k = ((s * H) + r) * (int64_t)W + col;
-        float out[2];
-        for (int c = 0; c < 2; c++)
+        double gq[3];
+        for (int q = 0; q < 3; q++)
         {
-            double gq[3];
-            for (int q = 0; q < 3; q++)
+            const double *src = T + ((s * 6 + c * 3 + q) * vh) * (int64_t)W;
+            double v = 0.0;
+            for (int t = kWin - 1; t >= 0; t--) // scatter order: source rows ascending
             {
-                const double *src = T + ((s * 6 + c * 3 + q) * vh) * (int64_t)W;
-                double v = 0.0;
-                for (int t = kWin - 1; t >= 0; t--) // scatter order: source rows ascending
-                {
-                    const int i = r - t;
-                    if (i >= 0 && i < vh)
-                        v = __fma_rn(c_taps[t], src[(int64_t)i * W + col], v);
-                }
-                gq[q] = v;
+                const int i = r - t;
+                if (i >= 0 && i < vh)
+                    v = __fma_rn(c_taps[t], src[(int64_t)i * W + col], v);
             }
-            const double x = (double)pred[2 * k + c], y = (double)target[2 * k + c];
-            const float g_ssim = (float)((gq[0] + gq[1] * y + gq[2] * x) * inv_w); // ssim_channel's T grad
-            const float d = pred[2 * k + c] - target[2 * k + c];
-            const double sgn = d > 0.f ? 1.0 : (d < 0.f ? -1.0 : 0.0);
-            out[c] = (float)(inv * sgn - sw * (double)g_ssim);
+            gq[q] = v;
         }
-        reinterpret_cast<float2 *>(grad)[k] = make_float2(out[0], out[1]);
+        const double x = (double)pred[2 * k + c], y = (double)target[2 * k + c];
+        const float g_ssim = (float)((gq[0] + gq[1] * y + gq[2] * x) * inv_w); // ssim_channel's T grad
+        const float d = pred[2 * k + c] - target[2 * k + c];
+        const double sgn = d > 0.f ? 1.0 : (d < 0.f ? -1.0 : 0.0);
+        grad[2 * k + c] = (float)(inv * sgn - sw * (double)g_ssim);
     }
 }
 
@@ -314,7 +333,8 @@ static void upload_taps()
 size_t metrics_tmp_doubles(const Ctx &c, int nb)
 {
     const int vw = std::max(c.g.W - kWin + 1, 0), vh = std::max(c.g.H - kWin + 1, 0); // no SSIM below 11x11
-    return std::max<size_t>((size_t)nb * 2 * 5 * c.g.H * vw + (size_t)nb * 2 * vh, 1);
+    const int chunks = pt_chunks((int64_t)2 * c.g.H * c.g.W);
+    return std::max<size_t>((size_t)nb * 2 * 5 * c.g.H * vw + (size_t)nb * 2 * vh + (size_t)nb * 2 * chunks, 1);
 }
 
 // d_out* may be null; d_tmp holds metrics_tmp_doubles(c, nb); d_bad counts
@@ -325,8 +345,12 @@ void launch_metrics(Ctx &c, const float *d_pred, const float *d_target, int nb, 
     upload_taps();
     const int H = c.g.H, W = c.g.W, vw = W - kWin + 1, vh = H - kWin + 1;
     const int64_t n = (int64_t)2 * H * W;
-    metrics_point_kernel<<<nb, 512, 0, st>>>(d_pred, d_target, n, peak, d_psnr, d_l1, d_bad);
-    c.launches++;
+    const int chunks = pt_chunks(n);
+    double2 *pt = reinterpret_cast<double2 *>(d_tmp + (size_t)nb * 2 * 5 * H * std::max(vw, 0) +
+                                              (size_t)nb * 2 * std::max(vh, 0));
+    metrics_part_kernel<<<dim3(chunks, nb), 256, 0, st>>>(d_pred, d_target, n, chunks, pt, d_bad);
+    metrics_final_kernel<<<(nb + 127) / 128, 128, 0, st>>>(pt, chunks, nb, n, peak, d_psnr, d_l1);
+    c.launches += 2;
     if (!d_ssim)
         return;
     double *part = d_tmp + (size_t)nb * 2 * 5 * H * vw;
@@ -346,7 +370,9 @@ size_t loss_tmp_doubles(const Ctx &c, int nb)
 {
     const int H = c.g.H, W = c.g.W, vw = std::max(W - kWin + 1, 0), vh = std::max(H - kWin + 1, 0);
     // h-correlations (5 q) | partial sums | F (3 q x windows) | adjoint rows (3 q x vh x W) | l1 per pair
-    return std::max<size_t>((size_t)nb * 2 * (5 * (size_t)H * vw + vh + 3 * (size_t)vh * vw + 3 * (size_t)vh * W) + nb,
+    const int chunks = pt_chunks((int64_t)2 * H * W);
+    return std::max<size_t>((size_t)nb * 2 * (5 * (size_t)H * vw + vh + 3 * (size_t)vh * vw + 3 * (size_t)vh * W) + nb + 1 +
+                                (size_t)nb * 2 * chunks,
                             1);
 }
 
@@ -364,15 +390,18 @@ void launch_hybrid_loss(Ctx &c, const float *d_pred, const float *d_target, int 
     double *T = F + (size_t)nb * 2 * 3 * vh * vw;
     double *l1v = T + (size_t)nb * 2 * 3 * vh * W;
     const int threads = std::min(256, ((std::max(std::max(vw, W), 32) + 31) / 32) * 32);
-    metrics_point_kernel<<<nb, 512, 0, st>>>(d_pred, d_target, n, 1.0, nullptr, l1v, d_bad);
+    const int chunks = pt_chunks(n);
+    double2 *pt = reinterpret_cast<double2 *>(l1v + ((nb + 1) & ~1)); // 16-byte aligned
+    metrics_part_kernel<<<dim3(chunks, nb), 256, 0, st>>>(d_pred, d_target, n, chunks, pt, d_bad);
+    metrics_final_kernel<<<(nb + 127) / 128, 128, 0, st>>>(pt, chunks, nb, n, 1.0, nullptr, l1v);
     ssim_h_kernel<<<dim3(H, 2, nb), threads, 2 * W * sizeof(double), st>>>(d_pred, d_target, H, W, hcor);
     ssim_vgrad_kernel<<<dim3(vh, 2, nb), threads, 0, st>>>(hcor, H, W, part, F);
     loss_final_kernel<<<(nb + 127) / 128, 128, 0, st>>>(part, l1v, nb, vh, vw, lambda1, d_terms);
-    c.launches += 4;
+    c.launches += 5;
     if (d_grad)
     {
         scatter_h_kernel<<<dim3(vh, 6, nb), threads, 0, st>>>(F, H, W, T);
-        loss_grad_kernel<<<dim3(H, 1, nb), threads, 0, st>>>(T, d_pred, d_target, H, W, lambda1, d_grad);
+        loss_grad_kernel<<<dim3(H, 2, nb), threads, 0, st>>>(T, d_pred, d_target, H, W, lambda1, d_grad);
         c.launches += 2;
     }
     check_cuda(cudaGetLastError(), "hybrid loss kernels");

@@ -306,7 +306,8 @@ __global__ void __launch_bounds__(1024) seg_base_kernel(int64_t *__restrict__ se
     if (t == 0)
     {
         int64_t run = 0, mm = 0;
-        for (int i = 0; i < (int)blockDim.x; i++)
+        const int used = min((int)blockDim.x, (nb + per - 1) / max(per, 1)); // threads that hold positions
+        for (int i = 0; i < used; i++)
         {
             const int64_t v = part[i];
             part[i] = run;
@@ -315,6 +316,7 @@ __global__ void __launch_bounds__(1024) seg_base_kernel(int64_t *__restrict__ se
         }
         out[0] = run;
         out[1] = mm;
+        seg[nb] = run; // total (seg[i < nb] are only rewritten below)
     }
     __syncthreads();
     int64_t run = part[t];
@@ -328,8 +330,6 @@ __global__ void __launch_bounds__(1024) seg_base_kernel(int64_t *__restrict__ se
             run += v;
         }
     }
-    if (t == blockDim.x - 1)
-        seg[nb] = run;
 }
 
 void launch_bin_count(Ctx &c, int nb, cudaStream_t st)
