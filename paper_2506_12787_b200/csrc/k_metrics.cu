@@ -3,7 +3,7 @@
 // train::evaluate (training.cpp:380-406). All statistics in double like the
 // reference ("float/double instantiations agree to roundoff", spectrum.cpp:176).
 //
-//   metrics_part_kernel   one CTA per (pair, 8192-float chunk): sum (a-b)^2 and
+//   metrics_part_kernel   one CTA per (pair, 1024-float chunk): sum (a-b)^2 and
 //                         |a-b|; counts non-finite inputs (the reference throws
 //                         domain_error, spectrum.cpp:44-49)
 //   metrics_final_kernel  per pair, the chunk sums in order -> PSNR (clamped at
@@ -44,7 +44,7 @@ __device__ double block_sum(double v, double *sh)
     return t; // valid in thread 0
 }
 
-constexpr int kPtChunk = 8192; // floats per partial of the point metrics
+constexpr int kPtChunk = 1024; // floats per partial of the point metrics
 inline int pt_chunks(int64_t n) { return (int)((n + kPtChunk - 1) / kPtChunk); }
 
 // (sum (a-b)^2, sum |a-b|) of one chunk of one pair, fixed-order block sums

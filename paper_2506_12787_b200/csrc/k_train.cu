@@ -16,8 +16,9 @@
 //                      rows: the trunk's forward (A = [h | x] segments, B = W^T,
 //                      +bias, ReLU), the heads (+bias, written into the residual
 //                      planes) and dIN = dZ W fused with the previous layer's ReLU
-//                      mask (deform.cpp:305-324). 64 x (32 NT) tile, BK 16, FP32.
-//   gemm_dw_kernel     dW = dZ^T [IN | 1] per 512-row chunk (split-K; the appended
+//                      mask (deform.cpp:305-324). (16 RPT) x (32 NT) tile, BK 16, FP32,
+//                      3-stage cp.async ring; RPT picked so the busiest SM has the fewest rows
+//   gemm_dw_kernel     dW = dZ^T [IN | 1] per row chunk (split-K sized for ~2 CTAs/SM; the appended
 //                      ones column gives db), partials summed in ascending chunk
 //                      order by dw_reduce_kernel: deterministic, no atomics
 //   heads_bwd_kernel   dZ7 = (dR Wh) * (h7 > 0) in the reference's branch order
@@ -119,7 +120,8 @@ __global__ void adam_flat_kernel(float *__restrict__ p, const float *__restrict_
 
 // ------------------------------------------------------------- network GEMMs
 
-constexpr int BM = 64, BK = 16, GT = 256;
+constexpr int BK = 16, GT = 256;
+__device__ const float c_one = 1.0f; // the dW kernel's appended ones column
 
 // A(m, k): k < ka from a1 (row stride ld1), else from a2 (row stride ld2) up to kb
 struct ASrc
@@ -128,43 +130,56 @@ struct ASrc
     int ld1, ld2, ka, K;
 };
 
-__device__ __forceinline__ float a_at(const ASrc &a, int m, int k)
+__device__ __forceinline__ const float *a_ptr(const ASrc &a, int m, int k)
 {
-    if (k < a.ka)
-        return a.a1[int64_t(m) * a.ld1 + k];
-    if (k < a.K)
-        return a.a2[int64_t(m) * a.ld2 + (k - a.ka)];
-    return 0.0f;
+    return k < a.ka ? a.a1 + int64_t(m) * a.ld1 + k : a.a2 + int64_t(m) * a.ld2 + (k - a.ka);
 }
+
+// 4-byte cp.async, zero-filled when !pred (src must still be a valid address)
+__device__ __forceinline__ void cp4(float *dst, const float *src, bool pred)
+{
+    const unsigned d = static_cast<unsigned>(__cvta_generic_to_shared(dst));
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;\n" ::"r"(d), "l"(src), "r"(pred ? 4 : 0));
+}
+__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N>
+__device__ __forceinline__ void cp_wait()
+{
+    asm volatile("cp.async.wait_group %0;\n" ::"n"(N));
+}
+
+constexpr int STAGES = 3;
 
 // mode 0: +bias, ReLU -> out[m][j]; 1: * (mask[m][j] > 0) -> out[m][j];
 // 2: +bias -> planes out[j * plane + m]
-template <int NT, bool KCONTIG_B, int MODE>
+// Tile 16 RPT rows x 32 NT columns, k-tiles of 16 through a 3-stage cp.async ring
+// (two tiles in flight while one is consumed); thread = RPT rows x 2 NT columns.
+template <int NT, bool KCONTIG_B, int MODE, int RPT>
 __global__ void __launch_bounds__(GT) gemm_rows_kernel(ASrc a, const float *__restrict__ B, int sbk, int sbn, int M,
                                                        int N, const float *__restrict__ bias,
                                                        const float *__restrict__ mask, int ldm, float *__restrict__ out,
                                                        int64_t ldo)
 {
-    constexpr int BN = 32 * NT, AS = BM + 4, BS = BN + 4;
-    __shared__ __align__(16) float As[BK][AS];
-    __shared__ __align__(16) float Bs[BK][BS];
+    constexpr int BM = 16 * RPT, BN = 32 * NT, AS = BM + 4, BS = BN + 4;
+    __shared__ __align__(16) float As[STAGES][BK][AS];
+    __shared__ __align__(16) float Bs[STAGES][BK][BS];
     const int t = threadIdx.x, tx = t & 15, ty = t >> 4;
     const int m0 = blockIdx.x * BM;
-    float acc[4][2 * NT];
+    float acc[RPT][2 * NT];
 #pragma unroll
-    for (int i = 0; i < 4; i++)
+    for (int i = 0; i < RPT; i++)
 #pragma unroll
         for (int j = 0; j < 2 * NT; j++)
             acc[i][j] = 0.0f;
     constexpr int AL = BM * BK / GT, BL = BK * BN / GT;
-    float ra[AL], rb[BL];
-    auto load = [&](int k0) {
+    auto issue = [&](int k0, int stg) {
 #pragma unroll
         for (int i = 0; i < AL; i++)
         {
             const int e = t + GT * i, mm = e / BK, kk = e % BK;
             const int m = m0 + mm, k = k0 + kk;
-            ra[i] = (m < M && k < a.K) ? a_at(a, m, k) : 0.0f;
+            const bool ok = m < M && k < a.K;
+            cp4(&As[stg][kk][mm], ok ? a_ptr(a, m, k) : a.a1, ok);
         }
 #pragma unroll
         for (int i = 0; i < BL; i++)
@@ -172,43 +187,39 @@ __global__ void __launch_bounds__(GT) gemm_rows_kernel(ASrc a, const float *__re
             const int e = t + GT * i;
             const int kk = KCONTIG_B ? e % BK : e / BN, jj = KCONTIG_B ? e / BK : e % BN;
             const int k = k0 + kk;
-            rb[i] = (k < a.K && jj < N) ? B[int64_t(k) * sbk + int64_t(jj) * sbn] : 0.0f;
+            const bool ok = k < a.K && jj < N;
+            cp4(&Bs[stg][kk][jj], ok ? B + int64_t(k) * sbk + int64_t(jj) * sbn : B, ok);
         }
     };
-    auto store = [&]() {
+    const int nt = (a.K + BK - 1) / BK;
 #pragma unroll
-        for (int i = 0; i < AL; i++)
-        {
-            const int e = t + GT * i;
-            As[e % BK][e / BK] = ra[i];
-        }
-#pragma unroll
-        for (int i = 0; i < BL; i++)
-        {
-            const int e = t + GT * i;
-            const int kk = KCONTIG_B ? e % BK : e / BN, jj = KCONTIG_B ? e / BK : e % BN;
-            Bs[kk][jj] = rb[i];
-        }
-    };
-    load(0);
-    for (int k0 = 0; k0 < a.K; k0 += BK)
+    for (int sidx = 0; sidx < STAGES - 1; sidx++)
     {
-        __syncthreads();
-        store();
-        __syncthreads();
-        if (k0 + BK < a.K)
-            load(k0 + BK);
+        if (sidx < nt)
+            issue(sidx * BK, sidx);
+        cp_commit();
+    }
+    for (int kt = 0; kt < nt; kt++)
+    {
+        cp_wait<STAGES - 2>();
+        __syncthreads(); // tile kt landed for every thread; stage (kt-1) % STAGES is free
+        if (kt + STAGES - 1 < nt)
+            issue((kt + STAGES - 1) * BK, (kt + STAGES - 1) % STAGES);
+        cp_commit();
+        const int stg = kt % STAGES;
 #pragma unroll
         for (int kk = 0; kk < BK; kk++)
         {
-            const float4 av = *reinterpret_cast<const float4 *>(&As[kk][ty * 4]);
-            const float ar[4] = {av.x, av.y, av.z, av.w};
+            float ar[RPT];
+#pragma unroll
+            for (int i = 0; i < RPT; i++)
+                ar[i] = As[stg][kk][ty * RPT + i];
 #pragma unroll
             for (int jj = 0; jj < NT; jj++)
             {
-                const float2 bv = *reinterpret_cast<const float2 *>(&Bs[kk][tx * 2 + 32 * jj]);
+                const float2 bv = *reinterpret_cast<const float2 *>(&Bs[stg][kk][tx * 2 + 32 * jj]);
 #pragma unroll
-                for (int i = 0; i < 4; i++)
+                for (int i = 0; i < RPT; i++)
                 {
                     acc[i][2 * jj] = fmaf(ar[i], bv.x, acc[i][2 * jj]);
                     acc[i][2 * jj + 1] = fmaf(ar[i], bv.y, acc[i][2 * jj + 1]);
@@ -217,9 +228,9 @@ __global__ void __launch_bounds__(GT) gemm_rows_kernel(ASrc a, const float *__re
         }
     }
 #pragma unroll
-    for (int i = 0; i < 4; i++)
+    for (int i = 0; i < RPT; i++)
     {
-        const int m = m0 + ty * 4 + i;
+        const int m = m0 + ty * RPT + i;
         if (m >= M)
             continue;
 #pragma unroll
@@ -244,59 +255,96 @@ __global__ void __launch_bounds__(GT) gemm_rows_kernel(ASrc a, const float *__re
     }
 }
 
-constexpr int DW_T = 64, DW_CHUNK = 512;
+constexpr int DW_C = 64, DW_CHUNK_MIN = 64;
 
-// P[chunk][r][c] = sum_{m in chunk} dZ[m][r] * IN(m, c), IN(m, cols) = 1
+// P[chunk][r][c] = sum_{m in chunk} dZ[m][r] * IN(m, c), IN(m, K) = 1 (db).
+// Tile: all R rows (<= 32 NTR) x 64 columns; thread = 2 NTR rows x 4 columns;
+// k-tiles of 16 chunk rows through the same 3-stage cp.async ring.
+template <int NTR>
 __global__ void __launch_bounds__(GT) gemm_dw_kernel(const float *__restrict__ dz, int ldz, int R, ASrc in, int M,
-                                                     float *__restrict__ part)
+                                                     int chunk, const float *__restrict__ ones, float *__restrict__ part)
 {
-    __shared__ __align__(16) float As[BK][DW_T + 4];
-    __shared__ __align__(16) float Bs[BK][DW_T + 4];
+    constexpr int RT = 32 * NTR;
+    __shared__ __align__(16) float As[STAGES][BK][RT + 4];
+    __shared__ __align__(16) float Bs[STAGES][BK][DW_C + 4];
     const int t = threadIdx.x, tx = t & 15, ty = t >> 4;
-    const int r0 = blockIdx.x * DW_T, c0 = blockIdx.y * DW_T, ch = blockIdx.z;
+    const int c0 = blockIdx.x * DW_C, ch = blockIdx.y;
     const int C = in.K + 1;
-    const int mb = ch * DW_CHUNK, me = min(M, mb + DW_CHUNK);
-    float acc[4][4] = {};
-    for (int k0 = mb; k0 < me; k0 += BK)
-    {
-        __syncthreads();
+    const int mb = ch * chunk, me = min(M, mb + chunk);
+    constexpr int AL = RT * BK / GT, BL = DW_C * BK / GT;
+    float acc[2 * NTR][4];
 #pragma unroll
-        for (int i = 0; i < 4; i++)
+    for (int i = 0; i < 2 * NTR; i++)
+#pragma unroll
+        for (int j = 0; j < 4; j++)
+            acc[i][j] = 0.0f;
+    auto issue = [&](int k0, int stg) {
+#pragma unroll
+        for (int i = 0; i < AL; i++)
         {
-            const int e = t + GT * i, kk = e / DW_T, x = e % DW_T;
+            const int e = t + GT * i, kk = e / RT, x = e % RT;
             const int m = k0 + kk;
-            const int r = r0 + x, c = c0 + x;
-            As[kk][x] = (m < me && r < R) ? dz[int64_t(m) * ldz + r] : 0.0f;
-            Bs[kk][x] = (m < me && c < C) ? (c == in.K ? 1.0f : a_at(in, m, c)) : 0.0f;
+            const bool ok = m < me && x < R;
+            cp4(&As[stg][kk][x], ok ? dz + int64_t(m) * ldz + x : dz, ok);
         }
+#pragma unroll
+        for (int i = 0; i < BL; i++)
+        {
+            const int e = t + GT * i, kk = e / DW_C, x = e % DW_C;
+            const int m = k0 + kk, c = c0 + x;
+            const bool ok = m < me && c < C;
+            cp4(&Bs[stg][kk][x], ok ? (c == in.K ? ones : a_ptr(in, m, c)) : ones, ok);
+        }
+    };
+    const int nt = (me - mb + BK - 1) / BK;
+#pragma unroll
+    for (int sidx = 0; sidx < STAGES - 1; sidx++)
+    {
+        if (sidx < nt)
+            issue(mb + sidx * BK, sidx);
+        cp_commit();
+    }
+    for (int kt = 0; kt < nt; kt++)
+    {
+        cp_wait<STAGES - 2>();
         __syncthreads();
+        if (kt + STAGES - 1 < nt)
+            issue(mb + (kt + STAGES - 1) * BK, (kt + STAGES - 1) % STAGES);
+        cp_commit();
+        const int stg = kt % STAGES;
 #pragma unroll
         for (int kk = 0; kk < BK; kk++)
         {
-            const float4 av = *reinterpret_cast<const float4 *>(&As[kk][ty * 4]);
-            const float4 bv = *reinterpret_cast<const float4 *>(&Bs[kk][tx * 4]);
-            const float ar[4] = {av.x, av.y, av.z, av.w}, br[4] = {bv.x, bv.y, bv.z, bv.w};
+            const float4 bv = *reinterpret_cast<const float4 *>(&Bs[stg][kk][tx * 4]);
+            const float br[4] = {bv.x, bv.y, bv.z, bv.w};
 #pragma unroll
-            for (int i = 0; i < 4; i++)
+            for (int i = 0; i < NTR; i++)
+            {
+                const float2 av = *reinterpret_cast<const float2 *>(&As[stg][kk][ty * 2 + 32 * i]);
 #pragma unroll
                 for (int j = 0; j < 4; j++)
-                    acc[i][j] = fmaf(ar[i], br[j], acc[i][j]);
+                {
+                    acc[2 * i][j] = fmaf(av.x, br[j], acc[2 * i][j]);
+                    acc[2 * i + 1][j] = fmaf(av.y, br[j], acc[2 * i + 1][j]);
+                }
+            }
         }
     }
 #pragma unroll
-    for (int i = 0; i < 4; i++)
-    {
-        const int r = r0 + ty * 4 + i;
-        if (r >= R)
-            continue;
+    for (int i = 0; i < NTR; i++)
 #pragma unroll
-        for (int j = 0; j < 4; j++)
+        for (int h = 0; h < 2; h++)
         {
-            const int c = c0 + tx * 4 + j;
-            if (c < C)
-                part[(int64_t(ch) * R + r) * C + c] = acc[i][j];
+            const int r = ty * 2 + 32 * i + h;
+            if (r >= R)
+                continue;
+            const int c = c0 + tx * 4;
+            float *dst = part + (int64_t(ch) * R + r) * C;
+#pragma unroll
+            for (int j = 0; j < 4; j++)
+                if (c + j < C)
+                    dst[c + j] = acc[2 * i + h][j];
         }
-    }
 }
 
 // dW[r][c] (c < C-1) and db[r] (c == C-1) = sum over chunks in ascending order
@@ -378,6 +426,42 @@ __global__ void log_advance_kernel(const double *__restrict__ terms, double *__r
 
 inline int blocks(int64_t n, int t) { return int((n + t - 1) / t); }
 
+// rows per thread of gemm_rows_kernel: one CTA per SM in flight (128 regs x 256
+// threads), so pick the tile height that minimises the rows of the busiest SM
+inline int pick_rpt(int n)
+{
+    int best = 5, best_rows = 1 << 30;
+    for (int r = 5; r >= 3; r--)
+    {
+        const int ctas = (n + 16 * r - 1) / (16 * r);
+        const int rows = ((ctas + 147) / 148) * 16 * r;
+        if (rows < best_rows)
+        {
+            best_rows = rows;
+            best = r;
+        }
+    }
+    return best;
+}
+
+template <int NT, bool KC, int MODE>
+void launch_rows(int rpt, int n, const ASrc &a, const float *B, int sbk, int sbn, int N, const float *bias,
+                 const float *mask, int ldm, float *out, int64_t ldo, cudaStream_t st)
+{
+    switch (rpt)
+    {
+    case 3:
+        gemm_rows_kernel<NT, KC, MODE, 3><<<blocks(n, 48), GT, 0, st>>>(a, B, sbk, sbn, n, N, bias, mask, ldm, out, ldo);
+        break;
+    case 4:
+        gemm_rows_kernel<NT, KC, MODE, 4><<<blocks(n, 64), GT, 0, st>>>(a, B, sbk, sbn, n, N, bias, mask, ldm, out, ldo);
+        break;
+    default:
+        gemm_rows_kernel<NT, KC, MODE, 5><<<blocks(n, 80), GT, 0, st>>>(a, B, sbk, sbn, n, N, bias, mask, ldm, out, ldo);
+        break;
+    }
+}
+
 } // namespace
 
 void launch_gauss_adam(Ctx &c, const GaussDev &gp, const AdamHp &hp, const TrainSched &sc, bool step_center,
@@ -427,7 +511,7 @@ void launch_dense_fwd(Ctx &c, const float *a1, int ld1, int ka, const float *a2,
     ASrc a{a1, a2, ld1, ld2, ka, K};
     if (width > 160)
         throw std::invalid_argument("training supports deform-net widths up to 160");
-    gemm_rows_kernel<5, true, 0><<<blocks(n, BM), GT, 0, st>>>(a, W, 1, K, n, width, b, nullptr, 0, h, width);
+    launch_rows<5, true, 0>(pick_rpt(n), n, a, W, 1, K, width, b, nullptr, 0, h, width, st);
     c.launches++;
 }
 
@@ -437,7 +521,7 @@ void launch_heads_fwd(Ctx &c, const float *h7, int width, const float *Wh, const
 {
     const int n = c.g.n;
     ASrc a{h7, nullptr, width, 0, width, width};
-    gemm_rows_kernel<1, true, 2><<<blocks(n, BM), GT, 0, st>>>(a, Wh, 1, width, n, 5, bh, nullptr, 0, planes, plane);
+    launch_rows<1, true, 2>(4, n, a, Wh, 1, width, 5, bh, nullptr, 0, planes, plane, st);
     c.launches++;
 }
 
@@ -447,22 +531,39 @@ void launch_dense_bwd_input(Ctx &c, const float *dz, int width, const float *W, 
 {
     const int n = c.g.n;
     ASrc a{dz, nullptr, width, 0, width, width};
-    gemm_rows_kernel<5, false, 1><<<blocks(n, BM), GT, 0, st>>>(a, W, cols, 1, n, width, nullptr, h_prev, width,
-                                                                 dz_prev, width);
+    launch_rows<5, false, 1>(pick_rpt(n), n, a, W, cols, 1, width, nullptr, h_prev, width, dz_prev, width, st);
     c.launches++;
 }
 
-size_t dw_partial_floats(int n, int R, int C) { return size_t((n + DW_CHUNK - 1) / DW_CHUNK) * R * (C + 1); }
+size_t dw_partial_floats(int n, int R, int C) { return size_t((n + DW_CHUNK_MIN - 1) / DW_CHUNK_MIN) * R * (C + 1); }
+
+// rows per split-K chunk: about two CTAs per SM over the whole grid (a multiple
+// of 16 rows, at least DW_CHUNK_MIN)
+static int dw_chunk(int n, int coltiles)
+{
+    const int target = std::max(1, 2 * 148 / coltiles);
+    const int rows = (n + target - 1) / target;
+    return std::max(DW_CHUNK_MIN, (rows + 15) / 16 * 16);
+}
 
 // dW [R][K] = dZ^T [a1 | a2], db [R] = column sums of dZ
 void launch_dense_bwd_weights(Ctx &c, const float *dz, int R, const float *a1, int ld1, int ka, const float *a2,
                               int ld2, int K, float *part, float *dW, float *db, cudaStream_t st)
 {
     const int n = c.g.n;
-    const int chunks = std::max(1, (n + DW_CHUNK - 1) / DW_CHUNK);
+    const int coltiles = blocks(K + 1, DW_C);
+    const int chunk = dw_chunk(n, coltiles);
+    const int chunks = std::max(1, (n + chunk - 1) / chunk);
     ASrc in{a1, a2, ld1, ld2, ka, K};
-    dim3 grid(blocks(R, DW_T), blocks(K + 1, DW_T), chunks);
-    gemm_dw_kernel<<<grid, GT, 0, st>>>(dz, R, R, in, n, part);
+    dim3 grid(coltiles, chunks);
+    const float *one = nullptr;
+    check_cuda(cudaGetSymbolAddress((void **)&one, c_one), "ones symbol");
+    if (R <= 32)
+        gemm_dw_kernel<1><<<grid, GT, 0, st>>>(dz, R, R, in, n, chunk, one, part);
+    else if (R <= 160)
+        gemm_dw_kernel<5><<<grid, GT, 0, st>>>(dz, R, R, in, n, chunk, one, part);
+    else
+        throw std::invalid_argument("training supports deform-net widths up to 160");
     dw_reduce_kernel<<<blocks(int64_t(R) * (K + 1), 256), 256, 0, st>>>(part, chunks, R, K + 1, dW, db);
     c.launches += 2;
 }
