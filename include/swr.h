@@ -256,6 +256,28 @@ int swr_trainer_gradients(swr_trainer *tr, const float *pos01, int32_t sample, d
  * iteration, manifest hash and bbox. */
 int swr_trainer_save(swr_trainer *tr, const char *path);
 
+/* ------------------------------------------------------------ beam scan
+ * The synthetic-data generator's steering step (sim::build_steering_table,
+ * sim::beam_scan, wavesim.cpp:183-252) batched over samples on the GPU, and
+ * generate_dataset's target post-processing (dataset.cpp:86-124). The steering
+ * table [cells][K] is built once per (array, grid). Arrays: square, K <= 64. */
+typedef struct swr_steering swr_steering;
+int swr_steering_create(int32_t k_elements, double spacing, double wavelength, int32_t H, int32_t W, int device,
+                        swr_steering **out);
+void swr_steering_destroy(swr_steering *st);
+/* The table (build_steering_table layout: wr/wi [H*W][K], row-major per cell). */
+int swr_steering_table(swr_steering *st, double *wr, double *wi);
+/* beam_scan for B channels h [B][K][2] (complex double) -> spectra [B][H][W][2]
+ * (complex double), bit-identical to the reference without FP contraction. */
+int swr_beam_scan(swr_steering *st, const double *channel, int64_t B, double *spectra);
+/* Device variant: d_unit = phase-only channels u = h/|h| [B][K][2] already on the
+ * device, d_spectra [B][H][W][2] double, ordered on `stream` (a cudaStream_t;
+ * NULL = the handle's stream). */
+int swr_beam_scan_device(swr_steering *st, const double *d_unit, int64_t B, double *d_spectra, void *stream);
+/* Dataset targets for B valid samples: float(|A| / max|A|) with a zero imaginary
+ * channel, [B][H][W][2] float; *normalization = max|A| (1 when all zero). */
+int swr_beam_scan_targets(swr_steering *st, const double *channel, int64_t B, float *targets, double *normalization);
+
 /* Kernel launches issued by this context since creation (for the bench). */
 int64_t swr_launch_count(swr_ctx *ctx);
 

@@ -427,3 +427,33 @@ def load_dataset(dataset_dir, H, W):
     spec = np.zeros((n, H, W, 2), np.float32)
     L.wref_dataset_load(dataset_dir.encode(), C.byref(h), _f(pos), _f(spec), C.c_longlong(n))
     return h.value, pos, spec
+
+
+def ref_steering_table(H, W, k=16, spacing=0.0625, wavelength=0.125, nofma=False):
+    """build_steering_table through the reference library."""
+    L = C.CDLL(REF_NOFMA_SO if nofma else REF_SO)
+    wr = np.zeros((H * W, k))
+    wi = np.zeros_like(wr)
+    if L.wref_steering_table(k, C.c_double(spacing), C.c_double(wavelength), H, W, _d(wr), _d(wi)) != 0:
+        raise RuntimeError("wref_steering_table failed")
+    return wr, wi
+
+
+def ref_beam_scan(channel, H, W, k=16, spacing=0.0625, wavelength=0.125, nofma=False):
+    """sim::beam_scan(channel, array, grid) -> [H][W][2] float64."""
+    L = C.CDLL(REF_NOFMA_SO if nofma else REF_SO)
+    ch = np.ascontiguousarray(np.asarray(channel, np.complex128).reshape(k))
+    out = np.zeros((H, W, 2))
+    if L.wref_beam_scan(k, C.c_double(spacing), C.c_double(wavelength), H, W, _d(ch.view(np.float64)), _d(out)) != 0:
+        raise RuntimeError("wref_beam_scan failed")
+    return out
+
+
+def ref_sample_channels(count, seed):
+    """The channels generate_dataset scans for make_dataset(dir, H, W, count, seed)."""
+    L = C.CDLL(REF_SO)
+    ch = np.zeros((count, 16), np.complex128)
+    valid = np.zeros(count, np.int32)
+    if L.wref_sample_channels(count, C.c_ulonglong(seed), _d(ch.view(np.float64)), _i(valid)) != 0:
+        raise RuntimeError("wref_sample_channels failed")
+    return ch, valid.astype(bool)

@@ -12,6 +12,7 @@
 
 #include <omp.h>
 
+#include <complex>
 #include <cstring>
 #include <stdexcept>
 #include <string>
@@ -672,6 +673,61 @@ int wref_deform_backward(void *h, const float *pos01, const float *up_c, const f
         {
             std::memcpy(gw[i], L[i]->w.data(), sizeof(float) * L[i]->w.size());
             std::memcpy(gb[i], L[i]->b.data(), sizeof(float) * L[i]->b.size());
+        }
+    });
+}
+
+// build_steering_table (wavesim.cpp:183-211) for the default array geometry
+// overrides; wr/wi [cells][k]
+int wref_steering_table(int k, double spacing, double wavelength, int H, int W, double *wr, double *wi)
+{
+    return guarded([&] {
+        sim::ArrayConfig a;
+        a.k_elements = k;
+        a.spacing = spacing;
+        a.wavelength = wavelength;
+        const auto t = sim::build_steering_table(a, AngularGrid{H, W});
+        std::memcpy(wr, t.wr.data(), sizeof(double) * t.wr.size());
+        std::memcpy(wi, t.wi.data(), sizeof(double) * t.wi.size());
+    });
+}
+
+// beam_scan(channel, array, grid) (wavesim.cpp:213-259); channel [k][2], out [cells][2]
+int wref_beam_scan(int k, double spacing, double wavelength, int H, int W, const double *channel, double *out)
+{
+    return guarded([&] {
+        sim::ArrayConfig a;
+        a.k_elements = k;
+        a.spacing = spacing;
+        a.wavelength = wavelength;
+        std::vector<std::complex<double>> h(static_cast<std::size_t>(k));
+        for (int e = 0; e < k; e++)
+            h[std::size_t(e)] = {channel[2 * e], channel[2 * e + 1]};
+        const auto s = sim::beam_scan(h, a, AngularGrid{H, W});
+        std::memcpy(out, s.data.data(), sizeof(double) * s.data.size());
+    });
+}
+
+// the channels generate_dataset scans for wref_make_dataset's positions
+// (dataset.cpp:61-84: default Scene, sample_positions(scene, count, 0.3,
+// Rng(seed)), trace_paths, channel_response): channels [count][K][2], valid [count]
+int wref_sample_channels(int count, unsigned long long seed, double *channels, int *valid)
+{
+    return guarded([&] {
+        sim::Scene scene;
+        Rng rng(seed);
+        const auto positions = sim::sample_positions(scene, count, 0.3, rng);
+        const int k = scene.array.k_elements;
+        for (int i = 0; i < count; i++)
+        {
+            const auto paths = sim::trace_paths(scene, positions[std::size_t(i)]);
+            valid[i] = paths.empty() ? 0 : 1;
+            const auto h = sim::channel_response(paths, scene.array);
+            for (int e = 0; e < k; e++)
+            {
+                channels[(std::size_t(i) * k + e) * 2] = h[std::size_t(e)].real();
+                channels[(std::size_t(i) * k + e) * 2 + 1] = h[std::size_t(e)].imag();
+            }
         }
     });
 }

@@ -93,6 +93,14 @@ def lib():
         L.swr_trainer_gradients.argtypes = [C.c_void_p, C.c_void_p, C.c_int32, C.c_void_p, C.c_void_p, C.c_void_p,
                                             C.c_void_p]
         L.swr_trainer_save.argtypes = [C.c_void_p, C.c_char_p]
+        L.swr_steering_create.argtypes = [C.c_int32, C.c_double, C.c_double, C.c_int32, C.c_int32, C.c_int,
+                                          C.POINTER(C.c_void_p)]
+        L.swr_steering_destroy.argtypes = [C.c_void_p]
+        L.swr_steering_destroy.restype = None
+        L.swr_steering_table.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p]
+        L.swr_beam_scan.argtypes = [C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p]
+        L.swr_beam_scan_device.argtypes = [C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p, C.c_void_p]
+        L.swr_beam_scan_targets.argtypes = [C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p, C.c_void_p]
         L.swr_scene_set_manifest_hash.argtypes = [C.c_void_p, C.c_uint64]
         L.swr_scene_get_info.argtypes = [C.c_void_p, C.c_void_p]
         L.swr_scene_create_wrfc.argtypes = [C.c_char_p, C.c_int, C.POINTER(C.c_void_p)]
@@ -556,3 +564,52 @@ def train(ds: Dataset, cfg: TrainConfig, resume: str | None = None, device: int 
     tr = Trainer(cfg, ds, resume, device)
     log, _ = tr.run()
     return tr, log
+
+
+# ---------------------------------------------------------------- beam scan
+
+class Steering:
+    """sim::SteeringTable on one B200 (wavesim.cpp:183-211) + batched beam_scan
+    (wavesim.cpp:213-252) and generate_dataset's targets (dataset.cpp:86-124)."""
+
+    def __init__(self, H: int, W: int, k_elements: int = 16, spacing: float = 0.0625, wavelength: float = 0.125,
+                 device: int = 0):
+        h = C.c_void_p()
+        _check(lib().swr_steering_create(int(k_elements), float(spacing), float(wavelength), int(H), int(W), device,
+                                         C.byref(h)))
+        self._h = h
+        self.H, self.W, self.k = H, W, k_elements
+
+    def table(self):
+        wr = np.zeros((self.H * self.W, self.k), np.float64)
+        wi = np.zeros_like(wr)
+        _check(lib().swr_steering_table(self._h, _p(wr), _p(wi)))
+        return wr, wi
+
+    def scan(self, channels) -> np.ndarray:
+        """channels [B][K] complex -> spectra [B][H][W][2] float64."""
+        ch = np.ascontiguousarray(np.asarray(channels, np.complex128).reshape(-1, self.k))
+        B = ch.shape[0]
+        out = np.zeros((B, self.H, self.W, 2), np.float64)
+        _check(lib().swr_beam_scan(self._h, _p(ch.view(np.float64)), B, _p(out)))
+        return out
+
+    def targets(self, channels):
+        """Dataset targets [B][H][W][2] float32 (|A| / max|A|, imaginary 0) and the normalization."""
+        ch = np.ascontiguousarray(np.asarray(channels, np.complex128).reshape(-1, self.k))
+        B = ch.shape[0]
+        out = np.zeros((B, self.H, self.W, 2), np.float32)
+        norm = C.c_double()
+        _check(lib().swr_beam_scan_targets(self._h, _p(ch.view(np.float64)), B, _p(out), C.byref(norm)))
+        return out, norm.value
+
+    def close(self):
+        if getattr(self, "_h", None):
+            lib().swr_steering_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
