@@ -19,6 +19,8 @@
 
 #include "swr.h"
 
+#include <complex>
+#include <algorithm>
 #include <array>
 #include <cmath>
 #include <memory>
@@ -242,5 +244,134 @@ inline std::vector<MetricRow> evaluate(const Checkpoint &ck, const std::vector<s
     return rows;
 }
 } // namespace train
+
+namespace splat
+{
+// splat.hpp:77-89
+struct RenderGrads
+{
+    int n = 0;
+    std::vector<float> center_raw, cholesky, atten_logit, response, d_center, d_response, d_atten;
+};
+
+// splat::rasterize_backward (splat.cpp:494-669) for one position
+inline RenderGrads rasterize_backward(const train::Checkpoint &ck, const Residuals *res, const Spectrum &upstream)
+{
+    const int n = ck.info().n;
+    if (res && res->n != n)
+        throw std::invalid_argument("residual count does not match the primitive count");
+    if (upstream.data.size() != size_t(2) * ck.grid().cells())
+        throw std::invalid_argument("upstream spectrum does not match the grid");
+    RenderGrads g;
+    g.n = n;
+    g.center_raw.assign(size_t(2) * n, 0.f);
+    g.cholesky.assign(size_t(3) * n, 0.f);
+    g.atten_logit.assign(size_t(n), 0.f);
+    g.response.assign(size_t(2) * n, 0.f);
+    g.d_center.assign(size_t(2) * n, 0.f);
+    g.d_response.assign(size_t(2) * n, 0.f);
+    g.d_atten.assign(size_t(n), 0.f);
+    detail::check(swr_rasterize_backward(ck.handle(), res ? res->d_center.data() : nullptr,
+                                         res ? res->d_response.data() : nullptr, res ? res->d_atten.data() : nullptr,
+                                         1, upstream.data.data(), g.center_raw.data(), g.cholesky.data(),
+                                         g.atten_logit.data(), g.response.data(), g.d_center.data(),
+                                         g.d_response.data(), g.d_atten.data()));
+    return g;
+}
+} // namespace splat
+
+namespace train
+{
+// training.hpp:63-68
+struct LossTerms
+{
+    double loss = 0.0, l1_term = 0.0, ssim_term = 0.0;
+};
+
+// train::hybrid_loss (training.cpp:62-106); grad may be null
+inline LossTerms hybrid_loss(const Checkpoint &ck, const Spectrum &prediction, const Spectrum &target, double lambda1,
+                             Spectrum *grad)
+{
+    if (prediction.data.size() != target.data.size() || prediction.data.size() != size_t(2) * ck.grid().cells())
+        throw std::invalid_argument("spectrum shape mismatch");
+    double t[3];
+    if (grad)
+    {
+        grad->grid = prediction.grid;
+        grad->data.assign(prediction.data.size(), 0.f);
+    }
+    detail::check(swr_hybrid_loss(ck.handle(), prediction.data.data(), target.data.data(), 1, lambda1, t,
+                                  grad ? grad->data.data() : nullptr));
+    return {t[0], t[1], t[2]};
+}
+
+// TrainConfig (training.hpp:96-112), the reference defaults
+inline swr_train_config default_config()
+{
+    swr_train_config c;
+    swr_train_config_default(&c);
+    return c;
+}
+
+// train::train (training.cpp:198-376) on one B200: returns the trained model
+// saved to `out_path` (a WRFC the reference loads) and the per-iteration
+// (loss, l1_term, ssim_term) rows of its log
+inline std::vector<std::array<double, 3>> train(const std::string &dataset_dir, const swr_train_config &cfg,
+                                                const std::string &out_path, const char *resume_path = nullptr,
+                                                int device = 0)
+{
+    swr_dataset *ds = nullptr;
+    detail::check(swr_dataset_open(dataset_dir.c_str(), &ds));
+    std::unique_ptr<swr_dataset, void (*)(swr_dataset *)> dsg(ds, &swr_dataset_close);
+    swr_trainer *tr = nullptr;
+    detail::check(swr_trainer_create(&cfg, ds, resume_path, device, &tr));
+    std::unique_ptr<swr_trainer, void (*)(swr_trainer *)> trg(tr, &swr_trainer_destroy);
+    const int64_t todo = std::max<int64_t>(0, cfg.coarse_iters + cfg.fine_iters - swr_trainer_iteration(tr));
+    std::vector<std::array<double, 3>> log(static_cast<size_t>(todo));
+    int64_t done = 0;
+    double ms = 0.0;
+    detail::check(swr_trainer_run(tr, todo, todo ? log[0].data() : nullptr, &done, &ms));
+    log.resize(size_t(done));
+    detail::check(swr_trainer_save(tr, out_path.c_str()));
+    return log;
+}
+} // namespace train
+
+namespace sim
+{
+// wavesim.hpp:32-39
+struct ArrayConfig
+{
+    int k_elements = 16;
+    double spacing = 0.0625;
+    double wavelength = 0.125;
+};
+
+// SteeringTable + beam_scan (wavesim.cpp:183-252) on the device
+class BeamScanner
+{
+  public:
+    BeamScanner(const ArrayConfig &a, const AngularGrid &g, int device = 0) : grid_(g), k_(a.k_elements)
+    {
+        swr_steering *st = nullptr;
+        detail::check(swr_steering_create(a.k_elements, a.spacing, a.wavelength, g.n_elevation, g.n_azimuth, device,
+                                          &st));
+        st_.reset(st);
+    }
+    // channels [B][K] complex -> spectra [B][cells][2] (double)
+    std::vector<double> scan(const std::vector<std::complex<double>> &channels) const
+    {
+        const int64_t B = int64_t(channels.size()) / k_;
+        std::vector<double> out(size_t(B) * 2 * grid_.cells());
+        detail::check(swr_beam_scan(st_.get(), reinterpret_cast<const double *>(channels.data()), B, out.data()));
+        return out;
+    }
+
+  private:
+    AngularGrid grid_;
+    int k_;
+    std::unique_ptr<swr_steering, void (*)(swr_steering *)> st_{nullptr, &swr_steering_destroy};
+};
+} // namespace sim
 
 } // namespace wrfsplat::b200
