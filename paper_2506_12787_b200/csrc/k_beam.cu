@@ -182,14 +182,11 @@ struct swr_steering
     int device = 0, k = 0, H = 0, W = 0;
     cudaStream_t stream = nullptr;
     double *wr = nullptr, *wi = nullptr;
-    std::vector<void *> scratch;
     ~swr_steering()
     {
         cudaSetDevice(device);
         cudaFree(wr);
         cudaFree(wi);
-        for (void *p : scratch)
-            cudaFree(p);
         if (stream)
             cudaStreamDestroy(stream);
     }

@@ -520,8 +520,8 @@ class Trainer:
         return out
 
     def _count(self) -> int:
+        # the Gaussian count: cfg.primitives (a resumed checkpoint must carry the same config)
         if self.n is None:
-            # resume may change n; read it from a params call with only the atten pointer sized by cfg
             self.n = int(self.cfg.primitives)
         return self.n
 
