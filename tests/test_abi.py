@@ -57,3 +57,22 @@ def test_bad_checkpoint_is_runtime_error(tmp_path):
     p.write_bytes(b"WRFX" + b"\0" * 60)
     with pytest.raises(swr.SwrError, match="bad magic|sm_100|device"):
         swr.load_checkpoint(str(p))
+
+
+def test_host_side_validation_needs_no_device(tmp_path):
+    """Argument checks of the newer entry points run before any CUDA call and map
+    to the reference's exception types (invalid_argument -> SWR_EINVAL)."""
+    lib = swr.lib()
+    out = C.c_void_p()
+    # steering: non-square arrays, empty grids (wavesim.cpp:11-19, 185-186)
+    assert lib.swr_steering_create(15, 0.0625, 0.125, 10, 10, 0, C.byref(out)) == 1
+    assert lib.swr_steering_create(16, 0.0625, 0.125, 0, 10, 0, C.byref(out)) == 1
+    assert lib.swr_steering_create(81, 0.0625, 0.125, 10, 10, 0, C.byref(out)) == 1
+    # trainer: null arguments
+    cfg = swr.TrainConfig()
+    assert cfg.width == 156 and cfg.primitives == 10000 and cfg.coarse_iters == 10000
+    assert lib.swr_trainer_create(C.byref(cfg), None, None, 0, C.byref(out)) == 1
+    # dataset: missing directory -> runtime_error (SWR_ERUNTIME)
+    assert lib.swr_dataset_open(str(tmp_path / "nope").encode(), C.byref(out)) == 2
+    with pytest.raises(TypeError):
+        swr.TrainConfig(not_a_field=1)

@@ -184,3 +184,21 @@ def test_saved_checkpoint_renders_like_reference(tiny, tmp_path):
     got = swr.render(ck, pos, pooled=False, aoa=False)["spectra"][0]
     want = ref.render_at(pos[0])
     assert np.abs(got - want).max() <= 1e-5 * max(1.0, np.abs(want).max())
+
+
+def test_run_in_pieces_equals_one_run(tiny):
+    """The host plan (Rng stream, stage switch, Adam step counters), the device
+    cursor and the per-stage graph replays carry across run() calls."""
+    ds = swr.Dataset(tiny)
+    c = cfg(coarse_iters=9, fine_iters=9, anneal_threshold=4)
+    one = swr.Trainer(c, ds)
+    log_one, _ = one.run()
+    parts = swr.Trainer(c, ds)
+    logs = [parts.run(k)[0] for k in (1, 4, 5, 2, 100)]
+    assert parts.iteration == 18
+    np.testing.assert_array_equal(np.concatenate(logs), log_one)
+    a, b = one.params(), parts.params()
+    for k in FIELDS:
+        np.testing.assert_array_equal(a[k], b[k])
+    for wa, wb in zip(a["weights"], b["weights"]):
+        np.testing.assert_array_equal(wa, wb)
