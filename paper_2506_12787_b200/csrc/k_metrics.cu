@@ -8,11 +8,14 @@
 //                         domain_error, spectrum.cpp:44-49)
 //   metrics_final_kernel  per pair, the chunk sums in order -> PSNR (clamped at
 //                         100 dB) and L1
-//   ssim_h_kernel         one CTA per (pair, channel, row): the 11-tap horizontal
-//                         correlation of x, y, x^2, y^2, xy (valid columns)
-//   ssim_v_kernel         one CTA per (pair, channel, valid row): vertical taps,
-//                         the per-window SSIM, a fixed-order block sum
-//   ssim_final_kernel     mean over windows, average of the two channels
+//   ssim_fused_kernel     one CTA per (pair, channel, 32 x 64 block of windows):
+//                         the input block and its 11-tap horizontal correlations
+//                         of x, y, x^2, y^2, xy stay in shared memory, then the
+//                         vertical taps, the per-window SSIM, a fixed-order sum
+//   ssim_fused_final      mean over windows, average of the two channels
+//   ssim_h_kernel         (hybrid loss) one CTA per (pair, channel, row): the
+//                         horizontal correlations into a global buffer the
+//                         gradient's adjoint pass reads back
 // Every reduction has a fixed order, so the results are deterministic.
 #include "swr_internal.h"
 
@@ -137,18 +140,70 @@ __global__ void __launch_bounds__(256) ssim_h_kernel(const float *__restrict__ a
     }
 }
 
-__global__ void __launch_bounds__(256) ssim_v_kernel(const double *__restrict__ tmp, int H, int W, double peak, double *__restrict__ part)
+// Fused SSIM of one (pair, channel, 32-row x 64-column block of windows): the
+// input window block (42 x 74 cells, double) and its horizontal 11-tap
+// correlations (5 quantities x 42 rows x 64 columns) stay in shared memory, so
+// nothing round-trips through HBM. Per value the operation order is the same
+// as the loss path's (horizontal then vertical taps, ascending, fma), so the
+// window statistics are the same doubles; the block's sum is fixed-order.
+constexpr int kFR = 32, kFC = 64;                       // windows per block (rows, columns)
+constexpr int kFIR = kFR + kWin - 1, kFIC = kFC + kWin - 1; // input rows / columns per block
+constexpr size_t kFusedSmem = sizeof(double) * (2 * kFIR * kFIC + 5 * kFIR * kFC + 32);
+
+__global__ void __launch_bounds__(256) ssim_fused_kernel(const float *__restrict__ a, const float *__restrict__ b,
+                                                         int H, int W, double peak, double *__restrict__ part)
 {
-    __shared__ double sh[32];
-    const int i = blockIdx.x, c = blockIdx.y;
-    const int64_t s = blockIdx.z;
+    extern __shared__ double fsm[];
+    double *xin = fsm, *yin = fsm + kFIR * kFIC; // [kFIR][kFIC]
+    double *hq = yin + kFIR * kFIC;              // [5][kFIR][kFC]
+    double *sh = hq + 5 * kFIR * kFC;            // [32]
+    const int ct = blockIdx.x, rt = blockIdx.y;
+    const int64_t sc = blockIdx.z; // pair * 2 + channel
+    const int64_t s = sc >> 1;
+    const int c = int(sc & 1);
     const int vw = W - kWin + 1, vh = H - kWin + 1;
-    const int64_t qs = (int64_t)H * vw;
-    const double *in = tmp + ((s * 2 + c) * 5) * qs;
+    const int i0 = rt * kFR, j0 = ct * kFC;
+    const float *x = a + s * int64_t(H) * W * 2, *y = b + s * int64_t(H) * W * 2;
+    for (int e = threadIdx.x; e < kFIR * kFIC; e += blockDim.x)
+    {
+        const int r = e / kFIC, cc = e % kFIC;
+        const int gi = i0 + r, gj = j0 + cc;
+        const bool ok = gi < H && gj < W;
+        xin[e] = ok ? (double)x[(int64_t(gi) * W + gj) * 2 + c] : 0.0;
+        yin[e] = ok ? (double)y[(int64_t(gi) * W + gj) * 2 + c] : 0.0;
+    }
+    __syncthreads();
+    // horizontal correlations (ssim_h_kernel's order)
+    for (int e = threadIdx.x; e < kFIR * kFC; e += blockDim.x)
+    {
+        const int r = e / kFC, jj = e % kFC;
+        const double *xr = xin + r * kFIC + jj, *yr = yin + r * kFIC + jj;
+        double mx = 0.0, my = 0.0, mxx = 0.0, myy = 0.0, mxy = 0.0;
+#pragma unroll
+        for (int t = 0; t < kWin; t++)
+        {
+            const double g = c_taps[t], xv = xr[t], yv = yr[t];
+            mx = __fma_rn(g, xv, mx);
+            my = __fma_rn(g, yv, my);
+            mxx = __fma_rn(g, xv * xv, mxx);
+            myy = __fma_rn(g, yv * yv, myy);
+            mxy = __fma_rn(g, xv * yv, mxy);
+        }
+        hq[0 * kFIR * kFC + e] = mx;
+        hq[1 * kFIR * kFC + e] = my;
+        hq[2 * kFIR * kFC + e] = mxx;
+        hq[3 * kFIR * kFC + e] = myy;
+        hq[4 * kFIR * kFC + e] = mxy;
+    }
+    __syncthreads();
+    // vertical taps + per-window SSIM
     const double c1 = (0.01 * peak) * (0.01 * peak), c2 = (0.03 * peak) * (0.03 * peak);
     double acc = 0.0;
-    for (int j = threadIdx.x; j < vw; j += blockDim.x)
+    for (int e = threadIdx.x; e < kFR * kFC; e += blockDim.x)
     {
+        const int ii = e / kFC, jj = e % kFC;
+        if (i0 + ii >= vh || j0 + jj >= vw)
+            continue;
         double m[5];
 #pragma unroll
         for (int q = 0; q < 5; q++)
@@ -156,7 +211,7 @@ __global__ void __launch_bounds__(256) ssim_v_kernel(const double *__restrict__ 
             double v = 0.0;
 #pragma unroll
             for (int t = 0; t < kWin; t++)
-                v = __fma_rn(c_taps[t], in[q * qs + (int64_t)(i + t) * vw + j], v);
+                v = __fma_rn(c_taps[t], hq[q * kFIR * kFC + (ii + t) * kFC + jj], v);
             m[q] = v;
         }
         const double ux = m[0], uy = m[1];
@@ -167,10 +222,12 @@ __global__ void __launch_bounds__(256) ssim_v_kernel(const double *__restrict__ 
     }
     acc = block_sum(acc, sh);
     if (threadIdx.x == 0)
-        part[(s * 2 + c) * vh + i] = acc;
+        part[(sc * gridDim.y + rt) * gridDim.x + ct] = acc;
 }
 
-__global__ void ssim_final_kernel(const double *__restrict__ part, int nb, int vh, int vw, double *__restrict__ ssim)
+// per pair: the blocks' sums in (channel, row block, column block) order -> mean SSIM
+__global__ void ssim_fused_final_kernel(const double *__restrict__ part, int nb, int blocks, int64_t windows,
+                                        double *__restrict__ ssim)
 {
     const int s = blockIdx.x * blockDim.x + threadIdx.x;
     if (s >= nb)
@@ -179,12 +236,13 @@ __global__ void ssim_final_kernel(const double *__restrict__ part, int nb, int v
     for (int c = 0; c < 2; c++)
     {
         double t = 0.0;
-        for (int i = 0; i < vh; i++)
-            t += part[((int64_t)s * 2 + c) * vh + i];
-        ch[c] = t / ((double)vh * vw);
+        for (int k = 0; k < blocks; k++)
+            t += part[((int64_t)s * 2 + c) * blocks + k];
+        ch[c] = t / (double)windows;
     }
     ssim[s] = 0.5 * (ch[0] + ch[1]);
 }
+
 
 // ------------------------------------------------- hybrid loss + gradient
 // training.cpp:62-106: loss = lambda1 * L1 + (1 - lambda1) * (1 - SSIM), and its
@@ -334,7 +392,8 @@ size_t metrics_tmp_doubles(const Ctx &c, int nb)
 {
     const int vw = std::max(c.g.W - kWin + 1, 0), vh = std::max(c.g.H - kWin + 1, 0); // no SSIM below 11x11
     const int chunks = pt_chunks((int64_t)2 * c.g.H * c.g.W);
-    return std::max<size_t>((size_t)nb * 2 * 5 * c.g.H * vw + (size_t)nb * 2 * vh + (size_t)nb * 2 * chunks, 1);
+    const size_t blocks = (size_t)((vw + kFC - 1) / kFC) * ((vh + kFR - 1) / kFR);
+    return std::max<size_t>((size_t)nb * 2 * blocks + (size_t)nb * 2 * chunks, 1);
 }
 
 // d_out* may be null; d_tmp holds metrics_tmp_doubles(c, nb); d_bad counts
@@ -346,19 +405,25 @@ void launch_metrics(Ctx &c, const float *d_pred, const float *d_target, int nb, 
     const int H = c.g.H, W = c.g.W, vw = W - kWin + 1, vh = H - kWin + 1;
     const int64_t n = (int64_t)2 * H * W;
     const int chunks = pt_chunks(n);
-    double2 *pt = reinterpret_cast<double2 *>(d_tmp + (size_t)nb * 2 * 5 * H * std::max(vw, 0) +
-                                              (size_t)nb * 2 * std::max(vh, 0));
+    const int cbt = (std::max(vw, 0) + kFC - 1) / kFC, rbt = (std::max(vh, 0) + kFR - 1) / kFR;
+    double *part = d_tmp;                                                       // [nb][2][rbt * cbt]
+    double2 *pt = reinterpret_cast<double2 *>(d_tmp + (size_t)nb * 2 * cbt * rbt); // [nb][chunks]
     metrics_part_kernel<<<dim3(chunks, nb), 256, 0, st>>>(d_pred, d_target, n, chunks, pt, d_bad);
     metrics_final_kernel<<<(nb + 127) / 128, 128, 0, st>>>(pt, chunks, nb, n, peak, d_psnr, d_l1);
     c.launches += 2;
     if (!d_ssim)
         return;
-    double *part = d_tmp + (size_t)nb * 2 * 5 * H * vw;
-    const int threads = std::min(256, ((std::max(vw, 32) + 31) / 32) * 32);
-    ssim_h_kernel<<<dim3(H, 2, nb), threads, 2 * W * sizeof(double), st>>>(d_pred, d_target, H, W, d_tmp);
-    ssim_v_kernel<<<dim3(vh, 2, nb), threads, 0, st>>>(d_tmp, H, W, peak, part);
-    ssim_final_kernel<<<(nb + 127) / 128, 128, 0, st>>>(part, nb, vh, vw, d_ssim);
-    c.launches += 3;
+    static bool configured = false;
+    if (!configured)
+    {
+        check_cuda(cudaFuncSetAttribute(ssim_fused_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        (int)kFusedSmem),
+                   "ssim smem attribute");
+        configured = true;
+    }
+    ssim_fused_kernel<<<dim3(cbt, rbt, 2 * nb), 256, kFusedSmem, st>>>(d_pred, d_target, H, W, peak, part);
+    ssim_fused_final_kernel<<<(nb + 127) / 128, 128, 0, st>>>(part, nb, cbt * rbt, (int64_t)vh * vw, d_ssim);
+    c.launches += 2;
     check_cuda(cudaGetLastError(), "metrics kernels");
 }
 
