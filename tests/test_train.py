@@ -202,3 +202,24 @@ def test_run_in_pieces_equals_one_run(tiny):
         np.testing.assert_array_equal(a[k], b[k])
     for wa, wb in zip(a["weights"], b["weights"]):
         np.testing.assert_array_equal(wa, wb)
+
+
+@pytest.mark.parametrize("cutoff,tile", [(0.0, 16), (3.0, 32), (1.5, 8)])
+def test_raster_params_gradients_match_reference(full, tmp_path, cutoff, tile):
+    """Cutoff off (every primitive covers every tile: the worst-case pair buffer),
+    wide tiles (the one-record-per-warp raster) and narrow tiles."""
+    c = cfg(primitives=400, coarse_iters=2, fine_iters=2, anneal_threshold=100, cutoff_radius=cutoff, tile=tile)
+    ds = swr.Dataset(full)
+    tr = swr.Trainer(c, ds)
+    log, _ = tr.run()
+    assert np.all(np.isfinite(log))
+    path = str(tmp_path / "p.wrfc")
+    tr.save(path)
+    ref = O.Reference(path=path)
+    _, spec = ds.read([2])
+    for p in (None, np.array([0.4, 0.5, 0.6], np.float32)):
+        got = tr.gradients(2, p)
+        want = ref.gradients(spec[0], c.lambda1, p)
+        assert np.abs(got["terms"] - want["terms"]).max() <= 1e-6 * abs(want["terms"][0]) + 1e-9
+        for k, _ in swr.GRAD_FIELDS:
+            _close(got[k], want[k], 1e-5, k)
