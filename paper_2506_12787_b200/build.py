@@ -43,7 +43,7 @@ def _sources():
 
 def _digest(path: str, flags) -> str:
     h = hashlib.sha1(" ".join(flags).encode())
-    for f in [path] + sorted(glob.glob(os.path.join(CSRC, "*.h")) + glob.glob(os.path.join(ROOT, "include", "*.h"))):
+    for f in [path] + sorted(glob.glob(os.path.join(CSRC, "*.h")) + glob.glob(os.path.join(CSRC, "*.cuh")) + glob.glob(os.path.join(ROOT, "include", "*.h"))):
         with open(f, "rb") as fh:
             h.update(fh.read())
     return h.hexdigest()[:16]

@@ -304,7 +304,7 @@ void build_scene(Ctx &c, const HostScene &hs, int device)
     check_cuda(cudaStreamSynchronize(c.stream), "centre terms");
     dfree(c, d_cenc);
     if (mlp_tc_available() && WP == 160)
-        prepare_tc_weights(c, whT, wcen, heads, cenc);
+        prepare_tc_weights(c, whT, heads);
 }
 
 // ------------------------------------------------------------- work buffers

@@ -7,8 +7,14 @@
 // TX position s (39 values) (deform.cpp:54-70, 158-171). Trunk layers 0, 2, 4, 6
 // read x (layer 0 alone, 2/4/6 after the hidden state, deform.cpp:41,177-192).
 // Here W x is split into W_c xc[g] + (W_p xp[s] + b):
-//   * W_c xc[g] runs on the tensor cores as 3 extra UMMA K steps (K = 48) whose A
-//     operand is the tile's xc rows in shared memory;
+//   * W_c xc[g] depends on the Gaussian only: it is computed once per scene in
+//     FP32 (center_terms_kernel, k_mlp.cu) and stored per 32-Gaussian block in
+//     the tcgen05.cp source layout ("cterm"). Each layer 0/2/4/6 accumulator
+//     STARTS from it: the issuer copies the block into TMEM with
+//     tcgen05.cp.32x128b.warpx4 (one 32-row copy broadcast to the 4 lane
+//     quarters = the 4 positions of the CTA), and the layer's UMMAs accumulate on
+//     top (cp and mma from one thread execute in issue order). Layer 0 thus needs
+//     no UMMA at all, and layers 2/4/6 only their 10 hidden K steps;
 //   * W_p xp[s] + b ("pterm", computed per position by pos_prep_kernel) is added in
 //     the epilogue; a CTA's 128 rows are 32 Gaussians x 4 positions with the TMEM
 //     lane quarter = the position, so this addend is warp-uniform.
@@ -72,27 +78,37 @@ constexpr int PAIR_S = 2 * TS;          // positions per pair tile
 constexpr int WPC = 160;                // padded width (N and K of the hidden layers)
 constexpr int KSTEPS = WPC / 16;        // 10 UMMA K steps per hidden layer
 constexpr int NPART = 2;
-constexpr int KC = 3;                   // K steps of the xc (centre encoding) products: K = 48
-constexpr int XCK = 16 * KC;            // 48
-constexpr int NL = 8;                   // trunk MMA layers per tile: 0 (xc only), 1..7; then the heads
+constexpr int NL = 8;                   // trunk layers per tile: 0 (cterm copy only), 1..7; then the heads
 constexpr int NHEAD_N = 32;             // heads UMMA N (5 real columns)
 // output part p: N = npart(p) columns from pcol(p) (N multiple of 32 for cta_group::2
-// with A in TMEM); feeds the next layer's K steps pcol/16 ..
+// with A in TMEM); feeds the next layer's K steps pcol/16 .. Each part's conversion
+// (epilogue) overlaps the UMMAs of the later part and of the next layer's K steps
+// that do not read it. Finer parts (64/32/32/32 was tried) spread the epilogue's
+// issue pressure over the whole layer, and the single-thread UMMA issuer, which
+// shares its SM sub-partition with 6 epilogue warps, then falls behind the tensor
+// pipe (tools/umma_parts_bench.cu: the pipe alone runs every split at N/2 clk per
+// UMMA; with busy neighbour warps the issue rate collapses): 96/64 measured best.
 __host__ __device__ constexpr int npart(int p) { return p == 0 ? 96 : 64; }
 __host__ __device__ constexpr int pcol(int p) { return p == 0 ? 0 : 96; }
-constexpr int KSPLIT = 6; // K steps fed by part 0
-__host__ __device__ constexpr int part_of_chunk(int c) { return c < KSPLIT ? 0 : 1; }
+__host__ __device__ constexpr int part_of_chunk(int c) { return c < 6 ? 0 : 1; }
 // one operand (hi or lo), one K step, this CTA's half of N output columns
 __host__ __device__ constexpr int kstep_bytes_n(int n) { return n / 2 * 16 * 2; }
 __host__ __device__ constexpr int kstep_bytes(int p) { return kstep_bytes_n(npart(p)); }
-constexpr int SLOT = (KC + KSTEPS) * 2 * kstep_bytes(0); // largest stage: 13 K steps x (hi, lo) = 39 KB
-constexpr int NSTAGE = 3;
-constexpr int XC_OP = TM * XCK * 2;     // one xc A operand (hi or lo) of a CTA tile: 12 KB
-constexpr int XC_BLOCK = TG * XCK * 2;  // per 32-Gaussian block, one operand: 3 KB
-constexpr int A_LBO = (TM / 8) * 128;   // xc A tile: K-direction core-matrix stride (2 KB)
-constexpr int A_SBO = 128;
+// cterm segment of output part p: npart(p) / 4 groups of [32 rows][4 f32] (one
+// tcgen05.cp.32x128b each), full N (both CTAs of a pair hold the same Gaussians)
+__host__ __device__ constexpr int cseg_bytes(int p) { return npart(p) * TG * 4; }
+// cterm block layout: [160 / 4 column groups][32 rows][4] f32, so part p's segment
+// starts at byte pcol(p) * TG * 4
+__host__ __device__ constexpr int cseg_off(int p) { return pcol(p) * TG * 4; }
+constexpr int C_BLOCK = WPC * TG * 4;   // one layer's cterm of a 32-Gaussian block: 20 KB
+constexpr int W_MAX = KSTEPS * 2 * kstep_bytes(0); // largest weight stage: 10 K steps x (hi, lo) = 30 KB
+constexpr int SLOT = W_MAX + cseg_bytes(0);        // + the cterm segment at W_MAX: 42 KB
+#ifndef SWR_TC_NSTAGE
+#define SWR_TC_NSTAGE 3
+#endif
+constexpr int NSTAGE = SWR_TC_NSTAGE;
 #ifndef SWR_TC_GROUPS
-#define SWR_TC_GROUPS 5
+#define SWR_TC_GROUPS 6
 #endif
 constexpr int NGRP = SWR_TC_GROUPS;     // epilogue column groups (5 or 6)
 constexpr int EPI_WARPS = 4 * NGRP;     // column groups x 4 TMEM lane quarters
@@ -105,26 +121,36 @@ constexpr int HEAD_COL = NREG * WPC;    // heads accumulator: TMEM columns 480-5
 constexpr int kProducerWarp = EPI_WARPS, kMmaWarp = EPI_WARPS + 1;
 constexpr int PROW = 4 * WPC;           // pterm row of one position (4 layers)
 constexpr int SMEM_RING = NSTAGE * SLOT;
-constexpr int SMEM_XC = 2 * 2 * XC_OP;  // double-buffered (tile parity) hi + lo
 constexpr int SMEM_P = 2 * TS * PROW * 4;
 constexpr int SMEM_CONST = (8 * WPC + 8) * 4;
 // w_full[NSTAGE], w_empty[NSTAGE], a_ready[2 sets][2 parts], acc[2 sets][2 parts],
-// acc_h, xc_ready[2 buffers]
-constexpr int NBARS = 2 * NSTAGE + 4 + 4 + 1 + 2;
-constexpr int SMEM_BYTES = SMEM_RING + SMEM_XC + SMEM_P + SMEM_CONST + NBARS * 8 + 16 + 1024;
+// acc_h
+constexpr int NBARS = 2 * NSTAGE + 2 * NPART + 2 * NPART + 1;
+constexpr int SMEM_BYTES = SMEM_RING + SMEM_P + SMEM_CONST + NBARS * 8 + 16 + 1024;
 static_assert(SMEM_BYTES <= 227 * 1024, "shared memory budget");
-// epilogue column group g converts 16-column chunks g and g + NGRP. With 6 groups
-// part 0 (chunks 0-5) is one chunk per warp (24 warps) and part 1 (chunks 6-9) is
-// converted by groups 0-3; with 5 groups group 0 takes chunks 0 and 5.
-__host__ __device__ constexpr int part_warps(int p) { return p == 0 ? 4 * NGRP : 16; }
+static_assert(NPART == 2 && pcol(NPART - 1) + npart(NPART - 1) == WPC, "output parts cover the width");
+// epilogue column group g converts 16-column chunks g and g + NGRP (if < 10), in
+// that order (= part order). With 6 groups: part 0 (chunks 0-5) one chunk per
+// group, part 1 (chunks 6-9) by groups 0-3. part_warps(p): warps (x 4 lane quarters) that report part p, one
+// arrival per warp and part.
+__host__ __device__ constexpr int part_warps(int p)
+{
+    int w = 0;
+    for (int g = 0; g < NGRP; g++)
+        w += (part_of_chunk(g) == p || (g + NGRP < KSTEPS && part_of_chunk(g + NGRP) == p)) ? 4 : 0;
+    return w;
+}
 
+// layers whose input includes the centre encoding (deform.cpp:41: layer 0 and the
+// skip layers 2, 4, 6): their accumulator starts from the cterm
 __host__ __device__ constexpr bool has_xc(int l) { return l == 0 || l == 2 || l == 4 || l == 6; }
-// weight stream per tile: one stage per (trunk layer, part): the xc K steps
-// (layers 0,2,4,6) then the 10 hidden K steps (layers 1..7), each K step hi then
-// lo, rank 0's half of the part's columns then rank 1's; finally the heads stage
+// weight stream per tile: one stage per (trunk layer, part): the 10 hidden K steps
+// (layers 1..7; layer 0 has none), each K step hi then lo, rank 0's half of the
+// part's columns then rank 1's; finally the heads stage. A stage of a layer with
+// a cterm also receives the tile's cterm segment (at W_MAX, both CTAs in full).
 __host__ __device__ constexpr int stage_bytes(int l, int p)
 {
-    return ((has_xc(l) ? KC : 0) + (l >= 1 ? KSTEPS : 0)) * 2 * kstep_bytes(p);
+    return (l >= 1 ? KSTEPS : 0) * 2 * kstep_bytes(p);
 }
 constexpr int HEAD_STAGE = KSTEPS * 2 * (NHEAD_N / 2) * 16 * 2; // 10 KB per CTA
 // byte offset of stage (l, p) (l = NL: the heads) in the packed stream, both ranks
@@ -139,7 +165,7 @@ __host__ __device__ constexpr size_t stream_offset(int l, int p)
 struct TcArgs
 {
     const uint16_t *w_tc;  // packed weights in consumption order (prepare_tc_weights)
-    const uint16_t *xc;    // [n/32 blocks][hi | lo][48 x 32] bf16, UMMA core-matrix layout
+    const float *cterm;    // [n/32 blocks][4 layers][part 0 | part 1][npart/4][32 rows][4] f32 (W_c xc, no bias)
     const float *bias;     // [8][160]
     const float *pterm;    // [nb][4][160] position term of layers 0,2,4,6 (bias included)
     const float *hbias;    // [5]
@@ -191,23 +217,12 @@ __device__ __forceinline__ void tile_origin(const TcArgs &a, int tile, uint32_t 
     s0 = (tile % a.n_sblk) * PAIR_S + (int)rank * TS;
 }
 
-// cp.async the CTA's tile operands: the xc A tile (4 copies of the 32-Gaussian
-// block, one per position row group) and the 4 pterm rows (zero-filled outside
-// the problem); issued by all epilogue threads
-__device__ __forceinline__ void prefetch_tile(const TcArgs &a, int tile, uint32_t rank, uint8_t *xc_buf, float *p_buf,
-                                              int et)
+// cp.async the CTA's 4 pterm rows (zero-filled outside the problem); issued by
+// all epilogue threads
+__device__ __forceinline__ void prefetch_tile(const TcArgs &a, int tile, uint32_t rank, float *p_buf, int et)
 {
     int g0, s0;
     tile_origin(a, tile, rank, g0, s0);
-    const uint8_t *blk = reinterpret_cast<const uint8_t *>(a.xc) + (size_t)(g0 / TG) * 2 * XC_BLOCK;
-    // per operand (hi, lo) and 8-element K group kc: 512 B of the block -> 4 copies
-    for (int i = et; i < 2 * (XCK / 8) * 4 * 32; i += EPI_THREADS)
-    {
-        const int piece = i & 31, copy = (i >> 5) & 3, kc = (i >> 7) % (XCK / 8), op = (i >> 7) / (XCK / 8);
-        const uint8_t *src = blk + op * XC_BLOCK + kc * 512 + piece * 16;
-        uint8_t *dst = xc_buf + op * XC_OP + kc * A_LBO + copy * 512 + piece * 16;
-        tc::cp_async16(dst, src, true);
-    }
     for (int i = et; i < TS * PROW / 4; i += EPI_THREADS)
     {
         const int sl = i / (PROW / 4), k = (i % (PROW / 4)) * 4;
@@ -225,26 +240,17 @@ __device__ __forceinline__ void stamp(const TcArgs &a, int it, int l, int slot)
 }
 
 // UMMA issue (one elected thread), descriptors compile-time offsets from one base.
-// xc products of output part P: A = the tile's xc rows in shared memory, K = 48
-template <int N, bool SPLIT>
-__device__ __forceinline__ void issue_xc(uint32_t d, uint32_t b, uint32_t xhi, uint32_t xlo)
+// cterm of an N-column output part: N / 4 copies of [32 rows][4 f32] from the
+// stage's cterm segment into the accumulator columns, each broadcast to the 4
+// TMEM lane quarters (the 4 positions); both CTAs copy from their own segment
+template <int N>
+__device__ __forceinline__ void issue_cterm(uint32_t d, uint32_t cseg)
 {
-    constexpr uint32_t KB = kstep_bytes_n(N), LBO = N / 2 / 8 * 128;
-    constexpr uint32_t IDESC = tc::make_idesc(1, 2 * TM, N);
-    constexpr uint32_t DH = tc::desc_hi(128), AH = tc::desc_hi(A_SBO);
-    const uint32_t b0 = tc::desc_lo(b, LBO), ah0 = tc::desc_lo(xhi, A_LBO), al0 = tc::desc_lo(xlo, A_LBO);
+    constexpr uint32_t DH = tc::desc_hi(128); // 8-row groups of 16 B rows: 128 B apart (contiguous)
+    const uint32_t c0 = tc::desc_lo(cseg, 16);
 #pragma unroll
-    for (int kk = 0; kk < KC; kk++)
-    {
-        const uint64_t dbh = tc::desc_of(b0 + (kk * 2 * KB >> 4), DH);
-        const uint64_t dah = tc::desc_of(ah0 + (2 * kk * A_LBO >> 4), AH);
-        tc::mma2_f16(d, dah, dbh, IDESC, kk > 0 ? 1u : 0u);
-        if (SPLIT)
-        {
-            tc::mma2_f16(d, tc::desc_of(al0 + (2 * kk * A_LBO >> 4), AH), dbh, IDESC, 1u);
-            tc::mma2_f16(d, dah, tc::desc_of(b0 + ((kk * 2 + 1) * KB >> 4), DH), IDESC, 1u);
-        }
-    }
+    for (int g = 0; g < N / 4; g++)
+        tc::cp2_32x128b_x4(d + 4 * g, tc::desc_of(c0 + (g * TG * 16 >> 4), DH));
 }
 // hidden K steps [K0, K0 + NK) of an N-column output: A = previous layer's
 // converted output in TMEM
@@ -269,47 +275,46 @@ __device__ __forceinline__ void issue_hidden(uint32_t d, uint32_t bh, uint32_t a
         }
     }
 }
+// hidden K steps fed by input part J (= the previous layer's output part J),
+// after waiting for its conversion (WAITS)
+template <int N, int J, bool WAITS, bool SPLIT>
+__device__ __forceinline__ void mma_from_part(uint32_t d, uint32_t bh, uint32_t areg, bool first, uint64_t *ready,
+                                              uint32_t ready_ph)
+{
+    if (WAITS)
+    {
+        MBAR_WAIT_CL(&ready[J], (ready_ph >> J) & 1, 101 + J);
+        tc::tc_fence_after();
+    }
+    if (tc::elect_one())
+        issue_hidden<N, pcol(J) / 16, npart(J) / 16, SPLIT>(d, bh, areg, J == 0 && first);
+    __syncwarp();
+    if constexpr (J + 1 < NPART)
+        mma_from_part<N, J + 1, WAITS, SPLIT>(d, bh, areg, first, ready, ready_ph);
+}
 // the 10 hidden K steps of one output (whole warp); WAITS: wait for each converted
 // part of the previous layer before the K steps that read it
 template <int N, bool WAITS, bool SPLIT>
 __device__ __forceinline__ void mma_hidden(uint32_t d, uint32_t bh, uint32_t areg, bool first, uint64_t *ready,
                                            uint32_t ready_ph)
 {
-    if (WAITS)
-    {
-        MBAR_WAIT_CL(&ready[0], ready_ph & 1, 101);
-        tc::tc_fence_after();
-        if (tc::elect_one())
-            issue_hidden<N, 0, KSPLIT, SPLIT>(d, bh, areg, first);
-        __syncwarp();
-        MBAR_WAIT_CL(&ready[1], (ready_ph >> 1) & 1, 102);
-        tc::tc_fence_after();
-        if (tc::elect_one())
-            issue_hidden<N, KSPLIT, KSTEPS - KSPLIT, SPLIT>(d, bh, areg, false);
-        __syncwarp();
-    }
-    else
-    {
-        if (tc::elect_one())
-            issue_hidden<N, 0, KSTEPS, SPLIT>(d, bh, areg, first);
-        __syncwarp();
-    }
+    mma_from_part<N, 0, WAITS, SPLIT>(d, bh, areg, first, ready, ready_ph);
 }
-// all UMMAs of output part P of trunk layer l from one weight stage at b
+// output part P of trunk layer l from one stage at b: the cterm copy (layers
+// 0/2/4/6), then the hidden UMMAs (layers 1..7) accumulating on top of it
 template <int P, bool SPLIT>
-__device__ __forceinline__ void mma_part(int l, uint32_t d, uint32_t areg, uint32_t b, uint32_t xhi, uint32_t xlo,
-                                         uint64_t *ready, uint32_t ready_ph)
+__device__ __forceinline__ void mma_part(int l, uint32_t d, uint32_t areg, uint32_t b, uint64_t *ready,
+                                         uint32_t ready_ph)
 {
-    constexpr uint32_t KB = kstep_bytes(P);
     const bool xc = has_xc(l);
     if (xc)
     {
         if (tc::elect_one())
-            issue_xc<npart(P), SPLIT>(d, b, xhi, xlo);
+            issue_cterm<npart(P)>(d, b + W_MAX);
         __syncwarp();
     }
     if (l >= 1)
-        mma_hidden<npart(P), P == 0, SPLIT>(d, b + (xc ? KC * 2 * KB : 0), areg, !xc, ready, ready_ph);
+        mma_hidden<npart(P), P == 0, SPLIT>(d, b, areg, !xc, ready, ready_ph);
 }
 
 template <bool SPLIT>
@@ -319,8 +324,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1) mlp_tc_k
     // identical offsets in both CTAs (UMMA descriptors of the pair address both)
     uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     uint8_t *ring = smem;
-    uint8_t *xcbuf = ring + SMEM_RING;                                 // [2][hi | lo]
-    float *pbuf = reinterpret_cast<float *>(xcbuf + SMEM_XC);          // [2][4][4][160]
+    float *pbuf = reinterpret_cast<float *>(ring + SMEM_RING);         // [2][4][4][160]
     float *sbias = pbuf + 2 * TS * PROW;                               // [8][160]
     float *shb = sbias + 8 * WPC;                                      // [8]
     uint64_t *bars = reinterpret_cast<uint64_t *>(shb + 8);
@@ -328,7 +332,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1) mlp_tc_k
     uint64_t *a_ready = bars + 2 * NSTAGE; // [set][part] (leader): a converted output part, both CTAs
     uint64_t *acc = a_ready + 2 * NPART;   // [set][part]: a layer's accumulator part complete (commit multicast)
     uint64_t *acc_h = acc + 2 * NPART;     // heads accumulator complete
-    uint64_t *xc_ready = acc_h + 1;        // [buffer] (leader): both CTAs' xc operands have landed
     uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(bars + NBARS);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -346,8 +349,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1) mlp_tc_k
             tc::mbar_init(&acc[k], 1);
         }
         tc::mbar_init(acc_h, 1);
-        tc::mbar_init(&xc_ready[0], 2 * EPI_WARPS);
-        tc::mbar_init(&xc_ready[1], 2 * EPI_WARPS);
         tc::fence_mbar_init();
     }
     for (int i = threadIdx.x; i < 8 * WPC; i += THREADS)
@@ -364,8 +365,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1) mlp_tc_k
     const int ntiles_mine = cluster < a.ntiles ? (a.ntiles - 1 - cluster) / nclusters + 1 : 0;
 
     // Issue order (= weight-stream order = conversion order): layer 0 of the first
-    // tile, then per tile layers 1..7, layer 0 of the NEXT tile (its UMMAs need
-    // only xc, so they cover the conversion of layer 7), then the heads.
+    // tile, then per tile layers 1..7, layer 0 of the NEXT tile (a cterm copy that
+    // needs nothing from this tile), then the heads.
     auto stage_count = [&](int it) { return NL * NPART - (it + 1 < ntiles_mine ? 0 : NPART) + 1; };
     if (warp == kProducerWarp)
     {
@@ -375,6 +376,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1) mlp_tc_k
         uint32_t ph = 0;
         auto load = [&](int l, int p, int it) {
             const uint32_t bytes = l < NL ? stage_bytes(l, p) : HEAD_STAGE;
+            const uint32_t cbytes = l < NL && has_xc(l) ? cseg_bytes(p) : 0;
             const size_t off = stream_offset(l, p);
             MBAR_WAIT(&w_empty[stage], ph ^ 1, 1);
             if (tc::elect_one())
@@ -383,9 +385,19 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1) mlp_tc_k
                     tc::mbar_arrive(&w_full[stage]); // debug: stale weights, no TMA traffic
                 else
                 {
-                    tc::mbar_arrive_expect_tx(&w_full[stage], bytes);
-                    tc::bulk_g2s(ring + stage * SLOT, reinterpret_cast<const uint8_t *>(a.w_tc) + off + rank * bytes,
-                                 bytes, &w_full[stage]);
+                    tc::mbar_arrive_expect_tx(&w_full[stage], bytes + cbytes);
+                    if (bytes)
+                        tc::bulk_g2s(ring + stage * SLOT,
+                                     reinterpret_cast<const uint8_t *>(a.w_tc) + off + rank * bytes, bytes,
+                                     &w_full[stage]);
+                    if (cbytes)
+                    {
+                        int g0, s0;
+                        tile_origin(a, cluster + it * nclusters, rank, g0, s0);
+                        const uint8_t *src = reinterpret_cast<const uint8_t *>(a.cterm) +
+                                             ((size_t)(g0 / TG) * 4 + l / 2) * C_BLOCK + cseg_off(p);
+                        tc::bulk_g2s(ring + stage * SLOT + W_MAX, src, cbytes, &w_full[stage]);
+                    }
                 }
             }
             __syncwarp();
@@ -438,10 +450,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1) mlp_tc_k
         // leader: whole warp converged (waits by all lanes), UMMAs and commits by
         // one elected lane: keeps the issue loop free of YIELD/divergence overhead
         int stage = 0;
-        uint32_t ph = 0, aph = 0, xph = 0; // phase bits: aph bit set*2+part, xph bit buffer
+        uint32_t ph = 0, aph = 0; // phase bits: aph bit set*NPART+part
+        constexpr uint32_t PMASK = (1u << NPART) - 1;
         int ct = 0;                        // trunk layers issued: acc set = ct & 1
         int k = 0;                         // layers that read a converted layer: a_ready set = k & 1
-        const uint32_t r_base = tc::smem_u32(ring), x_base = tc::smem_u32(xcbuf);
+        const uint32_t r_base = tc::smem_u32(ring);
         auto next_stage = [&]() {
             if (++stage == NSTAGE)
             {
@@ -451,31 +464,25 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1) mlp_tc_k
         };
         // trunk layer l of local tile it
         auto trunk = [&](int it, int l) {
-            const uint32_t xhi = x_base + (it & 1) * 2 * XC_OP, xlo = xhi + XC_OP;
-            if (l == 0)
-            {
-                MBAR_WAIT_CL(&xc_ready[it & 1], (xph >> (it & 1)) & 1, 3);
-                xph ^= 1u << (it & 1);
-            }
             const int m = 8 * it + l; // TMEM region rotation
             const uint32_t dreg = tmem + (m % NREG) * WPC;
             const uint32_t areg = tmem + ((m + NREG - 1) % NREG) * WPC;
             const int ks = k & 1;
-            const uint32_t rph = (aph >> (ks * 2)) & 3;
+            const uint32_t rph = (aph >> (ks * NPART)) & PMASK;
 #pragma unroll
             for (int p = 0; p < NPART; p++)
             {
                 if (lane == 0)
-                    stamp(a, it, l, 100 + p);
+                    stamp(a, it, l, 112 + p);
                 MBAR_WAIT_CL(&w_full[stage], ph, 2);
                 tc::tc_fence_after();
                 if (lane == 0)
-                    stamp(a, it, l, 104 + p);
+                    stamp(a, it, l, 116 + p);
                 const uint32_t b = r_base + stage * SLOT;
                 if (p == 0)
-                    mma_part<0, SPLIT>(l, dreg, areg, b, xhi, xlo, &a_ready[ks * NPART], rph);
+                    mma_part<0, SPLIT>(l, dreg, areg, b, &a_ready[ks * NPART], rph);
                 else
-                    mma_part<1, SPLIT>(l, dreg + pcol(1), areg, b, xhi, xlo, &a_ready[ks * NPART], rph);
+                    mma_part<1, SPLIT>(l, dreg + pcol(1), areg, b, &a_ready[ks * NPART], rph);
                 if (tc::elect_one())
                 {
                     tc::mma2_commit(&w_empty[stage], 3);
@@ -483,13 +490,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1) mlp_tc_k
                 }
                 __syncwarp();
                 if (lane == 0)
-                    stamp(a, it, l, 108 + p);
+                    stamp(a, it, l, 120 + p);
                 next_stage();
             }
             ct++;
             if (l >= 1)
             {
-                aph ^= 3u << (ks * 2);
+                aph ^= PMASK << (ks * NPART);
                 k++;
             }
         };
@@ -504,11 +511,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1) mlp_tc_k
             // heads: A = layer 7's converted output, D = the heads columns
             const int ks = k & 1;
             if (lane == 0)
-                stamp(a, it, NL, 100);
+                stamp(a, it, NL, 112);
             MBAR_WAIT_CL(&w_full[stage], ph, 2);
             tc::tc_fence_after();
             mma_hidden<NHEAD_N, true, SPLIT>(tmem + HEAD_COL, r_base + stage * SLOT, tmem + ((8 * it + 7) % NREG) * WPC,
-                                             true, &a_ready[ks * NPART], (aph >> (ks * 2)) & 3);
+                                             true, &a_ready[ks * NPART], (aph >> (ks * NPART)) & PMASK);
             if (tc::elect_one())
             {
                 tc::mma2_commit(&w_empty[stage], 3);
@@ -516,9 +523,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1) mlp_tc_k
             }
             __syncwarp();
             if (lane == 0)
-                stamp(a, it, NL, 108);
+                stamp(a, it, NL, 120);
             next_stage();
-            aph ^= 3u << (ks * 2);
+            aph ^= PMASK << (ks * NPART);
             k++;
         }
     }
@@ -547,8 +554,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1) mlp_tc_k
                 fph ^= 1u << bit;
                 tc::tc_fence_after();
             }
-            if (lane == 0 && chunk < NGRP)
-                stamp(a, it, l, 16 + e);
+            if (lane == 0) // debug trace: first chunk 16 + e / 40 + e, second 64 + e / 88 + e
+                stamp(a, it, l, (chunk < NGRP ? 16 : 64) + e);
             if (!(a.debug & 2))
             {
                 const float *add = has_xc(l) ? prow + (l / 2) * WPC : sbias + l * WPC; // warp-uniform addend
@@ -574,8 +581,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1) mlp_tc_k
             if (lane == 0)
             {
                 tc::mbar_arrive_remote_relaxed(tc::mapa(&a_ready[(ct & 1) * NPART + p], 0)); // read by the next consumer
-                if (chunk < NGRP)
-                    stamp(a, it, l, 40 + e);
+                stamp(a, it, l, (chunk < NGRP ? 40 : 88) + e);
             }
         };
         auto convert_layer = [&](int it, int l) {
@@ -603,18 +609,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1) mlp_tc_k
                     a.res[hh * plane + (size_t)s * a.np + g] = v[hh] + shb[hh];
             }
         };
-        // operands of local tile `it` (buffer it & 1) have landed: publish them
+        // pterm rows of local tile `it` (buffer it & 1) have landed
         auto operands_ready = [&](int it) {
+            (void)it;
             tc::cp_async_wait_all();
-            tc::fence_proxy_async_smem(); // xc operand is read by the tensor core (async proxy)
-            __syncwarp();
-            if (lane == 0)
-                tc::mbar_arrive_remote(tc::mapa(&xc_ready[it & 1], 0));
             tc::named_bar(1, EPI_THREADS); // pterm rows copied by other warps are visible
         };
         auto prefetch = [&](int it) {
-            prefetch_tile(a, cluster + it * nclusters, rank, xcbuf + (it & 1) * 2 * XC_OP, pbuf + (it & 1) * TS * PROW,
-                          et);
+            prefetch_tile(a, cluster + it * nclusters, rank, pbuf + (it & 1) * TS * PROW, et);
         };
 
         if (ntiles_mine > 0)
@@ -697,40 +699,45 @@ int mlp_tc_trace(long long *out)
     return cudaMemcpy(out, g_trace_buf, 3 * 9 * 128 * sizeof(long long), cudaMemcpyDeviceToHost) == cudaSuccess ? 0 : 2;
 }
 
-// Pack the weights in the kernel's consumption order (see stage_bytes): per trunk
-// layer l = 0..7 and output part p, for pair rank 0 then 1 (each its half of the
-// part's columns): the xc products (layers 0,2,4,6: centre-encoding columns of
-// W_l, K padded 42 -> 48), then the 10 hidden K steps (layers 1..7); finally the
-// heads (N = 32, columns 0-4 real).
-// whT: [7][k][n] hidden weights (k-major); wcen: [4][n][dc] centre columns of
-// layers 0,2,4,6; heads: [5][wp]; cenc: [np][dc] centre encodings (host glibc,
-// deform.cpp:54-70).
-void prepare_tc_weights(Ctx &c, const std::vector<float> &whT, const std::vector<float> &wcen,
-                        const std::vector<float> &heads, const std::vector<float> &cenc)
+// cterm blocks from the per-Gaussian centre terms cg [np][4][160] (W_c xc of
+// layers 0,2,4,6, FP32, center_terms_kernel): block b, layer j, column group
+// n / 4, row = Gaussian % 32 -> the tcgen05.cp source layout (zero rows past np)
+__global__ void cterm_pack_kernel(const float *__restrict__ cg, float *__restrict__ ct, int np, int nblk)
 {
-    const int WP = c.net.wp, DC = c.net.dc;
+    const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (idx >= (int64_t)nblk * TG * 4 * WPC)
+        return;
+    const int n = (int)(idx % WPC), j = (int)((idx / WPC) % 4);
+    const int g = (int)(idx / (4 * WPC));
+    const int blk = g / TG, row = g % TG;
+    const size_t dst = ((size_t)blk * 4 + j) * (C_BLOCK / 4) + ((size_t)(n / 4) * TG + row) * 4 + n % 4;
+    ct[dst] = g < np ? cg[((size_t)g * 4 + j) * WPC + n] : 0.0f;
+}
+
+// Pack the weights in the kernel's consumption order (see stage_bytes): per trunk
+// layer l = 1..7 and output part p, for pair rank 0 then 1 (each its half of the
+// part's columns): the 10 hidden K steps; finally the heads (N = 32, columns 0-4
+// real). Layer 0 streams no weights (its accumulator is the cterm alone).
+// whT: [7][k][n] hidden weights (k-major); heads: [5][wp]. The cterm blocks are
+// repacked on the device from c.net.cg.
+void prepare_tc_weights(Ctx &c, const std::vector<float> &whT, const std::vector<float> &heads)
+{
+    const int WP = c.net.wp;
     std::vector<uint16_t> packed;
     auto kstep = [&](int nc, auto &&w_of) {
         const size_t at = packed.size();
         packed.resize(at + 2 * nc * 16);
         pack_kstep(packed.data() + at, nc, w_of);
     };
-    for (int l = 0; l < NL; l++)
+    for (int l = 1; l < NL; l++)
         for (int p = 0; p < NPART; p++)
             for (int rk = 0; rk < 2; rk++)
             {
                 const int nc = npart(p) / 2, cbase = pcol(p) + rk * nc;
-                if (has_xc(l))
-                    for (int kk = 0; kk < KC; kk++)
-                        kstep(nc, [&](int nl, int k16) {
-                            const int kx = 16 * kk + k16, n = cbase + nl;
-                            return kx < DC ? wcen[((size_t)(l / 2) * WP + n) * DC + kx] : 0.0f;
-                        });
-                if (l >= 1)
-                    for (int k = 0; k < KSTEPS; k++)
-                        kstep(nc, [&](int nl, int k16) {
-                            return whT[((size_t)(l - 1) * WP + (k * 16 + k16)) * WP + cbase + nl];
-                        });
+                for (int k = 0; k < KSTEPS; k++)
+                    kstep(nc, [&](int nl, int k16) {
+                        return whT[((size_t)(l - 1) * WP + (k * 16 + k16)) * WP + cbase + nl];
+                    });
             }
     for (int rk = 0; rk < 2; rk++)
         for (int k = 0; k < KSTEPS; k++)
@@ -738,33 +745,21 @@ void prepare_tc_weights(Ctx &c, const std::vector<float> &whT, const std::vector
                 const int n = rk * (NHEAD_N / 2) + nl;
                 return n < 5 ? heads[(size_t)n * WP + k * 16 + k16] : 0.0f;
             });
+    if (packed.size() * 2 != stream_offset(NL, 0) + 2 * (size_t)HEAD_STAGE)
+        throw std::logic_error("tc weight stream size");
     void *d = nullptr;
     check_cuda(cudaMalloc(&d, packed.size() * 2), "cudaMalloc tc weights");
     c.allocs.push_back(d);
     check_cuda(cudaMemcpy(d, packed.data(), packed.size() * 2, cudaMemcpyHostToDevice), "upload tc weights");
     c.net.w_tc = static_cast<uint16_t *>(d);
 
-    // xc operand blocks: 32 Gaussians x 48 K, hi then lo, K-major core matrices
-    // (element (row, k) at ((k/8)*4 + row/8)*64 + (row%8)*8 + k%8)
     const int nblk = (c.g.n + TG - 1) / TG;
-    std::vector<uint16_t> xb((size_t)nblk * XC_BLOCK, 0); // XC_BLOCK bytes per operand = hi+lo elements
-    for (int b = 0; b < nblk; b++)
-        for (int row = 0; row < TG; row++)
-        {
-            const int g = b * TG + row;
-            for (int k = 0; k < XCK; k++)
-            {
-                const float v = (g < c.g.n && k < DC) ? cenc[(size_t)g * DC + k] : 0.0f;
-                const uint16_t hb = bf16_bits(v);
-                const size_t idx = (size_t)((k / 8) * (TG / 8) + row / 8) * 64 + (row % 8) * 8 + k % 8;
-                xb[(size_t)b * XC_BLOCK + idx] = hb;
-                xb[(size_t)b * XC_BLOCK + XC_BLOCK / 2 + idx] = bf16_bits(v - bf16_float(hb));
-            }
-        }
-    check_cuda(cudaMalloc(&d, xb.size() * 2), "cudaMalloc xc blocks");
+    const size_t total = (size_t)nblk * TG * 4 * WPC;
+    check_cuda(cudaMalloc(&d, total * sizeof(float)), "cudaMalloc cterm blocks");
     c.allocs.push_back(d);
-    check_cuda(cudaMemcpy(d, xb.data(), xb.size() * 2, cudaMemcpyHostToDevice), "upload xc blocks");
-    c.net.xc_tc = static_cast<uint16_t *>(d);
+    c.net.c_tc = static_cast<float *>(d);
+    cterm_pack_kernel<<<(unsigned)((total + 255) / 256), 256, 0, c.stream>>>(c.net.cg, c.net.c_tc, c.g.np, nblk);
+    check_cuda(cudaStreamSynchronize(c.stream), "cterm blocks");
 }
 
 void launch_mlp_tc(Ctx &c, int nb, cudaStream_t st)
@@ -803,7 +798,7 @@ void launch_mlp_tc(Ctx &c, int nb, cudaStream_t st)
     }
     TcArgs a;
     a.w_tc = c.net.w_tc;
-    a.xc = c.net.xc_tc;
+    a.cterm = c.net.c_tc;
     a.bias = c.net.bias;
     a.pterm = c.w.pterm;
     a.hbias = c.net.hbias;

@@ -59,7 +59,7 @@ struct NetDev
     float *hbias;          // [5]
     // tcgen05 path (bf16 hi/lo, UMMA canonical K-major layout, see k_mlp_tc.cu)
     uint16_t *w_tc;        // packed bf16 hi/lo weights in the tensor-core kernel's consumption order
-    uint16_t *xc_tc;       // packed bf16 hi/lo centre encodings per 32-Gaussian block
+    float *c_tc;           // cg repacked per 32-Gaussian block as tcgen05.cp sources (k_mlp_tc.cu)
 };
 
 // Per-chunk scratch (positions per chunk = cap_b).
@@ -233,8 +233,7 @@ void launch_heads(Ctx &c, int nb, uint32_t flags, double *d_pooled, double *d_rs
 void launch_heads_from_spectra(Ctx &c, int nb, const float *d_spec, cudaStream_t st);
 
 bool mlp_tc_available();
-void prepare_tc_weights(Ctx &c, const std::vector<float> &whT, const std::vector<float> &wcen,
-                        const std::vector<float> &heads, const std::vector<float> &cenc);
+void prepare_tc_weights(Ctx &c, const std::vector<float> &whT, const std::vector<float> &heads);
 void launch_mlp_tc(Ctx &c, int nb, cudaStream_t st);
 int mlp_tc_trace(long long *out);
 size_t metrics_tmp_doubles(const Ctx &c, int nb);

@@ -342,6 +342,14 @@ __device__ __forceinline__ void mma2_f16_ts(uint32_t tmem_d, uint32_t tmem_a, ui
                  "tcgen05.mma.cta_group::2.kind::f16 [%0], [%1], %2, %3, p;\n\t}" ::"r"(tmem_d),
                  "r"(tmem_a), "l"(bdesc), "r"(idesc), "r"(accum));
 }
+// shared memory -> TMEM, CTA pair: each CTA copies 32 rows x 128 bits from ITS OWN
+// shared memory (same offset in both) into all four 32-lane quarters of its TMEM
+// at [taddr] (4 consecutive 32-bit columns). Ordered with this thread's later
+// tcgen05.mma (measured: tools/cp_test.cu)
+__device__ __forceinline__ void cp2_32x128b_x4(uint32_t taddr, uint64_t desc)
+{
+    asm volatile("tcgen05.cp.cta_group::2.32x128b.warpx4 [%0], %1;" ::"r"(taddr), "l"(desc) : "memory");
+}
 // all prior cta_group::2 UMMAs of this thread arrive on `bar` in every CTA of `mask`
 __device__ __forceinline__ void mma2_commit(uint64_t *bar, uint16_t mask)
 {

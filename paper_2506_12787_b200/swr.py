@@ -24,7 +24,8 @@ from dataclasses import dataclass
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libswr.so")
+# SWR_LIB: an alternative build of the same library (tools/build_variant.py experiments)
+LIB_PATH = os.environ.get("SWR_LIB") or os.path.join(_HERE, "libswr.so")
 
 OUT_SPECTRA, OUT_POOLED, OUT_RSSI, OUT_AOA, NO_RESIDUALS = 1, 2, 4, 8, 16
 MLP_FP32, MLP_BF16X3, MLP_BF16 = 0, 1, 2
