@@ -233,9 +233,18 @@ __device__ __forceinline__ void prefetch_tile(const TcArgs &a, int tile, uint32_
     tc::cp_async_commit();
 }
 
+// Debug hooks (SWR_TC_DEBUG bits: 1 stale weights, 2 skip the conversion math, 8
+// clock64 trace) exist only in builds with -DSWR_TC_DEBUG_HOOKS (tools/
+// build_variant.py): every instruction they add to the epilogue lengthens the
+// conversion chain between layers.
+#ifdef SWR_TC_DEBUG_HOOKS
+constexpr bool kHooks = true;
+#else
+constexpr bool kHooks = false;
+#endif
 __device__ __forceinline__ void stamp(const TcArgs &a, int it, int l, int slot)
 {
-    if (a.trace && blockIdx.x == 0 && it < 3)
+    if (kHooks && a.trace && blockIdx.x == 0 && it < 3)
         a.trace[(it * 9 + l) * 128 + slot] = clock64();
 }
 
@@ -381,7 +390,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1) mlp_tc_k
             MBAR_WAIT(&w_empty[stage], ph ^ 1, 1);
             if (tc::elect_one())
             {
-                if ((a.debug & 1) && it > 0)
+                if (kHooks && (a.debug & 1) && it > 0)
                     tc::mbar_arrive(&w_full[stage]); // debug: stale weights, no TMA traffic
                 else
                 {
@@ -556,7 +565,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1) mlp_tc_k
             }
             if (lane == 0) // debug trace: first chunk 16 + e / 40 + e, second 64 + e / 88 + e
                 stamp(a, it, l, (chunk < NGRP ? 16 : 64) + e);
-            if (!(a.debug & 2))
+            if (!kHooks || !(a.debug & 2))
             {
                 const float *add = has_xc(l) ? prow + (l / 2) * WPC : sbias + l * WPC; // warp-uniform addend
                 const int n0 = chunk * 16;

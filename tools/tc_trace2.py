@@ -1,4 +1,5 @@
 """Timeline of the tensor-core MLP kernel, CTA 0, local tile 2 (SWR_TC_DEBUG=8 clock64 stamps).
+Needs a build with hooks: python tools/build_variant.py tools/var/hooks.so k_mlp_tc.cu -DSWR_TC_DEBUG_HOOKS, then SWR_LIB=tools/var/hooks.so.
 Per layer and output part p: MMA [stage wait start, stage landed, part issued]; epilogue:
 for the warps converting part p, [first acc seen .. last acc seen] -> [first .. last converted].
 Cycles from the tile's first stamp."""
