@@ -11,6 +11,8 @@
 // depend only on FP64 ops whose float inputs multiply exactly.
 #include "swr_internal.h"
 
+#include <type_traits>
+
 #include <cfloat>
 
 namespace swr
@@ -585,17 +587,19 @@ __device__ __forceinline__ float wrap_fast(float x)
 // primitive index) is cut into chunks of 32 pairs; warp w takes chunks w, w+8, ...
 // For a chunk, each lane first prepares one pair (gathers its dynamic state,
 // shape and box, clips the box to the tile: rows [max(r0, tile), min(r1, tile)]
-// x the one or two wrapped column spans, splat.cpp:450-470) into a per-warp
-// record in shared memory, and the warp sorts its 32 records by sweep count
-// (bitonic, shuffles). Then each half-warp evaluates one record of a
-// similar-sized pair of records at a time, its 16 lanes mapped onto the clipped
-// box only (rows per sweep = 16 / columns), so no lane is spent on cells the
-// reference does not evaluate and the per-pair setup costs one lane. Each
-// half-warp accumulates into its own shared-memory copy of the tile (no
-// atomics); the copies are summed in fixed order at the end, so the result is
-// bit-deterministic. The cutoff mask uses the reference's float q
+// x the one or two wrapped column spans, splat.cpp:450-470) into a record, the
+// warp sorts the 32 records by sweep count (bitonic, shuffles) and stores them in
+// that order, so similar records pair up. Then each half-warp evaluates one
+// record of a pair at a time: its 16 lanes first tabulate the record's per-row
+// terms (d_el and i00 d_el^2, or +inf where the reference skips the row,
+// splat.cpp:405-408), then sweep the clipped box with the lanes mapped onto it
+// (rows per sweep = 16 / columns), so no lane is spent on cells the reference
+// does not evaluate. Each half-warp accumulates into its own shared-memory copy
+// of the tile (no atomics); the copies are summed in fixed order at the end, so
+// the result is bit-deterministic. The cutoff mask uses the reference's float q
 // (same operation order, no FMA); exp(-q/2) is ex2.approx of a prescaled
-// argument.
+// argument. Chunks whose azimuths could need the reference's multi-turn wrap
+// (|daz| >= 3 pi) take a separate instantiation of the sweep code.
 struct RasterRec
 {
     float4 dyn;   // el, az, amplitude re, im
@@ -606,18 +610,40 @@ struct RasterRec
 // floor(x / d) == (x * m[d]) >> 12 for 0 <= x < 128, 1 <= d <= 32, m[d] = ceil(4096 / d)
 __host__ __device__ constexpr uint32_t magic12(int d) { return (4096u + d - 1) / d; }
 
+// the two-step wrap of wrap_fast without its |x| >= 3 pi escape (caller guarantees |x| < 3 pi)
+__device__ __forceinline__ float wrap_near(float x)
+{
+    x = x >= (float)kPi ? __fsub_rn(x, (float)(2 * kPi)) : x;
+    x = x < (float)(-kPi) ? __fadd_rn(x, (float)(2 * kPi)) : x;
+    return x;
+}
+
+__device__ __forceinline__ float2 shfl_f2(float2 v, int src)
+{
+    return make_float2(__shfl_sync(0xffffffffu, v.x, src), __shfl_sync(0xffffffffu, v.y, src));
+}
+
 // G = records evaluated side by side per warp: 2 (half-warps, tiles <= 16 wide) or
 // 1 (whole warp, tiles up to 32 wide)
+// Occupancy: 4-warp CTAs with 8 resident per SM (32 warps; register cap 64) measured
+// best -- the kernel is latency-bound (short scoreboard on shared memory, MUFU) and
+// 8-warp CTAs idle at the final barrier when a tile's few chunks split unevenly
+// (tools/build_variant.py sweeps: 8 warps x 4 CTAs 20.9 ms, 4 x 8 20.1-20.4 ms,
+// 2 x 16 21.8 ms per 1024 spectra at 50k; at 10k 5.43 -> 4.75 ms).
+#ifndef SWR_RASTER_MINB
+#define SWR_RASTER_MINB 4 // x 8 warps: resident warps per SM / 8
+#endif
 template <int kRasterWarps, int G>
-__global__ void __launch_bounds__(32 * kRasterWarps) raster_kernel(Grid g, SceneDev sd, const float4 *__restrict__ dyn,
+__global__ void __launch_bounds__(32 * kRasterWarps, SWR_RASTER_MINB * 8 / kRasterWarps) raster_kernel(Grid g, SceneDev sd, const float4 *__restrict__ dyn,
                                                      const int4 *__restrict__ rng, const int64_t *__restrict__ seg,
                                                      const int *__restrict__ tile_off, const int *__restrict__ prims,
                                                      float *__restrict__ spec, float4 *__restrict__ tile_part,
                                                      double *__restrict__ tile_sum, int want_heads)
 {
-    extern __shared__ float2 acc[]; // [2 * warps][T*T], then RasterRec [warps][32]
-    __shared__ float elc[64], azc[32]; // elc zero-padded: a lane's last sweep may run past the tile
+    extern __shared__ float2 acc[]; // [G * warps][T*T], then RasterRec [warps][32]
+    __shared__ float elc[64], azc[32]; // elc zero-padded to 64 rows
     __shared__ uint32_t magic[33];
+    __shared__ float2 rowtab_all[kRasterWarps * G][32 / G]; // per record slot: (d_el, i00 d_el^2 | +inf) per tile row
     const int T = g.tile, TT = T * T;
     const int t = blockIdx.x, s = blockIdx.y;
     const int tr0 = (t / g.tw) * T, tc0 = (t % g.tw) * T;
@@ -625,8 +651,6 @@ __global__ void __launch_bounds__(32 * kRasterWarps) raster_kernel(Grid g, Scene
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     constexpr int LPR = 32 / G; // lanes per record
     RasterRec *recs = reinterpret_cast<RasterRec *>(acc + G * kRasterWarps * TT) + warp * 32;
-    __shared__ uint8_t order_all[kRasterWarps * 32]; // per warp: records sorted by sweep count
-    uint8_t *order = order_all + warp * 32;
     for (int i = threadIdx.x; i < G * kRasterWarps * TT; i += blockDim.x)
         acc[i] = make_float2(0.f, 0.f);
     if (threadIdx.x < 64)
@@ -641,8 +665,9 @@ __global__ void __launch_bounds__(32 * kRasterWarps) raster_kernel(Grid g, Scene
     const int64_t sbase = (int64_t)s * g.np;
     const int half = G == 2 ? lane >> 4 : 0, hl = lane & (LPR - 1); // record slot and its lane
     float2 *my = acc + (G * warp + half) * TT;
+    float2 *rowtab = rowtab_all[G * warp + half];
     const uint32_t acc_base = (uint32_t)__cvta_generic_to_shared(my);
-    const uint32_t el_base = (uint32_t)__cvta_generic_to_shared(elc);
+    const uint32_t tab_base = (uint32_t)__cvta_generic_to_shared(rowtab);
     const float cut2 = g.cut2;
     const float kExp = -0.72134752044448170368f; // -0.5 * log2(e)
     const int *plist = prims + lb;               // 32-bit offsets inside this (position, tile) list
@@ -650,6 +675,71 @@ __global__ void __launch_bounds__(32 * kRasterWarps) raster_kernel(Grid g, Scene
     const float4 *dyn_s = dyn + sbase;
     const int4 *rng_s = rng + sbase;
     const int tcw = tc1 - tc0 + 1;
+
+    // evaluate the warp's 32 stored records (SLOW: azimuth differences may need
+    // the multi-turn wrap)
+    auto evaluate = [&](auto slow_tag) {
+        constexpr bool SLOW = decltype(slow_tag)::value;
+#pragma unroll 1
+        for (int j = 0; j < 32 / G; j++)
+        {
+            const RasterRec &R = recs[G * j + half]; // this slot's record
+            const int4 bx = R.box;
+            const int sweeps = bx.z >> 24;
+            const int loop = G == 2 ? max(sweeps, __shfl_xor_sync(0xffffffffu, sweeps, 16)) : sweeps;
+            if (loop == 0)
+                continue;
+            const float4 A = R.dyn, S = R.shape;
+            // per-row terms of this record: d_el and q_c = i00 d_el^2, +inf where
+            // (d_el / l1)^2 > r^2 (the reference skips the row; q = inf fails q <= r^2)
+            if (hl < T)
+            {
+                const float d_el = __fsub_rn(elc[hl], A.x);
+                const float u0 = __fmul_rn(d_el, S.w);
+                const float qc = __fmul_rn(u0, u0) > cut2 ? __int_as_float(0x7f800000)
+                                                          : __fmul_rn(__fmul_rn(S.x, d_el), d_el);
+                rowtab[hl] = make_float2(d_el, qc);
+            }
+            __syncwarp();
+            const int ncol = bx.z & 63, na = (bx.z >> 6) & 63, a0off = (bx.z >> 12) & 63, rpi = (bx.z >> 18) & 63;
+            const uint32_t mn = (uint32_t)bx.w & 0x1fffu, mr = (uint32_t)bx.w >> 13;
+            const int lr = (int)(((uint32_t)hl * mn) >> 12), lc = hl - lr * ncol;
+            const bool lane_on = sweeps > 0 && lr < rpi;
+            const int cc = lane_on ? (lc < na ? a0off + lc : lc - na) : 0; // column inside the tile
+            const float xaz = __fsub_rn(azc[cc], A.y);
+            const float d_az = SLOW ? wrap_fast(xaz) : wrap_near(xaz);
+            const float w1 = __fmul_rn(__fmul_rn(S.z, d_az), d_az);
+            const float w2 = __fmul_rn(S.y, d_az); // (2 * i01) * d_az
+            // lane-private pointers (32-bit shared addresses): its row's table entry
+            // and its cell; both advance by rpi rows per sweep
+            const int rr0 = lane_on ? bx.x + lr : 0;
+            uint32_t tp = tab_base + 8u * (uint32_t)rr0;
+            uint32_t cp = acc_base + 8u * (uint32_t)(rr0 * T + cc);
+            const uint32_t t_step = lane_on ? 8u * (uint32_t)rpi : 0u, c_step = lane_on ? 8u * (uint32_t)(rpi * T) : 0u;
+            // sweeps in which this lane's row is inside the box
+            const int nvalid = lane_on ? (int)(((uint32_t)(bx.y - rr0 + rpi) * mr) >> 12) : 0;
+#pragma unroll 2
+            for (int it = 0; it < loop; it++, tp += t_step, cp += c_step)
+            {
+                float d_el, qc;
+                asm volatile("ld.shared.v2.f32 {%0, %1}, [%2];" : "=f"(d_el), "=f"(qc) : "r"(tp));
+                const float q = __fadd_rn(__fadd_rn(qc, __fmul_rn(d_el, w2)), w1);
+                const bool ok = it < nvalid && q <= cut2;
+                float e;
+                asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(e) : "f"(q * kExp));
+                // predicated read-modify-write of the cell (no branch)
+                asm volatile("{\n\t.reg .pred p;\n\t.reg .f32 a, b;\n\t"
+                             "setp.ne.u32 p, %0, 0;\n\t"
+                             "@p ld.shared.v2.f32 {a, b}, [%1];\n\t"
+                             "@p fma.rn.f32 a, %2, %4, a;\n\t"
+                             "@p fma.rn.f32 b, %3, %4, b;\n\t"
+                             "@p st.shared.v2.f32 [%1], {a, b};\n\t}" ::"r"((uint32_t)ok),
+                             "r"(cp), "f"(A.z), "f"(A.w), "f"(e)
+                             : "memory");
+            }
+            __syncwarp(); // the row table is rewritten for the next record
+        }
+    };
 
     // gathered state of the lane's pair in the next chunk (software pipelined)
     int c0 = warp * 32;
@@ -660,7 +750,8 @@ __global__ void __launch_bounds__(32 * kRasterWarps) raster_kernel(Grid g, Scene
 #pragma unroll 1
     for (; c0 < cnt; c0 += kRasterWarps * 32)
     {
-        // this lane's pair -> record
+        bool slow;
+        // this lane's pair -> record, stored in sweep-count order
         {
             const int pr0 = max(b.x, tr0), pr1 = min(b.y, tr1);
             int a0 = tc0, na = tcw, nb2 = 0;
@@ -681,13 +772,12 @@ __global__ void __launch_bounds__(32 * kRasterWarps) raster_kernel(Grid g, Scene
                 mr = magic[rpi];
                 sweeps = (int)(((uint32_t)(nrow + rpi - 1) * mr) >> 12);
             }
-            RasterRec r;
-            r.dyn = d;
-            r.shape = make_float4(sh.x, __fmul_rn(2.0f, sh.y), sh.z, sh.w);
+            // |azc - az| < 3 pi for every column when az in (-3, 9) (azc in [0, 2 pi))
+            slow = __any_sync(0xffffffffu, sweeps > 0 && !(d.y > -3.0f && d.y < 9.0f));
             const int a0off = na > 0 ? a0 - tc0 : 0; // (a0 may lie past the tile when only the wrapped span is in it)
-            r.box = make_int4(pr0 - tr0, pr1 - tr0, ncol | (na << 6) | (a0off << 12) | (rpi << 18) | (sweeps << 24),
-                              (int)(mn | (mr << 13)));
-            recs[lane] = r;
+            const int4 box = make_int4(pr0 - tr0, pr1 - tr0,
+                                       ncol | (na << 6) | (a0off << 12) | (rpi << 18) | (sweeps << 24),
+                                       (int)(mn | (mr << 13)));
             // sort (sweeps, lane) ascending across the warp: similar records pair up
             uint32_t key = ((uint32_t)sweeps << 5) | (uint32_t)lane;
 #pragma unroll
@@ -699,7 +789,16 @@ __global__ void __launch_bounds__(32 * kRasterWarps) raster_kernel(Grid g, Scene
                     const bool up = (lane & k) == 0, lower = (lane & jj) == 0;
                     key = (lower == up) ? min(key, o) : max(key, o);
                 }
-            order[lane] = (uint8_t)(key & 31);
+            const int src = (int)(key & 31);
+            RasterRec r;
+            const float2 dxy = shfl_f2(make_float2(d.x, d.y), src), dzw = shfl_f2(make_float2(d.z, d.w), src);
+            const float2 sxy = shfl_f2(make_float2(sh.x, __fmul_rn(2.0f, sh.y)), src),
+                         szw = shfl_f2(make_float2(sh.z, sh.w), src);
+            r.dyn = make_float4(dxy.x, dxy.y, dzw.x, dzw.y);
+            r.shape = make_float4(sxy.x, sxy.y, szw.x, szw.y);
+            r.box = make_int4(__shfl_sync(0xffffffffu, box.x, src), __shfl_sync(0xffffffffu, box.y, src),
+                              __shfl_sync(0xffffffffu, box.z, src), __shfl_sync(0xffffffffu, box.w, src));
+            recs[lane] = r;
         }
         // prefetch the pairs of this warp's next chunk
         const int cn = c0 + kRasterWarps * 32;
@@ -708,55 +807,10 @@ __global__ void __launch_bounds__(32 * kRasterWarps) raster_kernel(Grid g, Scene
         d = gi >= 0 ? dyn_s[gi] : make_float4(0.f, 0.f, 0.f, 0.f);
         sh = gi >= 0 ? sd.shape[gi] : make_float4(0.f, 0.f, 0.f, 0.f);
         __syncwarp();
-#pragma unroll 1
-        for (int j = 0; j < 32 / G; j++)
-        {
-            const RasterRec &R = recs[order[G * j + half]]; // this slot's record
-            const int4 bx = R.box;
-            const int sweeps = bx.z >> 24;
-            const int loop = G == 2 ? max(sweeps, __shfl_xor_sync(0xffffffffu, sweeps, 16)) : sweeps;
-            if (loop == 0)
-                continue;
-            const float4 A = R.dyn, S = R.shape;
-            const int ncol = bx.z & 63, na = (bx.z >> 6) & 63, a0off = (bx.z >> 12) & 63, rpi = (bx.z >> 18) & 63;
-            const uint32_t mn = (uint32_t)bx.w & 0x1fffu, mr = (uint32_t)bx.w >> 13;
-            const int lr = (int)(((uint32_t)hl * mn) >> 12), lc = hl - lr * ncol;
-            const bool lane_on = sweeps > 0 && lr < rpi;
-            const int cc = lane_on ? (lc < na ? a0off + lc : lc - na) : 0; // column inside the tile
-            const float d_az = wrap_fast(__fsub_rn(azc[cc], A.y));
-            const float w1 = __fmul_rn(__fmul_rn(S.z, d_az), d_az);
-            const float w2 = __fmul_rn(S.y, d_az); // (2 * i01) * d_az
-            // lane-private pointers (32-bit shared addresses): its row's el centre and
-            // its cell; both advance by rpi rows per sweep
-            const int rr0 = lane_on ? bx.x + lr : 0;
-            uint32_t elp = el_base + 4u * (uint32_t)rr0;
-            uint32_t cp = acc_base + 8u * (uint32_t)(rr0 * T + cc);
-            const uint32_t el_step = lane_on ? 4u * (uint32_t)rpi : 0u, c_step = lane_on ? 8u * (uint32_t)(rpi * T) : 0u;
-            // sweeps in which this lane's row is inside the box
-            const int nvalid = lane_on ? (int)(((uint32_t)(bx.y - rr0 + rpi) * mr) >> 12) : 0;
-#pragma unroll 2
-            for (int it = 0; it < loop; it++, elp += el_step, cp += c_step)
-            {
-                float elv;
-                asm volatile("ld.shared.f32 %0, [%1];" : "=f"(elv) : "r"(elp));
-                const float d_el = __fsub_rn(elv, A.x);
-                const float u0 = __fmul_rn(d_el, S.w);
-                const float q_c = __fmul_rn(__fmul_rn(S.x, d_el), d_el);
-                const float q = __fadd_rn(__fadd_rn(q_c, __fmul_rn(d_el, w2)), w1);
-                const bool ok = it < nvalid && !(__fmul_rn(u0, u0) > cut2) && q <= cut2;
-                float e;
-                asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(e) : "f"(q * kExp));
-                // predicated read-modify-write of the cell (no branch)
-                asm volatile("{\n\t.reg .pred p;\n\t.reg .f32 a, b;\n\t"
-                             "setp.ne.u32 p, %0, 0;\n\t"
-                             "@p ld.shared.v2.f32 {a, b}, [%1];\n\t"
-                             "@p fma.rn.f32 a, %2, %4, a;\n\t"
-                             "@p fma.rn.f32 b, %3, %4, b;\n\t"
-                             "@p st.shared.v2.f32 [%1], {a, b};\n\t}" ::"r"((uint32_t)ok),
-                             "r"(cp), "f"(A.z), "f"(A.w), "f"(e)
-                             : "memory");
-            }
-        }
+        if (slow)
+            evaluate(std::integral_constant<bool, true>());
+        else
+            evaluate(std::integral_constant<bool, false>());
         __syncwarp(); // records are rewritten for the next chunk
     }
     __syncthreads();
@@ -820,10 +874,17 @@ static void launch_raster_w(Ctx &c, int nb, float *d_spec, bool want_heads, cuda
 
 // warps = 8 (standalone) or 4 (small enough to run beside the persistent MLP kernel);
 // two records per warp when a tile row fits in 16 lanes
+#ifndef SWR_RASTER_WARPS
+#define SWR_RASTER_WARPS 4
+#endif
 void launch_raster(Ctx &c, int nb, float *d_spec, bool want_heads, cudaStream_t st, int warps)
 {
+    if (warps == 0)
+        warps = SWR_RASTER_WARPS;
     const bool narrow = c.g.tile <= 16;
-    if (warps == 4)
+    if (warps == 2)
+        narrow ? launch_raster_w<2, 2>(c, nb, d_spec, want_heads, st) : launch_raster_w<2, 1>(c, nb, d_spec, want_heads, st);
+    else if (warps == 4)
         narrow ? launch_raster_w<4, 2>(c, nb, d_spec, want_heads, st) : launch_raster_w<4, 1>(c, nb, d_spec, want_heads, st);
     else
         narrow ? launch_raster_w<8, 2>(c, nb, d_spec, want_heads, st) : launch_raster_w<8, 1>(c, nb, d_spec, want_heads, st);
