@@ -392,7 +392,9 @@ def main():
     wp = 160 if scene.width <= 160 else 512
     issued = None
     if args.precision != "fp32" and wp == 160:
-        issued = (3 if args.precision == "bf16x3" else 1) * 2 * (7 * wp * wp + 4 * 48 * wp + wp * 32)
+        # UMMA work per row: 7 hidden layers 160x160 + heads 160x32 (the centre-encoding
+        # terms enter as tcgen05.cp copies, no UMMAs), x3 split passes for bf16x3
+        issued = (3 if args.precision == "bf16x3" else 1) * 2 * (7 * wp * wp + wp * 32)
     traffic = None
     prof = os.path.join(ROOT, "profiles", "ncu_mlp_traffic.json")
     if os.path.exists(prof) and args.chunk == 256 and args.config == 2:
