@@ -304,7 +304,10 @@ void build_scene(Ctx &c, const HostScene &hs, int device)
     check_cuda(cudaStreamSynchronize(c.stream), "centre terms");
     dfree(c, d_cenc);
     if (mlp_tc_available() && WP == 160)
+    {
         prepare_tc_weights(c, whT, heads);
+        prepare_tc2_weights(c, whT, heads);
+    }
 }
 
 // ------------------------------------------------------------- work buffers
@@ -825,6 +828,12 @@ int swr_set_option(swr_ctx *ctx, const char *key, double value)
             if (v != 0 && !(mlp_tc_available() && c.has_net && c.net.wp == 160))
                 throw std::invalid_argument("tensor-core MLP unavailable for this scene (width must be <= 160)");
             c.mlp_precision = v;
+        }
+        else if (k == "mlp_kernel")
+        {
+            if (int(value) != 1 && int(value) != 2)
+                throw std::invalid_argument("mlp_kernel must be 1 (output parts) or 2 (two-tile ping-pong)");
+            c.mlp_kernel = int(value);
         }
         else if (k == "chunk")
         {
@@ -1448,6 +1457,11 @@ int swr_scene_set_manifest_hash(swr_ctx *ctx, uint64_t hash)
 int swr_debug_mlp_trace(long long *out)
 {
     return swr::mlp_tc_trace(out);
+}
+
+int swr_debug_mlp_trace2(long long *out)
+{
+    return swr::mlp_tc2_trace(out);
 }
 
 // debug: after a render, time (ms) the MLP alone, the raster (8 / 4 warps) alone

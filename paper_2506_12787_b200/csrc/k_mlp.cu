@@ -333,7 +333,10 @@ void launch_mlp(Ctx &c, int nb, cudaStream_t st)
 {
     if (c.mlp_precision != 0 && mlp_tc_available() && c.net.wp == 160)
     {
-        launch_mlp_tc(c, nb, st);
+        if (c.mlp_kernel == 2)
+            launch_mlp_tc2(c, nb, st);
+        else
+            launch_mlp_tc(c, nb, st);
         return;
     }
     if (c.net.wp <= 160)

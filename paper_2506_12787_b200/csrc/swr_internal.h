@@ -60,6 +60,8 @@ struct NetDev
     // tcgen05 path (bf16 hi/lo, UMMA canonical K-major layout, see k_mlp_tc.cu)
     uint16_t *w_tc;        // packed bf16 hi/lo weights in the tensor-core kernel's consumption order
     float *c_tc;           // cg repacked per 32-Gaussian block as tcgen05.cp sources (k_mlp_tc.cu)
+    uint16_t *w_tc2 = nullptr; // packed bf16 hi/lo weights of the ping-pong kernel (k_mlp_tc2.cu)
+    uint16_t *wh_tc2 = nullptr; // its heads B operand (bf16 hi/lo, 2 ranks x 16 columns)
 };
 
 // Per-chunk scratch (positions per chunk = cap_b).
@@ -105,6 +107,7 @@ struct Ctx
     float cutoff = 3.0f;
     int tile = 16;
     int mlp_precision = 0;
+    int mlp_kernel = 2;   // tensor-core MLP: 1 = output parts (k_mlp_tc.cu), 2 = two tiles ping-pong (k_mlp_tc2.cu)
     int chunk = 256;
     bool stage_timing = false;
     double rssi_slope = 1.0, rssi_intercept = 0.0;
@@ -235,6 +238,9 @@ void launch_heads_from_spectra(Ctx &c, int nb, const float *d_spec, cudaStream_t
 bool mlp_tc_available();
 void prepare_tc_weights(Ctx &c, const std::vector<float> &whT, const std::vector<float> &heads);
 void launch_mlp_tc(Ctx &c, int nb, cudaStream_t st);
+void launch_mlp_tc2(Ctx &c, int nb, cudaStream_t st);
+int mlp_tc2_trace(long long *out);
+void prepare_tc2_weights(Ctx &c, const std::vector<float> &whT, const std::vector<float> &heads);
 int mlp_tc_trace(long long *out);
 size_t metrics_tmp_doubles(const Ctx &c, int nb);
 void launch_metrics(Ctx &c, const float *d_pred, const float *d_target, int nb, double peak, double *d_psnr,

@@ -324,6 +324,32 @@ def test_mlp_tensor_core_matches_fp64_oracle(scene2k, precision, tol):
     assert worst <= tol, worst
 
 
+@pytest.mark.parametrize("kernel", [1, 2])
+def test_mlp_tensor_core_kernels_many_tiles(scene2k, kernel):
+    """Both tensor-core kernels (1: output parts, 2: two-tile ping-pong) with many
+    tiles per CTA pair (203 positions x 2k Gaussians: ~11 super-tiles per pair, a
+    ragged last position block), against the FP64 oracle."""
+    ck = swr.Checkpoint.from_scene(scene2k)
+    ck.set_option("mlp_precision", swr.MLP_BF16X3)
+    ck.set_option("mlp_kernel", kernel)
+    port = O.Port(scene2k)
+    pos = random_positions(203, seed=23)
+    p01 = np.stack([port.normalize(p) for p in pos])
+    got = swr.predict_residuals(ck, p01)
+    worst = 0.0
+    for b in range(0, 203, 7):
+        want = port.predict(p01[b], precise=True)
+        for g, w in zip((got.d_center[b], got.d_response[b], got.d_atten[b]), want):
+            worst = max(worst, float(np.abs(g - w).max() / max(1e-30, float(np.abs(w).max()))))
+    assert worst <= 3e-5, worst
+
+
+def test_mlp_kernel_option_validated(scene2k):
+    ck = swr.Checkpoint.from_scene(scene2k)
+    with pytest.raises(ValueError):
+        ck.set_option("mlp_kernel", 3)
+
+
 def test_tensor_core_render_end_to_end(scene2k):
     """bf16x3 MLP end to end. Spectra rendered from the GPU's own residuals match the
     oracle to 1e-5; against the oracle's FP64-MLP render, 99.9% of cells agree to 1e-5
