@@ -75,7 +75,9 @@ int swr_scene_create(int n_elevation, int n_azimuth, int n, const float *center_
 void swr_scene_destroy(swr_ctx *ctx);
 int swr_scene_get_info(swr_ctx *ctx, swr_scene_info *info);
 
-/* Options: "mlp_precision" (SWR_MLP_*), "chunk" (positions per device chunk),
+/* Options: "mlp_precision" (SWR_MLP_*), "mlp_kernel" (tensor-core MLP: 2 = two
+ * position tiles in flight per CTA pair, the default; 1 = single tile with two
+ * output parts), "chunk" (positions per device chunk),
  * "rssi_slope" / "rssi_intercept" (affine RSSI calibration, tasks.cpp:60-94),
  * "stage_timing" (1: record per-stage CUDA events), "stage_reset" (zero the
  * accumulated stage times). */
