@@ -36,11 +36,12 @@
 // alone and ~4,000 cycles lost per super-tile boundary; the epilogue (40
 // 16-column conversions per step on 24 warps, ~1,900 cycles) is now the
 // limiting chain, and the UMMA issuer shares its SM sub-partition with it.
+// (Timeline figures above were taken with 6 column groups; 5 is the default.)
 //
-// Warps (832 threads per CTA): 0-23 epilogue (6 column groups x 4 TMEM lane
-// quarters; group g converts 16-column chunks g and g + 6), 24 producer (TMA of
-// this CTA's half of each weight stage + cterm blocks), 25 UMMA issuer (leader
-// CTA) / stage relay (peer CTA).
+// Warps (704 threads per CTA with the default 5 column groups): 0-19 epilogue
+// (5 column groups x 4 TMEM lane quarters; group g converts 16-column chunks g
+// and g + 5), 20 producer (TMA of this CTA's half of each weight stage + cterm
+// blocks), 21 UMMA issuer (leader CTA) / stage relay (peer CTA).
 #include "swr_internal.h"
 #include "tc_ptx.cuh"
 
@@ -72,7 +73,10 @@ constexpr int C_BLOCK = WPC * TG * 4;     // one layer's cterm block: [40 column
 constexpr int SLOT = W_BYTES + C_BLOCK;   // weight stage + the layer's cterm block (layers 2, 4, 6)
 constexpr int NSTAGE = 2;                 // weight stages (layers 1..7), each serving both tiles
 constexpr int NCSTAGE = 1;                // layer 0's cterm block, read by the epilogue
-constexpr int NGRP = 6;
+#ifndef SWR_TC2_GROUPS
+#define SWR_TC2_GROUPS 5 // 5: every epilogue warp converts two chunks (measured ~1% faster than 6 and 7)
+#endif
+constexpr int NGRP = SWR_TC2_GROUPS;
 constexpr int EPI_WARPS = 4 * NGRP, EPI_THREADS = 32 * EPI_WARPS;
 constexpr int THREADS = 32 * (EPI_WARPS + 2);
 constexpr int kProducerWarp = EPI_WARPS, kMmaWarp = EPI_WARPS + 1;
