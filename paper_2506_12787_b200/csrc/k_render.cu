@@ -381,7 +381,7 @@ __global__ void __launch_bounds__(256) emit_kernel(Grid g, const int4 *__restric
             col(tc);
 }
 
-constexpr int kSortThreads = 256; // 8 warps, 512 pairs per warp per sort chunk
+constexpr int kSortThreads = 256; // 8 warps, kSort / 8 pairs per warp per sort chunk
 
 // Per (position, chunk of kSort pairs): histogram of tile keys.
 __global__ void __launch_bounds__(kSortThreads) sort_hist_kernel(const uint16_t *__restrict__ keys,
