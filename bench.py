@@ -170,7 +170,8 @@ def config_dict(args, scene):
              4: "AoA sweep: dense 64x32x32 TX grid ({b} per GPU), {n} Gaussians, argmax only",
              5: "large scene stress: {n} Gaussians, width-512 deformation MLP, {b} positions per GPU"}
     return {"workload": f"BASELINE config {args.config}: " + names[args.config].format(b=args.batch, n=scene.n),
-            "gaussians": scene.n, "positions_per_gpu": args.batch, "grid": [scene.H, scene.W],
+            "gaussians": scene.n, "positions_per_gpu": args.batch, "chunk": args.chunk,
+            "grid": [scene.H, scene.W],
             "mlp_width": scene.width, "mlp_precision": args.precision, "parallelism": f"positions sharded x{args.gpus}",
             "l2": "per-step working set (spectra 265 MB + bins ~1 GB) exceeds the 126 MB L2"}
 
@@ -189,7 +190,8 @@ def main():
     ap.add_argument("--batch", type=int, default=None, help="positions per GPU (configs 2 and 5)")
     ap.add_argument("--precision", default=os.environ.get("SWR_BENCH_PRECISION", "bf16x3"),
                     choices=["fp32", "bf16x3", "bf16"])
-    ap.add_argument("--chunk", type=int, default=256)
+    ap.add_argument("--chunk", type=int, default=None,
+                    help="positions per device chunk (default: the library's, ~12.8M Gaussian-position rows)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--verify", action="store_true",
                     help="N > 1: rank 0 re-renders every rank's positions and checks the gathered spectra bitwise")
@@ -240,7 +242,9 @@ def main():
 
     ck = swr.Checkpoint.from_scene(scene, device=local)
     ck.set_option("mlp_precision", {"fp32": 0, "bf16x3": 1, "bf16": 2}[args.precision])
-    ck.set_option("chunk", args.chunk)
+    if args.chunk:
+        ck.set_option("chunk", args.chunk)
+    args.chunk = int(ck.get_option("chunk"))
     from paper_2506_12787_b200.shard import ChunkedGather, chunk_spans, gather_to_root, max_over_ranks, shard_range
     H, W = scene.H, scene.W
     if total_pos is None:                       # weak scaling: fixed positions per GPU

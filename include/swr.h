@@ -82,6 +82,9 @@ int swr_scene_get_info(swr_ctx *ctx, swr_scene_info *info);
  * "stage_timing" (1: record per-stage CUDA events), "stage_reset" (zero the
  * accumulated stage times). */
 int swr_set_option(swr_ctx *ctx, const char *key, double value);
+/* Current value of an option (the keys above except "stage_reset"). The default
+ * "chunk" depends on the scene: ~12.8M (Gaussian, position) rows, 256..1024. */
+int swr_get_option(swr_ctx *ctx, const char *key, double *value);
 
 /* Batched render_at (training.cpp:189-195) + heads, host buffers, synchronous.
  * pos_m: [B][3] metres. Any output may be NULL when its flag is off.

@@ -20,6 +20,7 @@
 #include <fstream>
 #include <stdexcept>
 #include <string>
+#include <functional>
 #include <vector>
 #include <thread>
 #include <chrono>
@@ -184,6 +185,9 @@ void build_scene(Ctx &c, const HostScene &hs, int device)
     g.cell_az = (2.0 * kPi) / hs.W;
     c.cutoff = hs.cutoff;
     c.tile = hs.tile;
+    // default chunk: ~12.8M (Gaussian, position) rows per chunk, 256..1024 positions
+    // (measured: 256 is fastest at 50k Gaussians, 1024 at 10k; option "chunk" overrides)
+    c.chunk = int(std::min<int64_t>(1024, std::max<int64_t>(256, (int64_t(12800000) / std::max(1, hs.n)) / 64 * 64)));
     std::memcpy(c.bbox_min, hs.bmin, sizeof(hs.bmin));
     c.manifest_hash = hs.manifest_hash;
     std::memcpy(c.bbox_max, hs.bmax, sizeof(hs.bmax));
@@ -425,9 +429,13 @@ static void resolve_stage_times(Ctx &c, bool keep)
 // Render one chunk of nb positions whose (device) coordinates are d_pos.
 // Residuals come from the MLP (use_mlp), the caller (already in w.res) or are
 // zero. d_spec may be null (heads only).
+// raster_sub > 0: the raster runs in launches of raster_sub positions and
+// after_raster(first, count) is called after each (the host-buffer path queues
+// that slice's D2H there, so only the last slice's copy is left exposed)
 static void run_chunk(Ctx &c, const float *d_pos, int nb, bool normalized, bool use_mlp, bool with_res,
                       float *d_spec, bool heads, uint32_t flags, double *d_pooled, double *d_rssi, int32_t *d_aoa_rc,
-                      double *d_aoa_ang, cudaStream_t st)
+                      double *d_aoa_ang, cudaStream_t st, int raster_sub = 0,
+                      const std::function<void(int, int)> &after_raster = {})
 {
     Timer tm(c, st);
     tm.mark();
@@ -454,7 +462,14 @@ static void run_chunk(Ctx &c, const float *d_pos, int nb, bool normalized, bool 
     ensure_pairs(c, pairs, nb, max_seg);
     launch_bin_sort(c, nb, pairs, int(max_seg), st);
     tm.mark();
-    launch_raster(c, nb, d_spec, heads, st);
+    const int sub = raster_sub > 0 ? std::min(raster_sub, nb) : nb;
+    for (int s0 = 0; s0 < nb; s0 += sub)
+    {
+        const int n = std::min(sub, nb - s0);
+        launch_raster(c, n, d_spec, heads, st, 0, s0);
+        if (after_raster)
+            after_raster(s0, n);
+    }
     tm.mark();
     if (heads)
         launch_heads(c, nb, flags, d_pooled, d_rssi, d_aoa_rc, d_aoa_ang, st);
@@ -462,6 +477,8 @@ static void run_chunk(Ctx &c, const float *d_pos, int nb, bool normalized, bool 
     check_cuda(cudaGetLastError(), "kernel launch");
     tm.finish();
 }
+
+constexpr int kCopySlice = 256; // positions per raster launch + D2H slice in swr_render (chunks above 256)
 
 static bool is_pinned(const void *p)
 {
@@ -857,6 +874,28 @@ int swr_set_option(swr_ctx *ctx, const char *key, double value)
     });
 }
 
+int swr_get_option(swr_ctx *ctx, const char *key, double *value)
+{
+    return guarded([&] {
+        const Ctx &c = ctx->c;
+        const std::string k(key);
+        if (k == "mlp_precision")
+            *value = c.mlp_precision;
+        else if (k == "mlp_kernel")
+            *value = c.mlp_kernel;
+        else if (k == "chunk")
+            *value = c.chunk;
+        else if (k == "rssi_slope")
+            *value = c.rssi_slope;
+        else if (k == "rssi_intercept")
+            *value = c.rssi_intercept;
+        else if (k == "stage_timing")
+            *value = c.stage_timing ? 1.0 : 0.0;
+        else
+            throw std::invalid_argument("unknown option " + k);
+    });
+}
+
 int swr_render_device(swr_ctx *ctx, const float *d_pos, int64_t B, uint32_t flags, float *d_spec, double *d_pooled,
                       double *d_rssi, int32_t *d_aoa_rc, double *d_aoa_ang, void *stream)
 {
@@ -906,17 +945,22 @@ int swr_render(swr_ctx *ctx, const float *pos_m, int64_t B, uint32_t flags, floa
             const int nb = int(std::min<int64_t>(chunk, B - b0));
             if (want_spec && b0 >= 2 * chunk)
                 check_cuda(cudaStreamWaitEvent(st, freed[k], 0), "wait copy");
-            run_chunk(c, d_pos + 3 * b0, nb, false, use_mlp, false, want_spec ? d_spec[k] : nullptr, heads, flags,
-                      d_pooled + b0, d_rssi + b0, d_rc + 2 * b0, d_ang + 2 * b0, st);
-            if (want_spec)
-            {
+            // the raster of a chunk above 256 positions runs in 256-position slices, each
+            // slice's spectra copied out right behind it (smaller slices lengthen the
+            // raster's launch tails more than they shorten the exposed copy)
+            auto copy_slice = [&](int s0, int n) {
                 check_cuda(cudaEventRecord(done[k], st), "record");
                 check_cuda(cudaStreamWaitEvent(copy_st, done[k], 0), "wait compute");
-                check_cuda(cudaMemcpyAsync(spectra + per * b0, d_spec[k], sizeof(float) * per * nb,
+                check_cuda(cudaMemcpyAsync(spectra + per * (b0 + s0), d_spec[k] + per * s0, sizeof(float) * per * n,
                                            cudaMemcpyDeviceToHost, copy_st),
                            "D2H spectra");
+            };
+            run_chunk(c, d_pos + 3 * b0, nb, false, use_mlp, false, want_spec ? d_spec[k] : nullptr, heads, flags,
+                      d_pooled + b0, d_rssi + b0, d_rc + 2 * b0, d_ang + 2 * b0, st,
+                      want_spec && nb > kCopySlice ? kCopySlice : 0,
+                      want_spec ? std::function<void(int, int)>(copy_slice) : std::function<void(int, int)>());
+            if (want_spec)
                 check_cuda(cudaEventRecord(freed[k], copy_st), "record");
-            }
         }
         if (pooled && (flags & SWR_OUT_POOLED))
             check_cuda(cudaMemcpyAsync(pooled, d_pooled, sizeof(double) * B, cudaMemcpyDeviceToHost, st), "D2H");

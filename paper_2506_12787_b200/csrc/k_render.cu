@@ -638,14 +638,14 @@ __global__ void __launch_bounds__(32 * kRasterWarps, SWR_RASTER_MINB * 8 / kRast
                                                      const int4 *__restrict__ rng, const int64_t *__restrict__ seg,
                                                      const int *__restrict__ tile_off, const int *__restrict__ prims,
                                                      float *__restrict__ spec, float4 *__restrict__ tile_part,
-                                                     double *__restrict__ tile_sum, int want_heads)
+                                                     double *__restrict__ tile_sum, int want_heads, int s_base)
 {
     extern __shared__ float2 acc[]; // [G * warps][T*T], then RasterRec [warps][32]
     __shared__ float elc[64], azc[32]; // elc zero-padded to 64 rows
     __shared__ uint32_t magic[33];
     __shared__ float2 rowtab_all[kRasterWarps * G][32 / G]; // per record slot: (d_el, i00 d_el^2 | +inf) per tile row
     const int T = g.tile, TT = T * T;
-    const int t = blockIdx.x, s = blockIdx.y;
+    const int t = blockIdx.x, s = s_base + blockIdx.y; // positions [s_base, s_base + gridDim.y) of the chunk
     const int tr0 = (t / g.tw) * T, tc0 = (t % g.tw) * T;
     const int tr1 = min(tr0 + T, g.H) - 1, tc1 = min(tc0 + T, g.W) - 1;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -850,7 +850,7 @@ __global__ void __launch_bounds__(32 * kRasterWarps, SWR_RASTER_MINB * 8 / kRast
 }
 
 template <int WARPS, int G>
-static void launch_raster_w(Ctx &c, int nb, float *d_spec, bool want_heads, cudaStream_t st)
+static void launch_raster_w(Ctx &c, int nb, float *d_spec, bool want_heads, cudaStream_t st, int s_base)
 {
     dim3 grid(c.g.tiles, nb);
     const size_t smem = (size_t)G * WARPS * c.g.tile * c.g.tile * sizeof(float2) + WARPS * 32 * sizeof(RasterRec);
@@ -868,7 +868,7 @@ static void launch_raster_w(Ctx &c, int nb, float *d_spec, bool want_heads, cuda
     }
     raster_kernel<WARPS, G><<<grid, 32 * WARPS, smem, st>>>(c.g, c.s, c.w.dyn, c.w.rng, c.w.seg, c.w.tile_off,
                                                             c.w.sorted, d_spec, c.w.tile_part, c.w.tile_sum,
-                                                            want_heads ? 1 : 0);
+                                                            want_heads ? 1 : 0, s_base);
     c.launches++;
 }
 
@@ -877,17 +877,20 @@ static void launch_raster_w(Ctx &c, int nb, float *d_spec, bool want_heads, cuda
 #ifndef SWR_RASTER_WARPS
 #define SWR_RASTER_WARPS 4
 #endif
-void launch_raster(Ctx &c, int nb, float *d_spec, bool want_heads, cudaStream_t st, int warps)
+void launch_raster(Ctx &c, int nb, float *d_spec, bool want_heads, cudaStream_t st, int warps, int s_base)
 {
     if (warps == 0)
         warps = SWR_RASTER_WARPS;
     const bool narrow = c.g.tile <= 16;
     if (warps == 2)
-        narrow ? launch_raster_w<2, 2>(c, nb, d_spec, want_heads, st) : launch_raster_w<2, 1>(c, nb, d_spec, want_heads, st);
+        narrow ? launch_raster_w<2, 2>(c, nb, d_spec, want_heads, st, s_base)
+               : launch_raster_w<2, 1>(c, nb, d_spec, want_heads, st, s_base);
     else if (warps == 4)
-        narrow ? launch_raster_w<4, 2>(c, nb, d_spec, want_heads, st) : launch_raster_w<4, 1>(c, nb, d_spec, want_heads, st);
+        narrow ? launch_raster_w<4, 2>(c, nb, d_spec, want_heads, st, s_base)
+               : launch_raster_w<4, 1>(c, nb, d_spec, want_heads, st, s_base);
     else
-        narrow ? launch_raster_w<8, 2>(c, nb, d_spec, want_heads, st) : launch_raster_w<8, 1>(c, nb, d_spec, want_heads, st);
+        narrow ? launch_raster_w<8, 2>(c, nb, d_spec, want_heads, st, s_base)
+               : launch_raster_w<8, 1>(c, nb, d_spec, want_heads, st, s_base);
 }
 
 // Heads on given spectra: the same per-tile partials as the raster epilogue.

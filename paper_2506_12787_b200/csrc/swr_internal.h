@@ -233,7 +233,8 @@ void launch_setup(Ctx &c, int nb, bool with_res, cudaStream_t st);
 void launch_state_out(Ctx &c, int nb, bool with_res, float *d_state, cudaStream_t st);
 void launch_bin_count(Ctx &c, int nb, cudaStream_t st);   // per-segment scan + segment bases
 void launch_bin_sort(Ctx &c, int nb, int64_t pairs, int max_seg, cudaStream_t st);
-void launch_raster(Ctx &c, int nb, float *d_spec, bool want_heads, cudaStream_t st, int warps = 0);
+// positions [s_base, s_base + nb) of the current chunk (the spectra pointer is the chunk's)
+void launch_raster(Ctx &c, int nb, float *d_spec, bool want_heads, cudaStream_t st, int warps = 0, int s_base = 0);
 void launch_heads(Ctx &c, int nb, uint32_t flags, double *d_pooled, double *d_rssi,
                   int32_t *d_aoa_rc, double *d_aoa_ang, cudaStream_t st);
 void launch_heads_from_spectra(Ctx &c, int nb, const float *d_spec, cudaStream_t st);

@@ -51,6 +51,7 @@ def lib():
         L.swr_launch_count.argtypes = [C.c_void_p]
         L.swr_scene_destroy.argtypes = [C.c_void_p]
         L.swr_set_option.argtypes = [C.c_void_p, C.c_char_p, C.c_double]
+        L.swr_get_option.argtypes = [C.c_void_p, C.c_char_p, C.POINTER(C.c_double)]
         L.swr_render.argtypes = [C.c_void_p, C.c_void_p, C.c_int64, C.c_uint32, C.c_void_p, C.c_void_p,
                                  C.c_void_p, C.c_void_p, C.c_void_p]
         L.swr_render_device.argtypes = [C.c_void_p, C.c_void_p, C.c_int64, C.c_uint32, C.c_void_p, C.c_void_p,
@@ -201,6 +202,11 @@ class Checkpoint:
 
     def set_option(self, key: str, value: float) -> None:
         _check(lib().swr_set_option(self._h, key.encode(), float(value)))
+
+    def get_option(self, key: str) -> float:
+        v = C.c_double(0.0)
+        _check(lib().swr_get_option(self._h, key.encode(), C.byref(v)))
+        return v.value
 
     def launch_count(self) -> int:
         return int(lib().swr_launch_count(self._h))
