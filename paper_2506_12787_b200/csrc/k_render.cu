@@ -630,6 +630,10 @@ __device__ __forceinline__ float2 shfl_f2(float2 v, int src)
 // 8-warp CTAs idle at the final barrier when a tile's few chunks split unevenly
 // (tools/build_variant.py sweeps: 8 warps x 4 CTAs 20.9 ms, 4 x 8 20.1-20.4 ms,
 // 2 x 16 21.8 ms per 1024 spectra at 50k; at 10k 5.43 -> 4.75 ms).
+#ifndef SWR_SWEEP_UNROLL
+#define SWR_SWEEP_UNROLL 1 // measured: 1 beats 2, 3, 4 (raster 20.6 -> 20.2 ms at 50k)
+#endif
+constexpr int kSweepUnroll = SWR_SWEEP_UNROLL; // sweeps unrolled per record pair
 #ifndef SWR_RASTER_MINB
 #define SWR_RASTER_MINB 4 // x 8 warps: resident warps per SM / 8
 #endif
@@ -718,7 +722,7 @@ __global__ void __launch_bounds__(32 * kRasterWarps, SWR_RASTER_MINB * 8 / kRast
             const uint32_t t_step = lane_on ? 8u * (uint32_t)rpi : 0u, c_step = lane_on ? 8u * (uint32_t)(rpi * T) : 0u;
             // sweeps in which this lane's row is inside the box
             const int nvalid = lane_on ? (int)(((uint32_t)(bx.y - rr0 + rpi) * mr) >> 12) : 0;
-#pragma unroll 2
+#pragma unroll kSweepUnroll
             for (int it = 0; it < loop; it++, tp += t_step, cp += c_step)
             {
                 float d_el, qc;
