@@ -10,3 +10,5 @@ B="python bench.py --steps 1 --warmup 3 --no-cpu-baseline --batch 256"
 timeout -s KILL 300 $B > gpurun_out/plain.log 2>&1 && \
 timeout -s KILL 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches.csv $B > gpurun_out/ncu_launch.log 2>&1
 echo done
+timeout -s KILL 600 ncu --set full --clock-control none --import-source on -k regex:"raster_kernel" -s 1 -c 1 -o gpurun_out/prof_raster $B > gpurun_out/ncu_raster.log 2>&1
+echo raster-ncu-done
