@@ -31,7 +31,8 @@
 // once heads X / Y have read the regions they reuse).
 //
 // Measured (one 256-position chunk, 50k Gaussians, tools/mlp_kernels_time.py):
-// 8.30 ms vs 8.65 ms for k_mlp_tc.cu. A clock64 timeline (tools/tc2_trace.py,
+// 8.30 ms vs 8.65 ms for k_mlp_tc.cu with 6 column groups; ~8.2 ms with 5 (33.0
+// ms per 1,024 spectra in bench.py). A clock64 timeline (tools/tc2_trace.py,
 // hooks build) shows ~2,500 cycles per layer step against 2,400 for the UMMAs
 // alone and ~4,000 cycles lost per super-tile boundary; the epilogue (40
 // 16-column conversions per step on 24 warps, ~1,900 cycles) is now the
