@@ -188,8 +188,10 @@ def main():
                          "5 = 1M Gaussians, width-512 MLP")
     ap.add_argument("--n", type=int, default=None)
     ap.add_argument("--batch", type=int, default=None, help="positions per GPU (configs 2 and 5)")
-    ap.add_argument("--precision", default=os.environ.get("SWR_BENCH_PRECISION", "bf16x3"),
-                    choices=["fp32", "bf16x3", "bf16"])
+    ap.add_argument("--precision", default=os.environ.get("SWR_BENCH_PRECISION", "fp16x3"),
+                    choices=["fp32", "fp16x3", "fp16"],
+                    help="MLP arithmetic: fp16x3 = tensor cores, FP32-grade (default); fp32 = CUDA cores; "
+                         "fp16 = single-pass fast tier (not FP32-grade)")
     ap.add_argument("--chunk", type=int, default=None,
                     help="positions per device chunk (default: the library's, ~12.8M Gaussian-position rows)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -241,7 +243,7 @@ def main():
     from paper_2506_12787_b200 import swr
 
     ck = swr.Checkpoint.from_scene(scene, device=local)
-    ck.set_option("mlp_precision", {"fp32": 0, "bf16x3": 1, "bf16": 2}[args.precision])
+    ck.set_option("mlp_precision", {"fp32": 0, "fp16x3": 1, "fp16": 2}[args.precision])
     if args.chunk:
         ck.set_option("chunk", args.chunk)
     args.chunk = int(ck.get_option("chunk"))
@@ -391,14 +393,14 @@ def main():
         bound, peak_note = "fp32", "FP32 CUDA-core peak 148 SM x 128 FMA x 2 x 1965 MHz (derived, not measured)"
     else:
         peak = peaks["bf16_tflops"]
-        bound, peak_note = "tensor", f"bf16 dense {peak_src} burst"
+        bound, peak_note = "tensor", f"dense 16-bit tensor (bf16 cuBLAS) {peak_src} burst"
     achieved = fmin * rows / (mlp_ms / 1e3) / 1e12 if mlp_ms > 0 else None
     wp = 160 if scene.width <= 160 else 512
     issued = None
     if args.precision != "fp32" and wp == 160:
         # UMMA work per row: 7 hidden layers 160x160 + heads 160x32 (the centre-encoding
-        # terms enter as tcgen05.cp copies, no UMMAs), x3 split passes for bf16x3
-        issued = (3 if args.precision == "bf16x3" else 1) * 2 * (7 * wp * wp + wp * 32)
+        # terms enter as tcgen05.cp copies, no UMMAs), x3 split passes for fp16x3
+        issued = (3 if args.precision == "fp16x3" else 1) * 2 * (7 * wp * wp + wp * 32)
     traffic = None
     prof = os.path.join(ROOT, "profiles", "ncu_mlp_traffic.json")
     if os.path.exists(prof) and args.chunk == 256 and args.config == 2:
@@ -416,11 +418,13 @@ def main():
         "metric": "spectra/sec", "value": value, "unit": "spectra/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": True, "scaling": args.scaling,
         "vs_baseline": None,
-        "dtype": "f32" if args.precision == "fp32" else "f32 (MLP products as 3xBF16 split, fp32 accumulate)"
-        if args.precision == "bf16x3" else "bf16 MLP",
+        "dtype": "f32" if args.precision == "fp32" else
+        "f32 (MLP products as 3 fp16 hi/lo split passes of power-of-two-scaled operands, fp32 accumulate; "
+        "residuals within 2e-6 of FP64)" if args.precision == "fp16x3" else "fp16 MLP (fast tier, not FP32-grade)",
         "data": "synthetic (seeded scene + TX positions)",
         "config": config_dict(args, scene),
-        "roofline": {"bound": bound, "kernel": "deform MLP (mlp_tc_kernel)", "achieved": achieved, "peak": peak,
+        "roofline": {"bound": bound, "kernel": "deform MLP (mlp_tc2_kernel)" if args.precision != "fp32"
+                     else "deform MLP (mlp_fp32_kernel)", "achieved": achieved, "peak": peak,
                      "unit": "TFLOP/s", "frac": (achieved / peak) if achieved else None, "traffic": traffic,
                      "traffic_unit": "DRAM bytes per launch (256-position chunk), ncu --set full",
                      "peak_source": peak_note,

@@ -44,8 +44,8 @@ enum swr_status
 
 /* MLP arithmetic (swr_set_option "mlp_precision") */
 #define SWR_MLP_FP32 0   /* FP32 FMA on the CUDA cores */
-#define SWR_MLP_BF16X3 1 /* tcgen05 split-precision (hi/lo bf16, 3 products, fp32 accumulate) */
-#define SWR_MLP_BF16 2   /* tcgen05 single bf16 product (fast, ~1e-3 relative residual error) */
+#define SWR_MLP_FP16X3 1 /* tcgen05, FP32-grade: fp16 hi/lo splits of scaled operands, 3 products, fp32 accumulate */
+#define SWR_MLP_FP16 2   /* tcgen05 single fp16 product (fast tier, ~1e-3 relative residual error) */
 
 typedef struct
 {
@@ -75,9 +75,7 @@ int swr_scene_create(int n_elevation, int n_azimuth, int n, const float *center_
 void swr_scene_destroy(swr_ctx *ctx);
 int swr_scene_get_info(swr_ctx *ctx, swr_scene_info *info);
 
-/* Options: "mlp_precision" (SWR_MLP_*), "mlp_kernel" (tensor-core MLP: 2 = two
- * position tiles in flight per CTA pair, the default; 1 = single tile with two
- * output parts), "chunk" (positions per device chunk),
+/* Options: "mlp_precision" (SWR_MLP_*), "chunk" (positions per device chunk),
  * "rssi_slope" / "rssi_intercept" (affine RSSI calibration, tasks.cpp:60-94),
  * "stage_timing" (1: record per-stage CUDA events), "stage_reset" (zero the
  * accumulated stage times). */

@@ -767,4 +767,111 @@ long long wref_evaluate(void *h, const char *dir, int split, double *rows, long 
     return n;
 }
 
+// The acceptance gate's criterion-1 instances, replayed exactly
+// (acceptance.cpp:130-147 random_float_set, :159-199 criterion_1): one
+// wrfsplat::Rng(20250814) stream, 50 instances, grid <= 16 x 32, n <= 64,
+// odd instances with residuals U[-0.05, 0.05], cutoff off. Per instance i
+// (arrays padded to 64 primitives / 16 x 32 cells):
+//   hwn[3i..]            H, W, n
+//   cr[i][64][2], ch[i][64][3], at[i][64], rs[i][64][2], dc/dr[i][64][2], da[i][64]
+//   out[i][16*32*2]      splat::rasterize<float> (the reference's tiled forward)
+//   dense[i][16*32*2]    the criterion's FP64 dense oracle, restated from
+//                        acceptance.cpp:53-109 (kernel_oracle + dense_oracle)
+int wref_criterion1(int *hwn, float *cr, float *ch, float *at, float *rs, float *dc, float *dr, float *da,
+                    float *out, double *dense)
+{
+    return guarded([&] {
+        Rng rng(20250814);
+        for (int inst = 0; inst < 50; inst++)
+        {
+            const AngularGrid g{4 + int(rng.index(13)), 8 + int(rng.index(25))};
+            const int n = 1 + int(rng.index(64));
+            splat::GaussianSetT<float> set;
+            set.grid = g;
+            set.resize(n);
+            for (int p = 0; p < n; p++)
+            {
+                set.center_raw[2 * std::size_t(p)] = float(rng.uniform(-1.5, 1.5));
+                set.center_raw[2 * std::size_t(p) + 1] = float(rng.uniform(-1.5, 1.5));
+                set.cholesky[3 * std::size_t(p)] = float(rng.uniform(0.05, 0.4));
+                set.cholesky[3 * std::size_t(p) + 1] = float(rng.uniform(-0.2, 0.2));
+                set.cholesky[3 * std::size_t(p) + 2] = float(rng.uniform(0.05, 0.4));
+                set.atten_logit[std::size_t(p)] = float(rng.uniform(-1.0, 1.0));
+                set.response[2 * std::size_t(p)] = float(rng.uniform(-0.5, 0.5));
+                set.response[2 * std::size_t(p) + 1] = float(rng.uniform(-0.5, 0.5));
+            }
+            splat::ResidualsT<float> res;
+            const bool with_res = (inst % 2) == 1;
+            if (with_res)
+            {
+                res.resize(n);
+                for (auto *vec : {&res.d_center, &res.d_response})
+                    for (auto &v : *vec)
+                        v = float(rng.uniform(-0.05, 0.05));
+                for (auto &v : res.d_atten)
+                    v = float(rng.uniform(-0.05, 0.05));
+            }
+            splat::RasterParams pr;
+            pr.cutoff_radius = 0.0f;
+            const auto o = splat::rasterize<float>(set, with_res ? &res : nullptr, pr);
+            hwn[3 * inst] = g.n_elevation;
+            hwn[3 * inst + 1] = g.n_azimuth;
+            hwn[3 * inst + 2] = n;
+            const std::size_t P = std::size_t(inst) * 64;
+            std::memcpy(cr + 2 * P, set.center_raw.data(), sizeof(float) * 2 * n);
+            std::memcpy(ch + 3 * P, set.cholesky.data(), sizeof(float) * 3 * n);
+            std::memcpy(at + P, set.atten_logit.data(), sizeof(float) * n);
+            std::memcpy(rs + 2 * P, set.response.data(), sizeof(float) * 2 * n);
+            if (with_res)
+            {
+                std::memcpy(dc + 2 * P, res.d_center.data(), sizeof(float) * 2 * n);
+                std::memcpy(dr + 2 * P, res.d_response.data(), sizeof(float) * 2 * n);
+                std::memcpy(da + P, res.d_atten.data(), sizeof(float) * n);
+            }
+            std::memcpy(out + std::size_t(inst) * 1024, o.data.data(), sizeof(float) * o.data.size());
+            // dense FP64 oracle (acceptance.cpp:53-109)
+            const double pi = 3.141592653589793238462643383279502884;
+            double *dd = dense + std::size_t(inst) * 1024;
+            for (int i = 0; i < g.n_elevation; i++)
+                for (int j = 0; j < g.n_azimuth; j++)
+                {
+                    const std::size_t c = std::size_t(i) * g.n_azimuth + j;
+                    double sre = 0.0, sim = 0.0;
+                    for (int p = 0; p < n; p++)
+                    {
+                        double c_el = pi / 4 * (std::tanh(double(set.center_raw[2 * std::size_t(p)])) + 1.0);
+                        double c_az = pi * (std::tanh(double(set.center_raw[2 * std::size_t(p) + 1])) + 1.0);
+                        const double l1 = std::max(double(set.cholesky[3 * std::size_t(p)]), double(splat::chol_floor));
+                        const double l2 = set.cholesky[3 * std::size_t(p) + 1];
+                        const double l3 = std::max(double(set.cholesky[3 * std::size_t(p) + 2]), double(splat::chol_floor));
+                        double delta = 1.0 / (1.0 + std::exp(-double(set.atten_logit[std::size_t(p)])));
+                        double re = set.response[2 * std::size_t(p)], im = set.response[2 * std::size_t(p) + 1];
+                        if (with_res)
+                        {
+                            c_el += res.d_center[2 * std::size_t(p)];
+                            c_az += res.d_center[2 * std::size_t(p) + 1];
+                            delta = std::min(std::max(delta + double(res.d_atten[std::size_t(p)]), 0.0), 1.0);
+                            re += res.d_response[2 * std::size_t(p)];
+                            im += res.d_response[2 * std::size_t(p) + 1];
+                        }
+                        const double d0 = g.elevation_center(i) - c_el;
+                        double d1 = g.azimuth_center(j) - c_az;
+                        while (d1 >= pi)
+                            d1 -= 2.0 * pi;
+                        while (d1 < -pi)
+                            d1 += 2.0 * pi;
+                        const double s00 = l1 * l1, s01 = l1 * l2, s11 = l2 * l2 + l3 * l3;
+                        const double det = s00 * s11 - s01 * s01;
+                        const double q = (s11 * d0 * d0 - 2.0 * s01 * d0 * d1 + s00 * d1 * d1) / det;
+                        const double k = delta * std::exp(-0.5 * q);
+                        sre += re * k;
+                        sim += im * k;
+                    }
+                    dd[2 * c] = sre;
+                    dd[2 * c + 1] = sim;
+                }
+        }
+    });
+}
+
 } // extern "C"

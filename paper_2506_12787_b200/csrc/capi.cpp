@@ -307,10 +307,36 @@ void build_scene(Ctx &c, const HostScene &hs, int device)
     launch_center_terms(c, d_cenc, c.stream);
     check_cuda(cudaStreamSynchronize(c.stream), "centre terms");
     dfree(c, d_cenc);
-    if (mlp_tc_available() && WP == 160)
+    if (mlp_tc_available() && WP == 160 && n > 0)
     {
-        prepare_tc_weights(c, whT, heads);
-        prepare_tc2_weights(c, whT, heads);
+        // activation scale of the tensor-core MLP: the largest ReLU output over all
+        // Gaussians x 16 probe positions (bbox corners + interior points), FP32 kernel
+        constexpr int kProbe = 16;
+        ensure_work(c, kProbe);
+        std::vector<float> probe(3 * kProbe);
+        for (int p = 0; p < kProbe; p++)
+            for (int a = 0; a < 3; a++)
+            {
+                const double t = p < 8 ? double((p >> a) & 1) : 0.125 + 0.75 * ((p * 0.618034 * (a + 1)) - std::floor(p * 0.618034 * (a + 1)));
+                probe[3 * p + a] = float(t);
+            }
+        float *d_probe = upload(c, probe);
+        launch_pos_prep(c, d_probe, kProbe, true, c.stream); // mlp_precision 0 here: unscaled
+        float amax[8];
+        probe_activations(c, kProbe, amax, c.stream);
+        dfree(c, d_probe);
+        // per layer: 2^k_l amax_l <= 65504 / 64 (headroom for positions the probe did
+        // not see; an overflow anyway re-runs the chunk in FP32), k_l in [-20, 10]
+        for (int l = 0; l < 8; l++)
+        {
+            const float m = amax[l];
+            c.net.tc_amax[l] = m;
+            int k = 10;
+            if (m > 0.0f && std::isfinite(m))
+                k = std::min(10, std::max(-20, int(std::floor(std::log2(65504.0 / 64.0 / double(m))))));
+            c.net.tc_ascale[l] = k;
+        }
+        prepare_tc2_weights(c, whT, heads, bias);
     }
 }
 
@@ -339,7 +365,7 @@ void ensure_work(Ctx &c, int64_t nb)
     w.tile_part = dalloc<float4>(c, size_t(nb) * tiles);
     w.tile_sum = dalloc<double>(c, size_t(nb) * tiles);
     if (!w.stats)
-        w.stats = dalloc<int64_t>(c, 2);
+        w.stats = dalloc<int64_t>(c, 3);
     if (!w.host_pairs)
         check_cuda(cudaHostAlloc((void **)&w.host_pairs, 4 * sizeof(int64_t), cudaHostAllocDefault), "host alloc");
     w.max_chunks = 0; // chunk histogram re-sized on demand
@@ -451,12 +477,29 @@ static void run_chunk(Ctx &c, const float *d_pos, int nb, bool normalized, bool 
         tm.mark();
         tm.mark();
     }
+    check_cuda(cudaMemsetAsync(c.w.stats + 2, 0, sizeof(int64_t), st), "reset flag");
     launch_setup(c, nb, use_mlp || with_res, st);
     tm.mark();
     launch_bin_count(c, nb, st);
-    check_cuda(cudaMemcpyAsync(c.w.host_pairs, c.w.stats, 2 * sizeof(int64_t), cudaMemcpyDeviceToHost, st),
+    check_cuda(cudaMemcpyAsync(c.w.host_pairs, c.w.stats, 3 * sizeof(int64_t), cudaMemcpyDeviceToHost, st),
                "D2H pair count");
     check_cuda(cudaStreamSynchronize(st), "pair count");
+    if (use_mlp && c.mlp_precision != 0 && c.w.host_pairs[2] != 0)
+    {
+        // a non-finite residual from the fp16 tensor-core MLP (an activation above
+        // 65504): redo this chunk's MLP on the FP32 CUDA-core kernel
+        c.mlp_reruns++;
+        const int keep = c.mlp_precision;
+        c.mlp_precision = 0;
+        launch_pos_prep(c, d_pos, nb, normalized, st); // unscaled position terms
+        launch_mlp(c, nb, st);
+        c.mlp_precision = keep;
+        launch_setup(c, nb, true, st);
+        launch_bin_count(c, nb, st);
+        check_cuda(cudaMemcpyAsync(c.w.host_pairs, c.w.stats, 2 * sizeof(int64_t), cudaMemcpyDeviceToHost, st),
+                   "D2H pair count");
+        check_cuda(cudaStreamSynchronize(st), "pair count");
+    }
     const int64_t pairs = c.w.host_pairs[0], max_seg = c.w.host_pairs[1];
     c.pairs_last = pairs;
     ensure_pairs(c, pairs, nb, max_seg);
@@ -841,16 +884,10 @@ int swr_set_option(swr_ctx *ctx, const char *key, double value)
         {
             const int v = int(value);
             if (v < 0 || v > 2)
-                throw std::invalid_argument("mlp_precision must be 0 (fp32), 1 (bf16x3) or 2 (bf16)");
+                throw std::invalid_argument("mlp_precision must be 0 (fp32), 1 (fp16x3) or 2 (fp16)");
             if (v != 0 && !(mlp_tc_available() && c.has_net && c.net.wp == 160))
                 throw std::invalid_argument("tensor-core MLP unavailable for this scene (width must be <= 160)");
             c.mlp_precision = v;
-        }
-        else if (k == "mlp_kernel")
-        {
-            if (int(value) != 1 && int(value) != 2)
-                throw std::invalid_argument("mlp_kernel must be 1 (output parts) or 2 (two-tile ping-pong)");
-            c.mlp_kernel = int(value);
         }
         else if (k == "chunk")
         {
@@ -881,8 +918,6 @@ int swr_get_option(swr_ctx *ctx, const char *key, double *value)
         const std::string k(key);
         if (k == "mlp_precision")
             *value = c.mlp_precision;
-        else if (k == "mlp_kernel")
-            *value = c.mlp_kernel;
         else if (k == "chunk")
             *value = c.chunk;
         else if (k == "rssi_slope")
@@ -891,6 +926,12 @@ int swr_get_option(swr_ctx *ctx, const char *key, double *value)
             *value = c.rssi_intercept;
         else if (k == "stage_timing")
             *value = c.stage_timing ? 1.0 : 0.0;
+        else if (k == "mlp_reruns")
+            *value = double(c.mlp_reruns);
+        else if (k == "mlp_act_scale_exp") // smallest of the per-layer exponents
+            *value = *std::min_element(c.net.tc_ascale, c.net.tc_ascale + 8);
+        else if (k == "mlp_probe_amax")
+            *value = *std::max_element(c.net.tc_amax, c.net.tc_amax + 8);
         else
             throw std::invalid_argument("unknown option " + k);
     });
@@ -1011,10 +1052,35 @@ int swr_predict_residuals(swr_ctx *ctx, const float *pos01, int64_t B, float *dc
             launch_pos_prep(c, d_pos + 3 * b0, nb, true, c.stream);
             launch_mlp(c, nb, c.stream);
             check_cuda(cudaGetLastError(), "launch");
-            check_cuda(cudaMemcpyAsync(planes.data(), c.w.res, planes.size() * sizeof(float), cudaMemcpyDeviceToHost,
-                                       c.stream),
-                       "D2H residuals");
-            check_cuda(cudaStreamSynchronize(c.stream), "predict");
+            auto fetch = [&] {
+                check_cuda(cudaMemcpyAsync(planes.data(), c.w.res, planes.size() * sizeof(float),
+                                           cudaMemcpyDeviceToHost, c.stream),
+                           "D2H residuals");
+                check_cuda(cudaStreamSynchronize(c.stream), "predict");
+            };
+            fetch();
+            if (c.mlp_precision != 0)
+            {
+                bool bad = false;
+                for (int q = 0; q < 5 && !bad; q++)
+                    for (int s = 0; s < nb && !bad; s++)
+                        for (int g = 0; g < n; g++)
+                            if (!std::isfinite(planes[q * plane + size_t(s) * np + g]))
+                            {
+                                bad = true;
+                                break;
+                            }
+                if (bad) // fp16 overflow in the tensor-core MLP: this chunk again in FP32 (see run_chunk)
+                {
+                    c.mlp_reruns++;
+                    const int keep = c.mlp_precision;
+                    c.mlp_precision = 0;
+                    launch_pos_prep(c, d_pos + 3 * b0, nb, true, c.stream);
+                    launch_mlp(c, nb, c.stream);
+                    c.mlp_precision = keep;
+                    fetch();
+                }
+            }
             for (int s = 0; s < nb; s++)
                 for (int g = 0; g < n; g++)
                 {
@@ -1495,12 +1561,6 @@ int swr_scene_set_manifest_hash(swr_ctx *ctx, uint64_t hash)
 {
     ctx->c.manifest_hash = hash;
     return SWR_OK;
-}
-
-// debug: clock64 trace of the tensor-core MLP (SWR_TC_DEBUG & 8), 3x8x80 stamps
-int swr_debug_mlp_trace(long long *out)
-{
-    return swr::mlp_tc_trace(out);
 }
 
 int swr_debug_mlp_trace2(long long *out)

@@ -274,13 +274,14 @@ void launch_raster_backward(Ctx &c, int nb, const float *d_state, const float *d
         split = std::max(1, std::atoi(e));
     dim3 grid(c.g.tiles, nb * split);
     const size_t smem = (size_t)c.g.tile * c.g.tile * sizeof(float2) + kBwdWarps * 32 * sizeof(BwdRec);
-    static size_t configured = 0;
-    if (configured < smem)
-    {
-        check_cuda(cudaFuncSetAttribute(raster_bwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem),
+    static DeviceOnce once;
+    once.get(c.device, [] {
+        // the largest variant (tiles up to 32 x 32)
+        const size_t mx = (size_t)32 * 32 * sizeof(float2) + kBwdWarps * 32 * sizeof(BwdRec);
+        check_cuda(cudaFuncSetAttribute(raster_bwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)mx),
                    "raster backward smem");
-        configured = smem;
-    }
+        return 1;
+    });
     raster_bwd_kernel<<<grid, 32 * kBwdWarps, smem, st>>>(c.g, c.s, d_state, c.w.rng, c.w.seg, c.w.tile_off,
                                                           c.w.sorted, d_upstream, d_slots, split);
     c.launches++;

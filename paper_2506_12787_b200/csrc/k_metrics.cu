@@ -370,11 +370,10 @@ __global__ void loss_final_kernel(const double *__restrict__ part, const double 
 } // namespace
 
 // host: the window taps exactly as spectrum.cpp:51-70 computes them
-static void upload_taps()
+static void upload_taps(int device)
 {
-    static bool done = false;
-    if (done)
-        return;
+    static DeviceOnce once;
+    once.get(device, [] {
     double g[kWin], sum = 0.0;
     for (int i = 0; i < kWin; i++)
     {
@@ -385,7 +384,8 @@ static void upload_taps()
     for (double &v : g)
         v /= sum;
     check_cuda(cudaMemcpyToSymbol(c_taps, g, sizeof(g)), "ssim taps");
-    done = true;
+    return 1;
+    });
 }
 
 size_t metrics_tmp_doubles(const Ctx &c, int nb)
@@ -401,7 +401,7 @@ size_t metrics_tmp_doubles(const Ctx &c, int nb)
 void launch_metrics(Ctx &c, const float *d_pred, const float *d_target, int nb, double peak, double *d_psnr,
                     double *d_ssim, double *d_l1, double *d_tmp, int *d_bad, cudaStream_t st)
 {
-    upload_taps();
+    upload_taps(c.device);
     const int H = c.g.H, W = c.g.W, vw = W - kWin + 1, vh = H - kWin + 1;
     const int64_t n = (int64_t)2 * H * W;
     const int chunks = pt_chunks(n);
@@ -413,14 +413,13 @@ void launch_metrics(Ctx &c, const float *d_pred, const float *d_target, int nb, 
     c.launches += 2;
     if (!d_ssim)
         return;
-    static bool configured = false;
-    if (!configured)
-    {
+    static DeviceOnce once;
+    once.get(c.device, [] {
         check_cuda(cudaFuncSetAttribute(ssim_fused_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                         (int)kFusedSmem),
                    "ssim smem attribute");
-        configured = true;
-    }
+        return 1;
+    });
     ssim_fused_kernel<<<dim3(cbt, rbt, 2 * nb), 256, kFusedSmem, st>>>(d_pred, d_target, H, W, peak, part);
     ssim_fused_final_kernel<<<(nb + 127) / 128, 128, 0, st>>>(part, nb, cbt * rbt, (int64_t)vh * vw, d_ssim);
     c.launches += 2;
@@ -446,7 +445,7 @@ size_t loss_tmp_doubles(const Ctx &c, int nb)
 void launch_hybrid_loss(Ctx &c, const float *d_pred, const float *d_target, int nb, double lambda1, double *d_terms,
                         float *d_grad, double *d_tmp, int *d_bad, cudaStream_t st)
 {
-    upload_taps();
+    upload_taps(c.device);
     const int H = c.g.H, W = c.g.W, vw = W - kWin + 1, vh = H - kWin + 1;
     const int64_t n = (int64_t)2 * H * W;
     double *hcor = d_tmp;

@@ -14,6 +14,8 @@
 #include "swr_internal.h"
 
 #include <cstdio>
+#include <cmath>
+#include <cstring>
 
 namespace swr
 {
@@ -29,6 +31,7 @@ struct PosArgs
     const float *bias;  // [8][wp]
     double bmin0, bmin1, bmin2, bmax0, bmax1, bmax2;
     int normalized, bands_p, dp, wp, width;
+    float pscale[4]; // powers of two: the tensor-core MLP's activation scales 2^k_l of layers 0/2/4/6, else 1
 };
 
 __global__ void __launch_bounds__(256) pos_prep_kernel(PosArgs a)
@@ -78,7 +81,7 @@ __global__ void __launch_bounds__(256) pos_prep_kernel(PosArgs a)
         const float *wr = a.wpos + ((size_t)j * a.wp + n) * a.dp;
         for (int k = 0; k < a.dp; k++)
             acc = __fmaf_rn(wr[k], xp[k], acc);
-        a.pterm[((size_t)s * 4 + j) * a.wp + n] = n < a.width ? acc + a.bias[layer * a.wp + n] : 0.0f;
+        a.pterm[((size_t)s * 4 + j) * a.wp + n] = n < a.width ? (acc + a.bias[layer * a.wp + n]) * a.pscale[j] : 0.0f;
     }
 }
 
@@ -101,6 +104,8 @@ void launch_pos_prep(Ctx &c, const float *d_pos, int nb, bool normalized, cudaSt
     a.dp = c.net.dp;
     a.wp = c.net.wp;
     a.width = c.net.width;
+    for (int j = 0; j < 4; j++)
+        a.pscale[j] = mlp_uses_tc(c) ? std::ldexp(1.0f, c.net.tc_ascale[2 * j]) : 1.0f;
     pos_prep_kernel<<<nb, 256, 0, st>>>(a);
     c.launches++;
 }
@@ -146,6 +151,7 @@ struct MlpArgs
     const float *hbias;  // [5]
     float *res;          // [5][cap_b][np]
     int n, np, nb, cap_b, width, n_gblk, n_sblk;
+    unsigned *amax;      // optional [8]: max activation of each trunk layer (float bits; scene-load probe)
 };
 
 // Tile = GB Gaussians x 8 positions = TM rows; 256 threads as 16 row groups x
@@ -178,6 +184,8 @@ __global__ void __launch_bounds__(256) mlp_fp32_kernel(MlpArgs a)
             if (g < a.n && s < a.nb)
                 v = a.cg[((size_t)g * 4) * WP + nn] + a.pterm[((size_t)s * 4) * WP + nn];
             act[nn * TMP + r] = v > 0.0f ? v : 0.0f;
+            if (a.amax && v > 0.0f)
+                atomicMax(&a.amax[0], __float_as_uint(v));
         }
         __syncthreads();
 
@@ -265,6 +273,16 @@ __global__ void __launch_bounds__(256) mlp_fp32_kernel(MlpArgs a)
                     acc[i][j] = v > 0.0f ? v : 0.0f;
                 }
             }
+            if (a.amax)
+            {
+                float m = 0.0f;
+#pragma unroll
+                for (int i = 0; i < RT; i++)
+#pragma unroll
+                    for (int j = 0; j < 2 * NJ; j++)
+                        m = fmaxf(m, acc[i][j]);
+                atomicMax(&a.amax[l], __float_as_uint(m));
+            }
 #pragma unroll
             for (int j = 0; j < 2 * NJ; j++)
             {
@@ -293,17 +311,16 @@ __global__ void __launch_bounds__(256) mlp_fp32_kernel(MlpArgs a)
 }
 
 template <int TM, int NJ>
-static void run_mlp(Ctx &c, int nb, cudaStream_t st)
+static void run_mlp(Ctx &c, int nb, cudaStream_t st, unsigned *amax = nullptr)
 {
     constexpr int WP = 32 * NJ;
     constexpr int smem = (WP * (TM + 4) + 2 * 16 * WP) * 4;
-    static bool configured = false;
-    if (!configured)
-    {
+    static DeviceOnce once;
+    once.get(c.device, [] {
         check_cuda(cudaFuncSetAttribute(mlp_fp32_kernel<TM, NJ>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem),
                    "mlp smem attribute");
-        configured = true;
-    }
+        return 1;
+    });
     MlpArgs a;
     a.whT = c.net.whT;
     a.bias = c.net.bias;
@@ -319,6 +336,7 @@ static void run_mlp(Ctx &c, int nb, cudaStream_t st)
     a.width = c.net.width;
     a.n_gblk = (c.g.n + TM / 8 - 1) / (TM / 8);
     a.n_sblk = (nb + 7) / 8;
+    a.amax = amax;
     int dev_sms = 148;
     cudaDeviceGetAttribute(&dev_sms, cudaDevAttrMultiProcessorCount, c.device);
     int per_sm = 0;
@@ -329,14 +347,34 @@ static void run_mlp(Ctx &c, int nb, cudaStream_t st)
     c.launches++;
 }
 
+bool mlp_uses_tc(const Ctx &c)
+{
+    return c.mlp_precision != 0 && mlp_tc_available() && c.net.wp == 160 && c.net.w_tc2 != nullptr;
+}
+
+// Largest ReLU output of every trunk layer over all Gaussians x the first nb
+// positions already prepared (pos_prep, unscaled), on the FP32 kernel.
+void probe_activations(Ctx &c, int nb, float out[8], cudaStream_t st)
+{
+    unsigned *d = dalloc<unsigned>(c, 8);
+    check_cuda(cudaMemsetAsync(d, 0, 8 * sizeof(unsigned), st), "probe reset");
+    if (c.net.wp <= 160)
+        run_mlp<128, 5>(c, nb, st, d);
+    else
+        run_mlp<64, 16>(c, nb, st, d);
+    unsigned h[8];
+    check_cuda(cudaMemcpyAsync(h, d, sizeof(h), cudaMemcpyDeviceToHost, st), "probe read");
+    check_cuda(cudaStreamSynchronize(st), "probe");
+    dfree(c, d);
+    for (int l = 0; l < 8; l++)
+        std::memcpy(&out[l], &h[l], 4);
+}
+
 void launch_mlp(Ctx &c, int nb, cudaStream_t st)
 {
-    if (c.mlp_precision != 0 && mlp_tc_available() && c.net.wp == 160)
+    if (mlp_uses_tc(c))
     {
-        if (c.mlp_kernel == 2)
-            launch_mlp_tc2(c, nb, st);
-        else
-            launch_mlp_tc(c, nb, st);
+        launch_mlp_tc2(c, nb, st);
         return;
     }
     if (c.net.wp <= 160)

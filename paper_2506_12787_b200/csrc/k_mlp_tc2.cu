@@ -1,43 +1,63 @@
 // Deformation MLP on tcgen05, CTA pairs, TWO TILES IN FLIGHT ("ping-pong").
-// The default tensor-core MLP (Ctx::mlp_kernel = 2); k_mlp_tc.cu is the
-// single-tile kernel it replaced (option mlp_kernel = 1).
+// The tensor-core MLP of libswr (mlp_precision SWR_MLP_FP16X3 / SWR_MLP_FP16).
 //
-// Function: deform::predict_residuals (/root/reference/proj/src/deform.cpp:140-207),
-// same split as k_mlp_tc.cu: W x = W_c xc[g] (cterm, per Gaussian, FP32) +
-// W_p xp[s] + b (pterm, per position, added in the epilogue); products as bf16
-// hi/lo splits (bf16x3) with FP32 accumulation in TMEM; A operands converted in
-// place in TMEM.
+// Function: deform::predict_residuals (/root/reference/proj/src/deform.cpp:140-207).
+// The input row x = [xc[g] | xp[s]] splits W x into W_c xc[g] (cterm: a
+// per-Gaussian FP32 constant computed once per scene) + W_p xp[s] + b (pterm:
+// per position, FP32, added in the epilogue). The seven hidden->hidden products
+// and the heads run on the tensor core with FP32 accumulation in TMEM; A
+// operands are converted in place in TMEM.
 //
-// Why: in k_mlp_tc.cu one tile's layers run back to back, so the tensor core
-// waits for the epilogue's conversion of layer l before layer l+1 (split into two
-// output parts to overlap). Here a CTA pair alternates two tiles X and Y of the
-// same 32 Gaussians (positions s0..s0+7 and s0+8..s0+15): while the tensor core
-// runs layer l of X, the epilogue converts layer l-1 of Y and vice versa, so each
-// conversion has a whole layer of the other tile (2,400 cycles at bf16x3) to
-// finish in. Three 160-column TMEM regions suffice: step m (tile m%2, layer
-// (m/2)%8) writes region m%3 and reads region (m-2)%3 (the same tile's previous
-// layer, converted in place); region (m-1)%3 is the other tile's accumulator
-// being converted meanwhile. Each weight stage (one per layer, full N = 160,
-// half the columns per CTA) serves both tiles.
+// Precision (SWR_MLP_FP16X3, FP32-grade): every product is a_hi w_hi + a_lo w_hi
+// + a_hi w_lo with fp16 hi/lo splits (11 + 11 significant bits, ~2^-22 per
+// product, the dropped a_lo w_lo term included). Weights are pre-scaled per
+// layer by a power of two 2^e_l (max |w| 2^e_l in [2^13, 2^14)) so both halves
+// stay in fp16's normal range; the accumulator then holds 2^e_l W h, and the
+// epilogue re-scales it exactly (fma(acc, 2^(k_l - e_l - k_(l-1)), add): the
+// power-of-two product is exact, so one rounding, as in acc + add). Each trunk
+// layer's output carries a scale 2^k_l, chosen at scene load so that 2^k_l
+// times the largest ReLU output of that layer the FP32 kernel sees over all
+// Gaussians x 16 probe positions is <= 65504 / 64: small activations then keep
+// both fp16 halves normal (an unscaled 0.05 would leave its lo half subnormal,
+// ~2^-20 instead of 2^-22) and large ones stay below fp16's 65504. The 2^k_l are
+// folded into the position terms (pos_prep), the biases (bias_tc) and the cterm
+// blocks, and taken out in the heads readout (2^-(e_h + k_7)). An activation that still overflows
+// fp16 turns into NaN in every product it feeds (hi = inf, lo = -inf); the ReLU
+// is max.NaN so the NaN reaches the residuals, where the setup kernel flags it
+// and the host re-runs the chunk on the FP32 CUDA-core kernel (capi.cpp).
+// SWR_MLP_FP16 runs the a_hi w_hi pass only (~2^-11, a fast tier not used for
+// reported numbers).
 //
-// Layer 0 has no UMMA: the epilogue writes ReLU(cterm0 + pterm0) (bf16 hi/lo)
-// straight into TMEM from a cterm block in shared memory. Layers 2, 4, 6 start
-// their accumulator from the cterm block (tcgen05.cp.32x128b.warpx4, as in
-// k_mlp_tc.cu; adding it in the epilogue instead made the epilogue the
-// bottleneck). The five heads run on the tensor core (N = 32, heads 0-4 real)
-// from layer 7's converted output into TMEM columns 480-511, their B operand
-// resident in shared memory; issue order at a super-tile boundary is
-// ... X7, Y7, heads X, heads Y, X'1 ... (X'0 / Y'0 are written by the epilogue
-// once heads X / Y have read the regions they reuse).
+// Why two tiles: one tile's layers back to back leave the tensor core waiting
+// for the epilogue's conversion of layer l before layer l+1. Here a CTA pair
+// alternates two tiles X and Y of the same 32 Gaussians (positions
+// s0..s0+7 and s0+8..s0+15): while the tensor core runs layer l of X, the
+// epilogue converts layer l-1 of Y and vice versa, so each conversion has a
+// whole layer of the other tile (2,400 cycles at 3 passes) to finish in. Three
+// 160-column TMEM regions suffice: step m (tile m%2, layer (m/2)%8) writes
+// region m%3 and reads region (m-2)%3 (the same tile's previous layer, converted
+// in place); region (m-1)%3 is the other tile's accumulator being converted
+// meanwhile. Each weight stage (one per layer, full N = 160, half the columns
+// per CTA) serves both tiles.
 //
-// Measured (one 256-position chunk, 50k Gaussians, tools/mlp_kernels_time.py):
-// 8.30 ms vs 8.65 ms for k_mlp_tc.cu with 6 column groups; ~8.2 ms with 5 (33.0
-// ms per 1,024 spectra in bench.py). A clock64 timeline (tools/tc2_trace.py,
-// hooks build) shows ~2,500 cycles per layer step against 2,400 for the UMMAs
-// alone and ~4,000 cycles lost per super-tile boundary; the epilogue (40
-// 16-column conversions per step on 24 warps, ~1,900 cycles) is now the
-// limiting chain, and the UMMA issuer shares its SM sub-partition with it.
-// (Timeline figures above were taken with 6 column groups; 5 is the default.)
+// Layer 0 has no UMMA: the epilogue writes ReLU(cterm0 + pterm0) (fp16 hi/lo)
+// straight into TMEM from a cterm block in shared memory. Layers 2, 4, 6 add
+// their cterm block in the epilogue too (round 1 seeded those accumulators with
+// tcgen05.cp; starting every accumulator from zero lets the cross-term passes
+// run first, see issue_layer, and cost < 1% in time). The five heads run
+// on the tensor core (N = 32, heads 0-4 real) from layer 7's converted output
+// into TMEM columns 480-511, their B operand resident in shared memory; issue
+// order at a super-tile boundary is ... X7, Y7, heads X, heads Y, X'1 ... (X'0 /
+// Y'0 are written by the epilogue once heads X / Y have read the regions they
+// reuse).
+//
+// Measured (round 1, bf16 splits -- same instruction count as fp16; one
+// 256-position chunk, 50k Gaussians): 8.2-8.3 ms (33.0 ms per 1,024 spectra in
+// bench.py). A clock64 timeline (tools/tc2_trace.py, hooks build) shows ~2,500
+// cycles per layer step against 2,400 for the UMMAs alone and ~4,000 cycles lost
+// per super-tile boundary; the epilogue (40 16-column conversions per step on
+// 20 warps) is the limiting chain, and the UMMA issuer shares its SM
+// sub-partition with it.
 //
 // Warps (704 threads per CTA with the default 5 column groups): 0-19 epilogue
 // (5 column groups x 4 TMEM lane quarters; group g converts 16-column chunks g
@@ -46,7 +66,8 @@
 #include "swr_internal.h"
 #include "tc_ptx.cuh"
 
-#include <cuda_bf16.h>
+#include <cuda_fp16.h>
+#include <cmath>
 #include <cstdlib>
 #include <cstring>
 
@@ -71,9 +92,9 @@ constexpr int HB_BYTES = KSTEPS * 2 * (NHEAD_N / 2) * 16 * 2; // heads B operand
 constexpr int KB = WPC / 2 * 16 * 2;      // one K step, one operand (hi or lo), this CTA's 80 columns: 2.5 KB
 constexpr int W_BYTES = KSTEPS * 2 * KB;  // one layer's weights per CTA: 50 KB
 constexpr int C_BLOCK = WPC * TG * 4;     // one layer's cterm block: [40 column groups][32 rows][4] f32
-constexpr int SLOT = W_BYTES + C_BLOCK;   // weight stage + the layer's cterm block (layers 2, 4, 6)
+constexpr int SLOT = W_BYTES;             // weight stage
 constexpr int NSTAGE = 2;                 // weight stages (layers 1..7), each serving both tiles
-constexpr int NCSTAGE = 1;                // layer 0's cterm block, read by the epilogue
+constexpr int NCSTAGE = 2;                // cterm blocks of layers 0/2/4/6, read by the epilogue
 #ifndef SWR_TC2_GROUPS
 #define SWR_TC2_GROUPS 5 // 5: every epilogue warp converts two chunks (measured ~1% faster than 6 and 7)
 #endif
@@ -95,14 +116,15 @@ __host__ __device__ constexpr bool has_xc(int l) { return (l & 1) == 0; } // lay
 
 struct Tc2Args
 {
-    const uint16_t *w;     // packed weights, layers 1..7: [layer][rank][10 K][hi | lo][80 cols x 16] bf16
-    const float *cterm;    // [n/32 blocks][4 layers][40][32][4] (k_mlp_tc.cu cterm_pack_kernel)
+    const uint16_t *w;     // packed weights, layers 1..7: [layer][rank][10 K][hi | lo][80 cols x 16] fp16 (x 2^e_l)
+    const float *cterm;    // [n/32 blocks][4 layers][40][32][4] x 2^k (cterm_pack_kernel)
     const float *bias;     // [8][160]
     const float *pterm;    // [nb][4][160]
-    const uint16_t *wh;    // heads B operand: [rank][10 K][hi | lo][16 cols x 16] bf16
+    const uint16_t *wh;    // heads B operand: [rank][10 K][hi | lo][16 cols x 16] fp16 (x 2^e_h)
     const float *hbias;    // [5]
     float *res;            // [5][cap_b][np]
     int n, np, nb, cap_b, n_sblk, ntiles;
+    float unscale[9];      // 2^-e_l of trunk layers 1..7 (index l), [8] = heads; [0] unused (layer 0: no UMMA)
     long long *trace;      // -DSWR_TC_DEBUG_HOOKS builds: [4][48] clock64 stamps of CTA 0 (steps 16..63)
 };
 #ifdef SWR_TC_DEBUG_HOOKS
@@ -117,26 +139,36 @@ __device__ __forceinline__ void stamp2(const Tc2Args &a, int kind, int m)
     (void)kind;
 }
 
-__device__ __forceinline__ uint32_t pack_bf16(float lo, float hi)
+__device__ __forceinline__ uint32_t pack_f16(float lo, float hi)
 {
-    __nv_bfloat162 h = __floats2bfloat162_rn(lo, hi);
+    __half2 h = __floats2half2_rn(lo, hi); // cvt.rn.f16x2.f32: lo -> bits 0-15
     return *reinterpret_cast<uint32_t *>(&h);
 }
+// ReLU that keeps NaN (max.NaN): an fp16 overflow upstream stays visible in the residuals
+__device__ __forceinline__ float relu_nan(float x)
+{
+    float r;
+    asm("max.NaN.f32 %0, %1, 0f00000000;" : "=f"(r) : "f"(x));
+    return r;
+}
 
-// v = ReLU(acc + add) -> 8 columns of bf16 hi pairs, then 8 columns of lo pairs
-__device__ __forceinline__ void relu_split16(const float (&acc)[16], const float (&add)[16], uint32_t (&o)[16])
+// v = ReLU(acc * unscale + add) -> 8 columns of fp16 hi pairs, then 8 columns of
+// lo pairs (lo = v - float(hi) is exact in FP32: at most 13 significant bits)
+__device__ __forceinline__ void relu_split16(const float (&acc)[16], const float (&add)[16], float unscale,
+                                             uint32_t (&o)[16])
 {
 #pragma unroll
     for (int i = 0; i < 8; i++)
     {
-        float2 v = __fadd2_rn(make_float2(acc[2 * i], acc[2 * i + 1]), make_float2(add[2 * i], add[2 * i + 1]));
-        v.x = fmaxf(v.x, 0.0f);
-        v.y = fmaxf(v.y, 0.0f);
-        const uint32_t h = pack_bf16(v.x, v.y);
-        const float2 hf = make_float2(__uint_as_float(h << 16), __uint_as_float(h & 0xffff0000u));
+        float2 v = __ffma2_rn(make_float2(acc[2 * i], acc[2 * i + 1]), make_float2(unscale, unscale),
+                              make_float2(add[2 * i], add[2 * i + 1]));
+        v.x = relu_nan(v.x);
+        v.y = relu_nan(v.y);
+        const uint32_t h = pack_f16(v.x, v.y);
+        const float2 hf = __half22float2(*reinterpret_cast<const __half2 *>(&h));
         const float2 lo = __ffma2_rn(hf, make_float2(-1.0f, -1.0f), v);
         o[i] = h;
-        o[8 + i] = pack_bf16(lo.x, lo.y);
+        o[8 + i] = pack_f16(lo.x, lo.y);
     }
 }
 
@@ -156,57 +188,52 @@ __device__ __forceinline__ void super_origin(const Tc2Args &a, int tile, int &g0
     s0 = (tile % a.n_sblk) * SUPER_S;
 }
 
-// all UMMAs of one layer step: 10 K steps x (hi.hi, lo.hi, hi.lo), A from TMEM
+// all UMMAs of one layer step, A from TMEM: the two cross-term passes (a_lo w_hi,
+// a_hi w_lo) first, then a_hi w_hi. The tensor core's FP32 accumulation truncates
+// at each UMMA relative to the running sum, so summing the small cross terms
+// while the accumulator is still small leaves ~10 full-size truncations per
+// layer instead of 30.
 template <bool SPLIT>
-__device__ __forceinline__ void issue_layer(uint32_t d, uint32_t bh, uint32_t areg, bool first)
+__device__ __forceinline__ void issue_layer(uint32_t d, uint32_t bh, uint32_t areg)
 {
     constexpr uint32_t LBO = WPC / 2 / 8 * 128;
-    constexpr uint32_t IDESC = tc::make_idesc(1, 2 * TM, WPC);
+    constexpr uint32_t IDESC = tc::make_idesc(0, 2 * TM, WPC); // f16 x f16 -> f32
     constexpr uint32_t DH = tc::desc_hi(128);
     const uint32_t b0 = tc::desc_lo(bh, LBO);
+    if (SPLIT)
+    {
+#pragma unroll
+        for (int k = 0; k < KSTEPS; k++)
+            tc::mma2_f16_ts(d, areg + 16 * k + 8, tc::desc_of(b0 + (k * 2 * KB >> 4), DH), IDESC, k > 0 ? 1u : 0u);
+#pragma unroll
+        for (int k = 0; k < KSTEPS; k++)
+            tc::mma2_f16_ts(d, areg + 16 * k, tc::desc_of(b0 + ((k * 2 + 1) * KB >> 4), DH), IDESC, 1u);
+    }
 #pragma unroll
     for (int k = 0; k < KSTEPS; k++)
-    {
-        const uint64_t dbh = tc::desc_of(b0 + (k * 2 * KB >> 4), DH);
-        const uint32_t ahi = areg + 16 * k;
-        tc::mma2_f16_ts(d, ahi, dbh, IDESC, (k == 0 && first) ? 0u : 1u);
-        if (SPLIT)
-        {
-            tc::mma2_f16_ts(d, ahi + 8, dbh, IDESC, 1u);
-            tc::mma2_f16_ts(d, ahi, tc::desc_of(b0 + ((k * 2 + 1) * KB >> 4), DH), IDESC, 1u);
-        }
-    }
+        tc::mma2_f16_ts(d, areg + 16 * k, tc::desc_of(b0 + (k * 2 * KB >> 4), DH), IDESC, (SPLIT || k > 0) ? 1u : 0u);
 }
-// the heads: N = 32, A = layer 7's converted output in TMEM, B resident in shared memory
+// the heads: N = 32, A = layer 7's converted output in TMEM, B resident in shared
+// memory; same pass order as issue_layer
 template <bool SPLIT>
 __device__ __forceinline__ void issue_heads(uint32_t d, uint32_t bh, uint32_t areg)
 {
     constexpr uint32_t KBH = NHEAD_N / 2 * 16 * 2, LBO = NHEAD_N / 2 / 8 * 128;
-    constexpr uint32_t IDESC = tc::make_idesc(1, 2 * TM, NHEAD_N);
+    constexpr uint32_t IDESC = tc::make_idesc(0, 2 * TM, NHEAD_N);
     constexpr uint32_t DH = tc::desc_hi(128);
     const uint32_t b0 = tc::desc_lo(bh, LBO);
+    if (SPLIT)
+    {
+#pragma unroll
+        for (int k = 0; k < KSTEPS; k++)
+            tc::mma2_f16_ts(d, areg + 16 * k + 8, tc::desc_of(b0 + (k * 2 * KBH >> 4), DH), IDESC, k > 0 ? 1u : 0u);
+#pragma unroll
+        for (int k = 0; k < KSTEPS; k++)
+            tc::mma2_f16_ts(d, areg + 16 * k, tc::desc_of(b0 + ((k * 2 + 1) * KBH >> 4), DH), IDESC, 1u);
+    }
 #pragma unroll
     for (int k = 0; k < KSTEPS; k++)
-    {
-        const uint64_t dbh = tc::desc_of(b0 + (k * 2 * KBH >> 4), DH);
-        const uint32_t ahi = areg + 16 * k;
-        tc::mma2_f16_ts(d, ahi, dbh, IDESC, k > 0 ? 1u : 0u);
-        if (SPLIT)
-        {
-            tc::mma2_f16_ts(d, ahi + 8, dbh, IDESC, 1u);
-            tc::mma2_f16_ts(d, ahi, tc::desc_of(b0 + ((k * 2 + 1) * KBH >> 4), DH), IDESC, 1u);
-        }
-    }
-}
-// the cterm block into the 160 accumulator columns: 40 copies of [32 rows][4 f32],
-// each broadcast to the 4 lane quarters (the CTA's 4 positions)
-__device__ __forceinline__ void issue_cterm(uint32_t d, uint32_t cseg)
-{
-    constexpr uint32_t DH = tc::desc_hi(128);
-    const uint32_t c0 = tc::desc_lo(cseg, 16);
-#pragma unroll
-    for (int g = 0; g < WPC / 4; g++)
-        tc::cp2_32x128b_x4(d + 4 * g, tc::desc_of(c0 + (g * TG * 16 >> 4), DH));
+        tc::mma2_f16_ts(d, areg + 16 * k, tc::desc_of(b0 + (k * 2 * KBH >> 4), DH), IDESC, (SPLIT || k > 0) ? 1u : 0u);
 }
 // per lane (row = Gaussian g0 + lane): 16 cterm columns of a chunk from a cterm
 // block in shared memory ([40 column groups][32 rows][4] f32; 512 contiguous bytes
@@ -227,7 +254,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1) mlp_tc2_
     extern __shared__ uint8_t smem_raw[];
     uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     uint8_t *ring = smem;                                    // weight stages (layers 1..7)
-    uint8_t *cring = ring + SMEM_RING;                       // layer 0's cterm block
+    uint8_t *cring = ring + SMEM_RING;                       // cterm blocks (layers 0/2/4/6)
     float *pbuf = reinterpret_cast<float *>(cring + SMEM_CRING); // [2][2][4][640]
     uint8_t *hb = reinterpret_cast<uint8_t *>(pbuf + 2 * 2 * TS * PROW); // heads B operand (this CTA's 16 columns)
     float *sbias = reinterpret_cast<float *>(hb + HB_BYTES);            // [8][160]
@@ -290,7 +317,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1) mlp_tc2_
             super_origin(a, cluster + it * nclusters, g0, s0);
             for (int l = 0; l < NL; l++)
             {
-                if (l == 0)
+                if (has_xc(l))
                 {
                     MBAR_WAIT_PLAIN(&c_empty[cstage], cph ^ 1);
                     if (tc::elect_one())
@@ -312,16 +339,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1) mlp_tc2_
                     MBAR_WAIT_PLAIN(&w_empty[stage], ph ^ 1);
                     if (tc::elect_one())
                     {
-                        const uint32_t cb = has_xc(l) ? C_BLOCK : 0;
-                        tc::mbar_arrive_expect_tx(&w_full[stage], W_BYTES + cb);
+                        tc::mbar_arrive_expect_tx(&w_full[stage], W_BYTES);
                         tc::bulk_g2s(ring + stage * SLOT,
                                      reinterpret_cast<const uint8_t *>(a.w) + ((size_t)(l - 1) * 2 + rank) * W_BYTES,
                                      W_BYTES, &w_full[stage]);
-                        if (cb)
-                            tc::bulk_g2s(ring + stage * SLOT + W_BYTES,
-                                         reinterpret_cast<const uint8_t *>(a.cterm) +
-                                             ((size_t)(g0 / TG) * 4 + l / 2) * C_BLOCK,
-                                         cb, &w_full[stage]);
                     }
                     __syncwarp();
                     if (++stage == NSTAGE)
@@ -397,9 +418,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1) mlp_tc2_
                     if (tc::elect_one())
                     {
                         const uint32_t d = tmem + (m % 3) * WPC;
-                        if (has_xc(l))
-                            issue_cterm(d, b + W_BYTES); // the accumulator starts from W_c xc
-                        issue_layer<SPLIT>(d, b, tmem + ((m + 1) % 3) * WPC, !has_xc(l));
+                        issue_layer<SPLIT>(d, b, tmem + ((m + 1) % 3) * WPC);
                         tc::mma2_commit(&acc[t], 3);
                         if (t == 1)
                             tc::mma2_commit(&w_empty[stage], 3);
@@ -446,8 +465,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1) mlp_tc2_
             tc::cp_async_wait_all();
             tc::named_bar(1, EPI_THREADS);
         };
-        // one 16-column chunk: v = [acc +] add (+ cterm) -> ReLU -> bf16 hi/lo -> TMEM (in place)
-        auto convert = [&](uint32_t reg, int chunk, const float *add, const uint8_t *cblk, bool from_acc) {
+        // one 16-column chunk: v = [acc * 2^-e_l +] add (+ cterm) -> ReLU -> fp16 hi/lo -> TMEM (in place)
+        auto convert = [&](uint32_t reg, int chunk, const float *add, const uint8_t *cblk, bool from_acc,
+                           float unscale) {
             const int n0 = chunk * 16;
             uint32_t raw[16];
             if (from_acc)
@@ -481,7 +501,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1) mlp_tc2_
                     v[i] = 0.0f;
             }
             uint32_t o[16];
-            relu_split16(v, x, o);
+            relu_split16(v, x, unscale, o);
             tc::tmem_st16(reg + n0, o);
         };
         // heads readout (group-0 warps: one TMEM lane quarter each) of tile t of the
@@ -499,7 +519,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1) mlp_tc2_
                 const size_t plane = (size_t)a.cap_b * a.np;
 #pragma unroll
                 for (int h = 0; h < NHEADS; h++)
-                    a.res[h * plane + (size_t)s * a.np + g] = v[h] + shb[h];
+                    a.res[h * plane + (size_t)s * a.np + g] = __fmaf_rn(v[h], a.unscale[8], shb[h]);
             }
         };
         auto wait_heads = [&](int t) {
@@ -524,7 +544,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1) mlp_tc2_
             for (int l = 0; l < NL; l++)
             {
                 const uint8_t *cblk = nullptr;
-                if (l == 0)
+                if (has_xc(l))
                 {
                     MBAR_WAIT_PLAIN(&c_full[cstage], cph);
                     cblk = cring + cstage * C_BLOCK;
@@ -555,16 +575,17 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1) mlp_tc2_
                     const uint32_t reg = tmem + (m % 3) * WPC + lane_off;
                     const float *prow = pbuf + ((it & 1) * 2 + t) * TS * PROW + q * PROW;
                     const float *add = has_xc(l) ? prow + (l / 2) * WPC : sbias + l * WPC; // warp-uniform
-                    convert(reg, grp, add, cblk, l > 0);
+                    const float us = a.unscale[l]; // warp-uniform (layer 0: acc is not read)
+                    convert(reg, grp, add, cblk, l > 0, us);
                     if (two)
-                        convert(reg, c1, add, cblk, l > 0);
+                        convert(reg, c1, add, cblk, l > 0, us);
                     tc::tmem_st_wait();
                     tc::tc_fence_before();
                     __syncwarp();
                     if (lane == 0)
                         tc::mbar_arrive_remote_relaxed(tc::mapa(&a_ready[t], 0));
                 }
-                if (l == 0)
+                if (has_xc(l))
                 {
                     // both tiles have read this cterm block
                     if (lane == 0)
@@ -601,36 +622,81 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1) mlp_tc2_
     }
 }
 
-uint16_t bf16_bits(float f)
+// fp16 bits of x, round to nearest even (host; subnormals and overflow as IEEE)
+uint16_t f16_bits(float x) { return __half_as_ushort(__float2half_rn(x)); }
+float f16_float(uint16_t h) { return __half2float(__ushort_as_half(h)); }
+
+// power-of-two exponent e with max_abs * 2^e in [2^13, 2^14) (0 for an all-zero block)
+int scale_exp(float max_abs)
 {
-    uint32_t u;
-    std::memcpy(&u, &f, 4);
-    if ((u & 0x7fffffffu) > 0x7f800000u)
-        return 0x7fc0;
-    u += 0x7fffu + ((u >> 16) & 1u);
-    return (uint16_t)(u >> 16);
+    if (!(max_abs > 0.0f) || !std::isfinite(max_abs))
+        return 0;
+    int e2 = 0;
+    std::frexp(max_abs, &e2); // max_abs = m 2^e2, m in [0.5, 1)
+    return 14 - e2;
 }
 
-float bf16_float(uint16_t h)
+// w * 2^e split into fp16 hi + lo (both stored at the UMMA K-major slot idx)
+void put_split(uint16_t *hi, uint16_t *lo, size_t idx, float w, float scale)
 {
-    const uint32_t u = (uint32_t)h << 16;
-    float f;
-    std::memcpy(&f, &u, 4);
-    return f;
+    const float ws = w * scale; // exact (power of two)
+    const uint16_t hb = f16_bits(ws);
+    hi[idx] = hb;
+    lo[idx] = f16_bits(ws - f16_float(hb));
 }
 } // namespace
 
-// Packed weights of the ping-pong kernel: per layer l = 1..7, pair rank 0 then 1
-// (each its 80 of the 160 output columns), 10 K steps x (hi, lo) in UMMA K-major
+// cterm blocks from the per-Gaussian centre terms cg [np][4][160] (W_c xc of
+// layers 0,2,4,6, FP32, center_terms_kernel): block b, layer j, column group
+// n / 4, row = Gaussian % 32 -> the tcgen05.cp source layout (zero rows past np).
+// All four are added by the epilogue and carry the activation scale 2^k (exact).
+__global__ void cterm_pack_kernel(const float *__restrict__ cg, float *__restrict__ ct, int np, int nblk, float s0,
+                                  float s2, float s4, float s6)
+{
+    const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (idx >= (int64_t)nblk * TG * 4 * WPC)
+        return;
+    const int n = (int)(idx % WPC), j = (int)((idx / WPC) % 4);
+    const int g = (int)(idx / (4 * WPC));
+    const int blk = g / TG, row = g % TG;
+    const size_t dst = ((size_t)blk * 4 + j) * (C_BLOCK / 4) + ((size_t)(n / 4) * TG + row) * 4 + n % 4;
+    const float sc = j == 0 ? s0 : (j == 1 ? s2 : (j == 2 ? s4 : s6));
+    ct[dst] = g < np ? cg[((size_t)g * 4 + j) * WPC + n] * sc : 0.0f;
+}
+
+bool mlp_tc_available() { return true; }
+
+// Packed weights: per layer l = 1..7, pair rank 0 then 1 (each its 80 of the 160
+// output columns), 10 K steps x (hi, lo) fp16 of w * 2^e_l in UMMA K-major
 // core-matrix order: element (n_local, kk) of a K step at
-// ((kk/8)*(80/8) + n_local/8)*64 + (n_local%8)*8 + kk%8.
-void prepare_tc2_weights(Ctx &c, const std::vector<float> &whT, const std::vector<float> &heads)
+// ((kk/8)*(80/8) + n_local/8)*64 + (n_local%8)*8 + kk%8. Also the heads' B
+// operand (scale 2^e_h) and the cterm blocks.
+void prepare_tc2_weights(Ctx &c, const std::vector<float> &whT, const std::vector<float> &heads,
+                         const std::vector<float> &bias)
 {
     const int WP = c.net.wp;
     constexpr int NC = WPC / 2;
+    // per-layer scales from the largest |w| of the layer (zero padding included: harmless)
+    for (int l = 1; l < NL; l++)
+    {
+        float m = 0.0f;
+        for (size_t i = 0; i < (size_t)WP * WP; i++)
+            m = std::max(m, std::fabs(whT[(size_t)(l - 1) * WP * WP + i]));
+        c.net.tc_exp[l] = scale_exp(m);
+    }
+    {
+        float m = 0.0f;
+        for (int h = 0; h < NHEADS; h++)
+            for (int k = 0; k < WP; k++)
+                m = std::max(m, std::fabs(heads[(size_t)h * WP + k]));
+        c.net.tc_exp[8] = scale_exp(m);
+    }
+    c.net.tc_exp[0] = 0;
     std::vector<uint16_t> packed((size_t)7 * 2 * W_BYTES / 2);
     size_t at = 0;
     for (int l = 1; l < NL; l++)
+    {
+        const float sc = std::ldexp(1.0f, c.net.tc_exp[l]);
         for (int rk = 0; rk < 2; rk++)
             for (int k = 0; k < KSTEPS; k++)
             {
@@ -639,14 +705,13 @@ void prepare_tc2_weights(Ctx &c, const std::vector<float> &whT, const std::vecto
                     for (int kk = 0; kk < 16; kk++)
                     {
                         const float w = whT[((size_t)(l - 1) * WP + (k * 16 + kk)) * WP + rk * NC + nl];
-                        const uint16_t hb = bf16_bits(w);
-                        const size_t idx = (size_t)((kk / 8) * (NC / 8) + nl / 8) * 64 + (nl % 8) * 8 + kk % 8;
-                        hi[idx] = hb;
-                        lo[idx] = bf16_bits(w - bf16_float(hb));
+                        put_split(hi, lo, (size_t)((kk / 8) * (NC / 8) + nl / 8) * 64 + (nl % 8) * 8 + kk % 8, w, sc);
                     }
                 at += 2 * NC * 16;
             }
+    }
     // heads B operand: per rank its 16 of the 32 UMMA columns (heads 0-4 real)
+    const float hsc = std::ldexp(1.0f, c.net.tc_exp[8]);
     std::vector<uint16_t> hpk((size_t)2 * HB_BYTES / 2, 0);
     for (int rk = 0; rk < 2; rk++)
         for (int k = 0; k < KSTEPS; k++)
@@ -657,10 +722,7 @@ void prepare_tc2_weights(Ctx &c, const std::vector<float> &whT, const std::vecto
                 {
                     const int h = rk * 16 + nl;
                     const float w = h < NHEADS ? heads[(size_t)h * WP + k * 16 + kk] : 0.0f;
-                    const uint16_t hb = bf16_bits(w);
-                    const size_t idx = (size_t)((kk / 8) * 2 + nl / 8) * 64 + (nl % 8) * 8 + kk % 8;
-                    hi[idx] = hb;
-                    lo[idx] = bf16_bits(w - bf16_float(hb));
+                    put_split(hi, lo, (size_t)((kk / 8) * 2 + nl / 8) * 64 + (nl % 8) * 8 + kk % 8, w, hsc);
                 }
         }
     void *dh = nullptr;
@@ -673,6 +735,21 @@ void prepare_tc2_weights(Ctx &c, const std::vector<float> &whT, const std::vecto
     c.allocs.push_back(d);
     check_cuda(cudaMemcpy(d, packed.data(), packed.size() * 2, cudaMemcpyHostToDevice), "upload tc2 weights");
     c.net.w_tc2 = static_cast<uint16_t *>(d);
+
+    const int nblk = (c.g.n + TG - 1) / TG;
+    const size_t total = (size_t)nblk * TG * 4 * WPC;
+    check_cuda(cudaMalloc(&d, total * sizeof(float)), "cudaMalloc cterm blocks");
+    c.allocs.push_back(d);
+    c.net.c_tc = static_cast<float *>(d);
+    const int *k = c.net.tc_ascale;
+    cterm_pack_kernel<<<(unsigned)((total + 255) / 256), 256, 0, c.stream>>>(
+        c.net.cg, c.net.c_tc, c.g.np, nblk, std::ldexp(1.0f, k[0]), std::ldexp(1.0f, k[2]), std::ldexp(1.0f, k[4]),
+        std::ldexp(1.0f, k[6]));
+    std::vector<float> bs(bias.size());
+    for (size_t i = 0; i < bias.size(); i++)
+        bs[i] = std::ldexp(bias[i], k[i / WP]);
+    c.net.bias_tc = upload(c, bs);
+    check_cuda(cudaStreamSynchronize(c.stream), "cterm blocks");
 }
 
 static long long *g_trace2 = nullptr;
@@ -686,9 +763,8 @@ int mlp_tc2_trace(long long *out)
 
 void launch_mlp_tc2(Ctx &c, int nb, cudaStream_t st)
 {
-    static int max_clusters = 0;
-    if (!max_clusters)
-    {
+    static DeviceOnce once;
+    const int max_clusters = once.get(c.device, [] {
         for (auto k : {mlp_tc2_kernel<true>, mlp_tc2_kernel<false>})
         {
             check_cuda(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES),
@@ -708,15 +784,16 @@ void launch_mlp_tc2(Ctx &c, int nb, cudaStream_t st)
         cfg.dynamicSmemBytes = SMEM_BYTES;
         cfg.attrs = attr;
         cfg.numAttrs = 1;
-        check_cuda(cudaOccupancyMaxActiveClusters(&max_clusters, mlp_tc2_kernel<true>, &cfg),
-                   "tc2 mlp cluster occupancy");
-        if (max_clusters < 1)
+        int mc = 0;
+        check_cuda(cudaOccupancyMaxActiveClusters(&mc, mlp_tc2_kernel<true>, &cfg), "tc2 mlp cluster occupancy");
+        if (mc < 1)
             check_cuda(cudaErrorLaunchOutOfResources, "tc2 mlp: no CTA pair fits on this device");
-    }
+        return mc;
+    });
     Tc2Args a;
     a.w = c.net.w_tc2;
     a.cterm = c.net.c_tc;
-    a.bias = c.net.bias;
+    a.bias = c.net.bias_tc;
     a.pterm = c.w.pterm;
     a.wh = c.net.wh_tc2;
     a.hbias = c.net.hbias;
@@ -727,6 +804,12 @@ void launch_mlp_tc2(Ctx &c, int nb, cudaStream_t st)
     a.cap_b = (int)c.w.cap_b;
     a.n_sblk = (nb + SUPER_S - 1) / SUPER_S;
     a.ntiles = ((c.g.n + TG - 1) / TG) * a.n_sblk;
+    // layer l's accumulator holds 2^(e_l + k_(l-1)) W h; its output carries 2^k_l
+    const int *k = c.net.tc_ascale;
+    a.unscale[0] = 1.0f;
+    for (int l = 1; l < 8; l++)
+        a.unscale[l] = std::ldexp(1.0f, k[l] - c.net.tc_exp[l] - k[l - 1]);
+    a.unscale[8] = std::ldexp(1.0f, -(c.net.tc_exp[8] + k[7])); // heads: back to true residuals
     a.trace = nullptr;
     if (kHooks && getenv("SWR_TC_DEBUG"))
     {

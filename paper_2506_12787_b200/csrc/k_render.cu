@@ -113,7 +113,7 @@ __device__ __forceinline__ int4 bbox_of(const Grid &g, float el, float az, float
 // row/column ranges and the tile count.
 __global__ void __launch_bounds__(256) setup_kernel(Grid g, SceneDev sd, const float *__restrict__ res, int64_t plane,
                                                     float4 *__restrict__ dyn, int4 *__restrict__ rng, int *__restrict__ cnt,
-                                                    int with_res)
+                                                    int with_res, int64_t *__restrict__ nonfinite)
 {
     const int s = blockIdx.y;
     const int g4 = (blockIdx.x * blockDim.x + threadIdx.x) * 4;
@@ -142,6 +142,16 @@ __global__ void __launch_bounds__(256) setup_kernel(Grid g, SceneDev sd, const f
         const float v0[4] = {x0.x, x0.y, x0.z, x0.w}, v1[4] = {x1.x, x1.y, x1.z, x1.w};
         const float v2[4] = {x2.x, x2.y, x2.z, x2.w}, v3[4] = {x3.x, x3.y, x3.z, x3.w};
         const float v4[4] = {x4.x, x4.y, x4.z, x4.w};
+        if (nonfinite)
+        {
+            // an fp16 overflow in the tensor-core MLP surfaces here as NaN (k_mlp_tc2.cu)
+            bool bad = false;
+#pragma unroll
+            for (int k = 0; k < 4; k++)
+                bad |= !isfinite(v0[k]) || !isfinite(v1[k]) || !isfinite(v2[k]) || !isfinite(v3[k]) || !isfinite(v4[k]);
+            if (bad && g4 < g.n)
+                *nonfinite = 1;
+        }
 #pragma unroll
         for (int k = 0; k < 4; k++)
         {
@@ -168,7 +178,8 @@ __global__ void __launch_bounds__(256) setup_kernel(Grid g, SceneDev sd, const f
 void launch_setup(Ctx &c, int nb, bool with_res, cudaStream_t st)
 {
     dim3 grid((c.g.np / 4 + 255) / 256, nb);
-    setup_kernel<<<grid, 256, 0, st>>>(c.g, c.s, c.w.res, c.w.cap_b * c.g.np, c.w.dyn, c.w.rng, c.w.cnt, with_res);
+    setup_kernel<<<grid, 256, 0, st>>>(c.g, c.s, c.w.res, c.w.cap_b * c.g.np, c.w.dyn, c.w.rng, c.w.cnt, with_res,
+                                       with_res ? c.w.stats + 2 : nullptr);
     c.launches++;
 }
 

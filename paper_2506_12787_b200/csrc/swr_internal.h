@@ -8,6 +8,7 @@
 #include <algorithm>
 #include <array>
 #include <functional>
+#include <mutex>
 #include <stdexcept>
 #include <string>
 #include <vector>
@@ -60,11 +61,14 @@ struct NetDev
     float *wcen;           // [4][wp][dc] centre-encoding columns of layers 0,2,4,6
     float *heads;          // [5][wp] head weights (centre 2, response 2, atten 1)
     float *hbias;          // [5]
-    // tcgen05 path (bf16 hi/lo, UMMA canonical K-major layout, see k_mlp_tc.cu)
-    uint16_t *w_tc;        // packed bf16 hi/lo weights in the tensor-core kernel's consumption order
-    float *c_tc;           // cg repacked per 32-Gaussian block as tcgen05.cp sources (k_mlp_tc.cu)
-    uint16_t *w_tc2 = nullptr; // packed bf16 hi/lo weights of the ping-pong kernel (k_mlp_tc2.cu)
-    uint16_t *wh_tc2 = nullptr; // its heads B operand (bf16 hi/lo, 2 ranks x 16 columns)
+    // tcgen05 path (k_mlp_tc2.cu): fp16 hi/lo of w * 2^tc_exp[l], UMMA canonical K-major layout
+    float *c_tc = nullptr;      // cg repacked per 32-Gaussian block as tcgen05.cp sources (layers 2/4/6 scaled)
+    uint16_t *w_tc2 = nullptr;  // packed weights, layers 1..7, in the kernel's consumption order
+    uint16_t *wh_tc2 = nullptr; // heads B operand (2 ranks x 16 columns)
+    int tc_exp[9] = {};         // per-layer weight scale exponents (index l = 1..7), [8] heads
+    int tc_ascale[8] = {};      // activation scale exponent k_l of each trunk layer's output (scene-load probe)
+    float tc_amax[8] = {};      // the probe's largest ReLU output per trunk layer
+    float *bias_tc = nullptr;   // [8][160] bias_l x 2^k_l (layers 1, 3, 5, 7 read by the tensor-core epilogue)
 };
 
 // Per-chunk scratch (positions per chunk = cap_b).
@@ -110,7 +114,6 @@ struct Ctx
     float cutoff = 3.0f;
     int tile = 16;
     int mlp_precision = 0;
-    int mlp_kernel = 2;   // tensor-core MLP: 1 = output parts (k_mlp_tc.cu), 2 = two tiles ping-pong (k_mlp_tc2.cu)
     int chunk = 256;
     bool stage_timing = false;
     double rssi_slope = 1.0, rssi_intercept = 0.0;
@@ -118,6 +121,7 @@ struct Ctx
     Work w;
     int64_t launches = 0;
     int64_t pairs_last = 0;
+    int64_t mlp_reruns = 0;             // chunks whose fp16 tensor-core MLP overflowed and re-ran in FP32
     double stage_ms[6]{};               // accumulated while stage_timing is on (swr_stage_times resolves)
     std::vector<std::array<cudaEvent_t, 7>> stage_pending; // recorded per chunk, read lazily
     std::vector<void *> allocs;
@@ -125,6 +129,23 @@ struct Ctx
 };
 
 void check_cuda(cudaError_t e, const char *what);
+
+// One-time setup per device (kernel attributes and occupancy queries are per
+// device; thread-safe, retried if the initialiser throws).
+struct DeviceOnce
+{
+    static constexpr int kMax = 64;
+    std::once_flag flag[kMax];
+    int value[kMax] = {};
+    template <class F>
+    int get(int dev, F &&init)
+    {
+        if (dev < 0 || dev >= kMax)
+            throw std::invalid_argument("CUDA device ordinal out of range");
+        std::call_once(flag[dev], [&] { value[dev] = init(); });
+        return value[dev];
+    }
+};
 
 template <class T>
 inline T *dalloc(Ctx &c, size_t count)
@@ -240,12 +261,12 @@ void launch_heads(Ctx &c, int nb, uint32_t flags, double *d_pooled, double *d_rs
 void launch_heads_from_spectra(Ctx &c, int nb, const float *d_spec, cudaStream_t st);
 
 bool mlp_tc_available();
-void prepare_tc_weights(Ctx &c, const std::vector<float> &whT, const std::vector<float> &heads);
-void launch_mlp_tc(Ctx &c, int nb, cudaStream_t st);
+bool mlp_uses_tc(const Ctx &c);
+void probe_activations(Ctx &c, int nb, float out[8], cudaStream_t st);
 void launch_mlp_tc2(Ctx &c, int nb, cudaStream_t st);
 int mlp_tc2_trace(long long *out);
-void prepare_tc2_weights(Ctx &c, const std::vector<float> &whT, const std::vector<float> &heads);
-int mlp_tc_trace(long long *out);
+void prepare_tc2_weights(Ctx &c, const std::vector<float> &whT, const std::vector<float> &heads,
+                         const std::vector<float> &bias);
 size_t metrics_tmp_doubles(const Ctx &c, int nb);
 void launch_metrics(Ctx &c, const float *d_pred, const float *d_target, int nb, double peak, double *d_psnr,
                     double *d_ssim, double *d_l1, double *d_tmp, int *d_bad, cudaStream_t st);

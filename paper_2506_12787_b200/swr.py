@@ -28,7 +28,7 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("SWR_LIB") or os.path.join(_HERE, "libswr.so")
 
 OUT_SPECTRA, OUT_POOLED, OUT_RSSI, OUT_AOA, NO_RESIDUALS = 1, 2, 4, 8, 16
-MLP_FP32, MLP_BF16X3, MLP_BF16 = 0, 1, 2
+MLP_FP32, MLP_FP16X3, MLP_FP16 = 0, 1, 2
 
 _fp = C.POINTER(C.c_float)
 _dp = C.POINTER(C.c_double)

@@ -18,6 +18,10 @@ Fixtures:
                          build), spectra + heads (reference as shipped), canonical render
   criterion1.npz         the acceptance-criterion-1 style small instances (grid <= 16x32,
                          n <= 64, cutoff off, half with residuals) and the reference spectra
+  criterion1_ref.npz     the reference's OWN criterion-1 instances: its wrfsplat::Rng(20250814)
+                         stream replayed in the shim (acceptance.cpp:130-147, 159-199), with
+                         the reference's tiled float rasterize and the criterion's FP64 dense
+                         oracle (acceptance.cpp:53-109) for each
 """
 import os
 import sys
@@ -93,8 +97,27 @@ def main():
             c[f"{i}_dc"], c[f"{i}_dr"], c[f"{i}_da"] = r
         c[f"{i}_out"] = out
     np.savez_compressed(os.path.join(HERE, "criterion1.npz"), **c)
+    criterion1_ref()
     print("golden fixtures written")
 
 
+def criterion1_ref():
+    import ctypes as C
+    lib = C.CDLL(O.REF_SO)
+    hwn = np.zeros(150, np.int32)
+    cr, ch = np.zeros((50, 64, 2), np.float32), np.zeros((50, 64, 3), np.float32)
+    at, rs = np.zeros((50, 64), np.float32), np.zeros((50, 64, 2), np.float32)
+    dc, dr, da = np.zeros((50, 64, 2), np.float32), np.zeros((50, 64, 2), np.float32), np.zeros((50, 64), np.float32)
+    out, dense = np.zeros((50, 1024), np.float32), np.zeros((50, 1024), np.float64)
+    ptr = lambda a: a.ctypes.data_as(C.c_void_p)
+    rc = lib.wref_criterion1(*[ptr(a) for a in (hwn, cr, ch, at, rs, dc, dr, da, out, dense)])
+    assert rc == 0
+    np.savez_compressed(os.path.join(HERE, "criterion1_ref.npz"), hwn=hwn.reshape(50, 3), cr=cr, ch=ch, at=at,
+                        rs=rs, dc=dc, dr=dr, da=da, out=out, dense=dense)
+
+
 if __name__ == "__main__":
-    main()
+    if sys.argv[1:] == ["criterion1_ref"]:
+        criterion1_ref()
+    else:
+        main()

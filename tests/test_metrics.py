@@ -113,7 +113,7 @@ def test_gpu_evaluate_matches_render_then_metrics():
     from paper_2506_12787_b200 import swr
     sc = make_scene(400, seed=9)
     ck = swr.Checkpoint.from_scene(sc)
-    ck.set_option("mlp_precision", swr.MLP_BF16X3)
+    ck.set_option("mlp_precision", swr.MLP_FP16X3)
     pos = random_positions(7, seed=4)
     spec = swr.render(ck, pos)["spectra"]
     rng = np.random.default_rng(0)

@@ -98,6 +98,25 @@ def test_oracle_matches_criterion1_instances():
     assert worst <= 1e-5
 
 
+def test_oracle_matches_reference_criterion1_instances():
+    """The reference's own criterion-1 instances (Rng(20250814) stream replayed by
+    the reference build, tests/golden/make_golden.py criterion1_ref): the port
+    meets the gate (<= 1e-5 vs the FP64 dense oracle) and tracks the reference's
+    tiled float output."""
+    c = np.load(os.path.join(GOLD, "criterion1_ref.npz"))
+    worst_dense = worst_ref = 0.0
+    for i in range(50):
+        H, W, n = map(int, c["hwn"][i])
+        s = Scene(H=H, W=W, center_raw=c["cr"][i, :n], cholesky=c["ch"][i, :n], atten_logit=c["at"][i, :n],
+                  response=c["rs"][i, :n], cutoff=0.0)
+        r = (c["dc"][i, :n], c["dr"][i, :n], c["da"][i, :n]) if i % 2 == 1 else None
+        out = O.Port(s).rasterize(r, precise=True).ravel()
+        k = 2 * H * W
+        worst_dense = max(worst_dense, float(np.abs(out - c["dense"][i, :k]).max()))
+        worst_ref = max(worst_ref, float(np.abs(out - c["out"][i, :k]).max()))
+    assert worst_dense <= 1e-5 and worst_ref <= 1e-5, (worst_dense, worst_ref)
+
+
 @pytest.mark.skipif(not has_ref(), reason="reference build absent (GPU box)")
 @pytest.mark.parametrize("cutoff,H,W", [(3.0, 90, 360), (0.0, 12, 24), (3.0, 16, 32), (1.5, 45, 90)])
 def test_oracle_vs_reference_live(cutoff, H, W):
