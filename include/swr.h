@@ -43,6 +43,7 @@ enum swr_status
 #define SWR_NO_RESIDUALS 16u /* canonical render: skip the deformation net (rasterize(set, nullptr)) */
 
 /* MLP arithmetic (swr_set_option "mlp_precision") */
+/* default: SWR_MLP_FP16X3 for widths <= 160, SWR_MLP_FP32 above */
 #define SWR_MLP_FP32 0   /* FP32 FMA on the CUDA cores */
 #define SWR_MLP_FP16X3 1 /* tcgen05, FP32-grade: fp16 hi/lo splits of scaled operands, 3 products, fp32 accumulate */
 #define SWR_MLP_FP16 2   /* tcgen05 single fp16 product (fast tier, ~1e-3 relative residual error) */
@@ -62,6 +63,12 @@ typedef struct
  * checkpoint.cpp:100-146). device < 0 selects the current CUDA device. */
 int swr_scene_create_wrfc(const char *path, int device, swr_ctx **out);
 
+/* Host-only read of a WRFC file's header and trailer (no device needed): grid,
+ * primitive count, net dims, raster params, bbox and, for an RSSI model saved by
+ * tasks::save_rssi_model (tasks.cpp:131-150), its calibration: rssi_cal[0] =
+ * slope, rssi_cal[1] = intercept, *has_rssi = 1. Any output may be NULL. */
+int swr_wrfc_peek(const char *path, swr_scene_info *info, double *rssi_cal, int *has_rssi);
+
 /* Same from raw arrays in the reference layouts (GaussianSetT, splat.hpp:43-56;
  * DeformNetT layers in WRFD order: 8 trunk, head centre/response/atten,
  * row-major [rows x cols], deform.hpp:57-83). layer_w/layer_b may be NULL for
@@ -75,8 +82,21 @@ int swr_scene_create(int n_elevation, int n_azimuth, int n, const float *center_
 void swr_scene_destroy(swr_ctx *ctx);
 int swr_scene_get_info(swr_ctx *ctx, swr_scene_info *info);
 
+/* The scene as loaded, in the reference layouts (host copies kept by the
+ * context): GaussianSetT arrays (splat.hpp:43-56; NULL skips a field), deform
+ * layer `layer` in WRFD order 0..10 (deform.hpp:57-83; w [rows][cols] row-major,
+ * b [rows]; NULL w/b queries the shape only), checkpoint iteration and
+ * manifest hash (training.hpp:114-124). What the reference's train::Checkpoint
+ * holds by value, so swr.hpp can offer the same members. */
+int swr_scene_get_arrays(swr_ctx *ctx, float *center_raw, float *cholesky, float *atten_logit,
+                         float *response);
+int swr_scene_get_layer(swr_ctx *ctx, int layer, int *rows, int *cols, float *w, float *b);
+int swr_scene_get_meta(swr_ctx *ctx, int64_t *iteration, uint64_t *manifest_hash);
+
 /* Options: "mlp_precision" (SWR_MLP_*), "chunk" (positions per device chunk),
- * "rssi_slope" / "rssi_intercept" (affine RSSI calibration, tasks.cpp:60-94),
+ * "rssi_slope" / "rssi_intercept" (affine RSSI calibration, tasks.cpp:60-94; read
+ * from the trailer of an RSSI model, load_rssi_model tasks.cpp:139-150; SWR_OUT_RSSI
+ * fails with SWR_ERUNTIME while the scene has none, as load_rssi_model does),
  * "stage_timing" (1: record per-stage CUDA events), "stage_reset" (zero the
  * accumulated stage times). */
 int swr_set_option(swr_ctx *ctx, const char *key, double value);

@@ -223,6 +223,16 @@ class Reference:
     def save(self, path):
         self._check(self.lib.wref_ck_save(self.h, path.encode()))
 
+    def save_rssi_model(self, path, slope, intercept):
+        """tasks::save_rssi_model (tasks.cpp:131-137)."""
+        self._check(self.lib.wref_save_rssi_model(self.h, path.encode(), C.c_double(slope), C.c_double(intercept)))
+
+    def load_rssi_model(self, path):
+        """tasks::load_rssi_model (tasks.cpp:139-150) -> (slope, intercept)."""
+        out = np.zeros(2, np.float64)
+        self._check(self.lib.wref_load_rssi_model(path.encode(), _d(out)))
+        return float(out[0]), float(out[1])
+
     def normalize(self, pos_m):
         out = np.zeros(3, np.float32)
         self._check(self.lib.wref_normalize(self.h, _f(_c32(pos_m)), _f(out)))

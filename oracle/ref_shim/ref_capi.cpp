@@ -137,6 +137,28 @@ void *wref_ck_create(int H, int W, int n, const float *center_raw, const float *
     return ck;
 }
 
+// tasks::save_rssi_model (tasks.cpp:131-137): the checkpoint + calibration keys
+int wref_save_rssi_model(void *h, const char *path, double slope, double intercept)
+{
+    return guarded([&] {
+        tasks::RssiModel m;
+        m.ck = *ck_of(h);
+        m.slope = slope;
+        m.intercept = intercept;
+        tasks::save_rssi_model(path, m);
+    });
+}
+
+// tasks::load_rssi_model (tasks.cpp:139-150): calibration of an RSSI model file
+int wref_load_rssi_model(const char *path, double *slope_intercept)
+{
+    return guarded([&] {
+        const auto m = tasks::load_rssi_model(path);
+        slope_intercept[0] = m.slope;
+        slope_intercept[1] = m.intercept;
+    });
+}
+
 int wref_ck_save(void *h, const char *path)
 {
     return guarded([&] { train::save_checkpoint(path, *ck_of(h)); });

@@ -39,6 +39,27 @@ void check_cuda(cudaError_t e, const char *what)
         throw cuda_error(std::string(what) + ": " + cudaGetErrorString(e));
 }
 
+// Calls on one context are ordered on the device even when they use different
+// streams: every entry point that touches the context's buffers first waits for
+// the previous call's last work (an event), then records its own.
+struct StreamOrder
+{
+    Ctx &c;
+    cudaStream_t st;
+    StreamOrder(Ctx &cx, cudaStream_t s) : c(cx), st(s)
+    {
+        if (!c.order_ev)
+            check_cuda(cudaEventCreateWithFlags(&c.order_ev, cudaEventDisableTiming), "order event");
+        else if (c.order_pending)
+            check_cuda(cudaStreamWaitEvent(st, c.order_ev, 0), "order wait");
+    }
+    ~StreamOrder()
+    {
+        if (cudaEventRecord(c.order_ev, st) == cudaSuccess)
+            c.order_pending = true;
+    }
+};
+
 static thread_local std::string g_err;
 
 template <class F>
@@ -143,8 +164,38 @@ void refresh_scene_host(Ctx &c, const float *center_raw, const float *cholesky, 
     put(c.s.bwd, f.bwd.data(), 16 * np);
 }
 
+// Upper bound on the (tile, primitive) pairs of one position for ANY residuals:
+// residuals move centres and attenuation but never the covariance, so each
+// primitive's box extent is fixed by its static half widths (splat.cpp:222-248):
+// rows <= floor(2 h_el / cell) + 3, columns <= floor(2 h_az / cell) + 3 (or the
+// full circle), and a span of m cells crosses at most ceil((m - 1) / T) + 1 tiles
+// (+1 column tile for a split wrapped span).
+int64_t pair_bound(const Grid &g, const std::vector<double2> &half, int n)
+{
+    if (!g.cut)
+        return int64_t(n) * g.tiles;
+    auto span_tiles = [&](int64_t m) { return (m - 1 + g.tile - 1) / g.tile + 1; };
+    int64_t total = 0;
+    for (int p = 0; p < n; p++)
+    {
+        const double rows_d = std::floor(2.0 * half[p].x / g.cell_el) + 3.0;
+        const int64_t rows = rows_d >= double(g.H) ? g.H : std::max<int64_t>(1, int64_t(rows_d));
+        const int64_t tr = std::min<int64_t>(g.th, span_tiles(rows));
+        int64_t tc = g.tw;
+        if (2.0 * half[p].y < double(g.W) * g.cell_az)
+        {
+            const double cols_d = std::floor(2.0 * half[p].y / g.cell_az) + 3.0;
+            const int64_t cols = cols_d >= double(g.W) ? g.W : std::max<int64_t>(1, int64_t(cols_d));
+            tc = std::min<int64_t>(g.tw, span_tiles(cols) + 1);
+        }
+        total += tr * tc;
+    }
+    return std::max<int64_t>(total, 1);
+}
+
 void build_scene(Ctx &c, const HostScene &hs, int device)
 {
+    c.host = std::make_shared<const HostScene>(hs);
     if (hs.H < 1 || hs.W < 1)
         throw std::invalid_argument("gaussian set has an empty grid");
     if (hs.n < 0)
@@ -187,13 +238,22 @@ void build_scene(Ctx &c, const HostScene &hs, int device)
     c.tile = hs.tile;
     // default chunk: ~12.8M (Gaussian, position) rows per chunk, 256..1024 positions
     // (measured: 256 is fastest at 50k Gaussians, 1024 at 10k; option "chunk" overrides)
-    c.chunk = int(std::min<int64_t>(1024, std::max<int64_t>(256, (int64_t(12800000) / std::max(1, hs.n)) / 64 * 64)));
+
     std::memcpy(c.bbox_min, hs.bmin, sizeof(hs.bmin));
     c.manifest_hash = hs.manifest_hash;
     std::memcpy(c.bbox_max, hs.bmax, sizeof(hs.bmax));
+    c.rssi_calibrated = hs.has_rssi;
+    c.rssi_slope = hs.rssi_slope;
+    c.rssi_intercept = hs.rssi_intercept;
 
     const int n = hs.n, np = g.np;
     SceneFields f = scene_fields(g, n, hs.center_raw.data(), hs.cholesky.data(), hs.atten.data(), hs.response.data());
+    // positions per chunk: ~12.8M (Gaussian, position) rows, 256..1024 (measured: 256
+    // is fastest at 50k Gaussians, 1024 at 10k; option "chunk" overrides), and never
+    // more than keeps a chunk's pair list within 32-bit offsets for any residuals
+    c.pairs_per_pos_max = pair_bound(g, f.half, n);
+    c.chunk_cap = int(std::max<int64_t>(1, std::min<int64_t>(int64_t(1) << 30, (int64_t(INT32_MAX) - 1) / c.pairs_per_pos_max)));
+    c.chunk = int(std::min<int64_t>(c.chunk_cap, std::min<int64_t>(1024, std::max<int64_t>(256, (int64_t(12800000) / std::max(1, hs.n)) / 64 * 64))));
     const std::vector<float> &el0 = f.el0, &az0 = f.az0;
     std::vector<float> elc(hs.H), azc(hs.W);
     for (int r = 0; r < hs.H; r++)
@@ -337,6 +397,7 @@ void build_scene(Ctx &c, const HostScene &hs, int device)
             c.net.tc_ascale[l] = k;
         }
         prepare_tc2_weights(c, whT, heads, bias);
+        c.mlp_precision = 1; // FP32-grade tensor-core MLP by default (SWR_MLP_FP32 remains an option)
     }
 }
 
@@ -501,6 +562,8 @@ static void run_chunk(Ctx &c, const float *d_pos, int nb, bool normalized, bool 
         check_cuda(cudaStreamSynchronize(st), "pair count");
     }
     const int64_t pairs = c.w.host_pairs[0], max_seg = c.w.host_pairs[1];
+    if (pairs > INT32_MAX) // cannot happen within chunk_cap (pair_bound); the sort's offsets are 32-bit
+        throw std::runtime_error("pair list of a chunk exceeds 2^31 entries");
     c.pairs_last = pairs;
     ensure_pairs(c, pairs, nb, max_seg);
     launch_bin_sort(c, nb, pairs, int(max_seg), st);
@@ -753,6 +816,13 @@ HostScene parse_wrfc(const char *path)
     hs.config_json = cfg.dump();
     if (j.contains("iteration"))
         hs.iteration = j.at("iteration").get<int64_t>();
+    // an RSSI model (load_rssi_model, tasks.cpp:139-150): the affine calibration
+    if (j.contains("rssi_slope") && j.contains("rssi_intercept"))
+    {
+        hs.has_rssi = true;
+        hs.rssi_slope = j.at("rssi_slope").get<double>();
+        hs.rssi_intercept = j.at("rssi_intercept").get<double>();
+    }
     return hs;
 }
 
@@ -770,6 +840,11 @@ static void destroy(swr_ctx *h)
     if (!h)
         return;
     cudaSetDevice(h->c.device);
+    if (h->c.order_ev) // the last call's device work (possibly on a caller's stream) ends first
+    {
+        cudaEventSynchronize(h->c.order_ev);
+        cudaEventDestroy(h->c.order_ev);
+    }
     resolve_stage_times(h->c, false);
     for (void *p : h->c.allocs)
         cudaFree(p);
@@ -801,6 +876,37 @@ int swr_scene_create_wrfc(const char *path, int device, swr_ctx **out)
     }
     *out = h;
     return SWR_OK;
+}
+
+int swr_wrfc_peek(const char *path, swr_scene_info *info, double *rssi_cal, int *has_rssi)
+{
+    return guarded([&] {
+        const HostScene hs = parse_wrfc(path);
+        if (info)
+        {
+            std::memset(info, 0, sizeof(*info));
+            info->n_elevation = hs.H;
+            info->n_azimuth = hs.W;
+            info->n = hs.n;
+            info->width = hs.width;
+            info->bands_center = hs.bands_c;
+            info->bands_position = hs.bands_p;
+            info->cutoff_radius = hs.cutoff;
+            info->tile = hs.tile;
+            for (int a = 0; a < 3; a++)
+            {
+                info->bbox_min[a] = hs.bmin[a];
+                info->bbox_max[a] = hs.bmax[a];
+            }
+        }
+        if (has_rssi)
+            *has_rssi = hs.has_rssi ? 1 : 0;
+        if (rssi_cal)
+        {
+            rssi_cal[0] = hs.rssi_slope;
+            rssi_cal[1] = hs.rssi_intercept;
+        }
+    });
 }
 
 int swr_scene_create(int H, int W, int n, const float *center_raw, const float *cholesky, const float *atten_logit,
@@ -855,6 +961,52 @@ int swr_scene_create(int H, int W, int n, const float *center_raw, const float *
 
 void swr_scene_destroy(swr_ctx *ctx) { destroy(ctx); }
 
+int swr_scene_get_arrays(swr_ctx *ctx, float *center_raw, float *cholesky, float *atten_logit, float *response)
+{
+    return guarded([&] {
+        const HostScene &h = *ctx->c.host;
+        auto put = [](float *dst, const std::vector<float> &v) {
+            if (dst && !v.empty())
+                std::memcpy(dst, v.data(), v.size() * sizeof(float));
+        };
+        put(center_raw, h.center_raw);
+        put(cholesky, h.cholesky);
+        put(atten_logit, h.atten);
+        put(response, h.response);
+    });
+}
+
+int swr_scene_get_layer(swr_ctx *ctx, int layer, int *rows, int *cols, float *w, float *b)
+{
+    return guarded([&] {
+        const HostScene &h = *ctx->c.host;
+        if (h.lw.empty())
+            throw std::invalid_argument("scene has no deform net");
+        if (layer < 0 || layer >= int(h.lw.size()))
+            throw std::invalid_argument("layer index out of range");
+        const int r = int(h.lb[layer].size());
+        const int cl = r > 0 ? int(h.lw[layer].size() / size_t(r)) : 0;
+        if (rows)
+            *rows = r;
+        if (cols)
+            *cols = cl;
+        if (w)
+            std::memcpy(w, h.lw[layer].data(), h.lw[layer].size() * sizeof(float));
+        if (b)
+            std::memcpy(b, h.lb[layer].data(), h.lb[layer].size() * sizeof(float));
+    });
+}
+
+int swr_scene_get_meta(swr_ctx *ctx, int64_t *iteration, uint64_t *manifest_hash)
+{
+    return guarded([&] {
+        if (iteration)
+            *iteration = ctx->c.host->iteration;
+        if (manifest_hash)
+            *manifest_hash = ctx->c.manifest_hash;
+    });
+}
+
 int swr_scene_get_info(swr_ctx *ctx, swr_scene_info *info)
 {
     const Ctx &c = ctx->c;
@@ -893,12 +1045,18 @@ int swr_set_option(swr_ctx *ctx, const char *key, double value)
         {
             if (value < 1)
                 throw std::invalid_argument("chunk must be >= 1");
-            c.chunk = int(value);
+            c.chunk = int(std::min<double>(value, c.chunk_cap)); // pair offsets stay 32-bit
         }
         else if (k == "rssi_slope")
+        {
             c.rssi_slope = value;
+            c.rssi_calibrated = true;
+        }
         else if (k == "rssi_intercept")
+        {
             c.rssi_intercept = value;
+            c.rssi_calibrated = true;
+        }
         else if (k == "stage_timing")
             c.stage_timing = value != 0.0;
         else if (k == "stage_reset")
@@ -928,6 +1086,12 @@ int swr_get_option(swr_ctx *ctx, const char *key, double *value)
             *value = c.stage_timing ? 1.0 : 0.0;
         else if (k == "mlp_reruns")
             *value = double(c.mlp_reruns);
+        else if (k == "chunk_cap")
+            *value = c.chunk_cap;
+        else if (k == "pairs_per_position_max")
+            *value = double(c.pairs_per_pos_max);
+        else if (k == "rssi_calibrated")
+            *value = c.rssi_calibrated ? 1.0 : 0.0;
         else if (k == "mlp_act_scale_exp") // smallest of the per-layer exponents
             *value = *std::min_element(c.net.tc_ascale, c.net.tc_ascale + 8);
         else if (k == "mlp_probe_amax")
@@ -937,6 +1101,15 @@ int swr_get_option(swr_ctx *ctx, const char *key, double *value)
     });
 }
 
+// RSSI needs the affine calibration of an RSSI model (load_rssi_model throws the
+// same way on a checkpoint without it, tasks.cpp:146-147)
+static void check_rssi(const Ctx &c, uint32_t flags)
+{
+    if ((flags & SWR_OUT_RSSI) && !c.rssi_calibrated)
+        throw std::runtime_error("scene is not an RSSI model (no calibration in trailer); set the rssi_slope / "
+                                 "rssi_intercept options");
+}
+
 int swr_render_device(swr_ctx *ctx, const float *d_pos, int64_t B, uint32_t flags, float *d_spec, double *d_pooled,
                       double *d_rssi, int32_t *d_aoa_rc, double *d_aoa_ang, void *stream)
 {
@@ -944,10 +1117,12 @@ int swr_render_device(swr_ctx *ctx, const float *d_pos, int64_t B, uint32_t flag
         Ctx &c = ctx->c;
         if (B < 0)
             throw std::invalid_argument("negative batch");
+        check_rssi(c, flags);
         if (B == 0)
             return;
         check_cuda(cudaSetDevice(c.device), "cudaSetDevice");
         cudaStream_t st = stream ? (cudaStream_t)stream : c.stream;
+        StreamOrder order(c, st);
         device_render(c, d_pos, B, flags, d_spec, d_pooled, d_rssi, d_aoa_rc, d_aoa_ang, st);
     });
 }
@@ -959,10 +1134,12 @@ int swr_render(swr_ctx *ctx, const float *pos_m, int64_t B, uint32_t flags, floa
         Ctx &c = ctx->c;
         if (B < 0)
             throw std::invalid_argument("negative batch");
+        check_rssi(c, flags);
         if (B == 0)
             return;
         check_cuda(cudaSetDevice(c.device), "cudaSetDevice");
         cudaStream_t st = c.stream;
+        StreamOrder order(c, st);
         const int64_t chunk = std::max<int64_t>(1, std::min<int64_t>(B, c.chunk));
         ensure_work(c, chunk);
         const size_t per = size_t(2) * c.g.H * c.g.W;
@@ -1039,6 +1216,7 @@ int swr_predict_residuals(swr_ctx *ctx, const float *pos01, int64_t B, float *dc
         if (c.g.n < 1)
             throw std::invalid_argument("empty gaussian set");
         check_cuda(cudaSetDevice(c.device), "cudaSetDevice");
+        StreamOrder order(c, c.stream);
         const int64_t chunk = std::max<int64_t>(1, std::min<int64_t>(B, c.chunk));
         ensure_work(c, chunk);
         float *d_pos = dalloc<float>(c, size_t(3) * std::max<int64_t>(B, 1));
@@ -1102,6 +1280,7 @@ int swr_setup(swr_ctx *ctx, const float *dc, const float *dr, const float *da, i
     return guarded([&] {
         Ctx &c = ctx->c;
         check_cuda(cudaSetDevice(c.device), "cudaSetDevice");
+        StreamOrder order(c, c.stream);
         const int64_t chunk = std::max<int64_t>(1, std::min<int64_t>(B, c.chunk));
         ensure_work(c, chunk);
         const int n = c.g.n, np = c.g.np;
@@ -1153,6 +1332,7 @@ static void bins_for(Ctx &c, const float *dc, const float *dr, const float *da, 
                      int32_t *tile_prims, int64_t cap, int64_t *n_pairs, float *spectra)
 {
     check_cuda(cudaSetDevice(c.device), "cudaSetDevice");
+    StreamOrder order(c, c.stream);
     const int64_t chunk = std::max<int64_t>(1, std::min<int64_t>(B, c.chunk));
     ensure_work(c, chunk);
     const bool with_res = dc != nullptr;
@@ -1207,6 +1387,7 @@ int swr_heads(swr_ctx *ctx, const float *spectra, int64_t B, double *pooled, int
     return guarded([&] {
         Ctx &c = ctx->c;
         check_cuda(cudaSetDevice(c.device), "cudaSetDevice");
+        StreamOrder order(c, c.stream);
         const int64_t chunk = std::max<int64_t>(1, std::min<int64_t>(B, c.chunk));
         ensure_work(c, chunk);
         const size_t per = size_t(2) * c.g.H * c.g.W;
@@ -1287,6 +1468,7 @@ int swr_metrics_device(swr_ctx *ctx, const float *d_pred, const float *d_target,
             return;
         check_cuda(cudaSetDevice(c.device), "cudaSetDevice");
         cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : c.stream;
+        StreamOrder order(c, st);
         const int64_t chunk = std::max<int64_t>(1, std::min<int64_t>(B, c.chunk));
         metrics_workspace(c, int(chunk));
         check_cuda(cudaMemsetAsync(c.w.met_bad, 0, sizeof(int), st), "memset");
@@ -1314,6 +1496,7 @@ int swr_metrics(swr_ctx *ctx, const float *pred, const float *target, int64_t B,
         if (B == 0)
             return;
         check_cuda(cudaSetDevice(c.device), "cudaSetDevice");
+        StreamOrder order(c, c.stream);
         cudaStream_t st = c.stream;
         const int64_t chunk = std::max<int64_t>(1, std::min<int64_t>(B, c.chunk));
         metrics_workspace(c, int(chunk));
@@ -1358,6 +1541,7 @@ int swr_evaluate(swr_ctx *ctx, const float *pos_m, const float *target, int64_t 
         if (B == 0)
             return;
         check_cuda(cudaSetDevice(c.device), "cudaSetDevice");
+        StreamOrder order(c, c.stream);
         cudaStream_t st = c.stream;
         const int64_t chunk = std::max<int64_t>(1, std::min<int64_t>(B, c.chunk));
         ensure_work(c, chunk);
@@ -1445,6 +1629,7 @@ int swr_rasterize_backward(swr_ctx *ctx, const float *dc, const float *dr, const
         if (B == 0)
             return;
         check_cuda(cudaSetDevice(c.device), "cudaSetDevice");
+        StreamOrder order(c, c.stream);
         cudaStream_t st = c.stream;
         const int64_t chunk = std::max<int64_t>(1, std::min<int64_t>(B, c.chunk));
         ensure_work(c, chunk);
@@ -1525,6 +1710,7 @@ int swr_hybrid_loss(swr_ctx *ctx, const float *pred, const float *target, int64_
         if (B == 0)
             return;
         check_cuda(cudaSetDevice(c.device), "cudaSetDevice");
+        StreamOrder order(c, c.stream);
         cudaStream_t st = c.stream;
         const int64_t chunk = std::max<int64_t>(1, std::min<int64_t>(B, c.chunk));
         metrics_workspace(c, int(chunk));

@@ -8,6 +8,7 @@
 #include <algorithm>
 #include <array>
 #include <functional>
+#include <memory>
 #include <mutex>
 #include <stdexcept>
 #include <string>
@@ -102,6 +103,8 @@ struct Work
     int64_t *host_pairs = nullptr; // pinned mirror of stats
 };
 
+struct HostScene;
+
 struct Ctx
 {
     int device = 0;
@@ -115,8 +118,11 @@ struct Ctx
     int tile = 16;
     int mlp_precision = 0;
     int chunk = 256;
+    int chunk_cap = 1 << 30;            // largest chunk whose pair list fits 32-bit offsets (pair_bound)
+    int64_t pairs_per_pos_max = 1;      // pair_bound: (tile, primitive) pairs of one position, any residuals
     bool stage_timing = false;
     double rssi_slope = 1.0, rssi_intercept = 0.0;
+    bool rssi_calibrated = false; // from the WRFC trailer or set through the options
     cudaStream_t stream = nullptr;
     Work w;
     int64_t launches = 0;
@@ -126,6 +132,9 @@ struct Ctx
     std::vector<std::array<cudaEvent_t, 7>> stage_pending; // recorded per chunk, read lazily
     std::vector<void *> allocs;
     void *host_stage = nullptr; // persistent staging of the host-buffer API (capi.cpp)
+    std::shared_ptr<const HostScene> host; // the scene as loaded (reference layouts), for swr_scene_get_*
+    cudaEvent_t order_ev = nullptr; // last work of the previous C-ABI call (StreamOrder, capi.cpp)
+    bool order_pending = false;
 };
 
 void check_cuda(cudaError_t e, const char *what);
@@ -184,6 +193,8 @@ struct HostScene
     uint64_t manifest_hash = 0; // checkpoint.cpp:40,133 (hex string in the trailer)
     std::string config_json;    // trailer "config" object (checkpoint.cpp:36), WRFC files only
     int64_t iteration = 0;      // trailer "iteration"
+    bool has_rssi = false;      // trailer rssi_slope / rssi_intercept (save_rssi_model, tasks.cpp:131-150)
+    double rssi_slope = 1.0, rssi_intercept = 0.0;
 };
 
 // ------------------------------------------------------------ training (k_train.cu, train.cpp)

@@ -46,6 +46,7 @@ class Scene:
     tile: int = 16
     bbox_min: tuple = (0.0, 0.0, 0.0)
     bbox_max: tuple = (1.0, 1.0, 1.0)
+    rssi_cal: tuple | None = None  # (slope, intercept) of an RSSI model (tasks.cpp:131-150)
 
     @property
     def n(self) -> int:
@@ -88,11 +89,14 @@ def write_wrfc(path: str, sc: Scene) -> None:
         wrfd += struct.pack("<II", w.shape[0], w.shape[1])
     for w, b in zip(sc.weights, sc.biases):
         wrfd += f32(w) + f32(b)
-    trailer = json.dumps({
+    tj = {
         "config": _config_json(sc), "iteration": 0, "manifest_hash": "0000000000000000",
         "grid": {"n_elevation": sc.H, "n_azimuth": sc.W},
         "bbox_min": list(map(float, sc.bbox_min)), "bbox_max": list(map(float, sc.bbox_max)),
-    }, separators=(",", ":")).encode()
+    }
+    if sc.rssi_cal is not None:  # save_rssi_model's extra keys (tasks.cpp:131-137)
+        tj["rssi_slope"], tj["rssi_intercept"] = float(sc.rssi_cal[0]), float(sc.rssi_cal[1])
+    trailer = json.dumps(tj, separators=(",", ":")).encode()
     head = 16 + 3 * 16
     offs = [head, head + len(wrf2), head + len(wrf2) + len(wrfd)]
     sizes = [len(wrf2), len(wrfd), len(trailer)]
@@ -138,7 +142,9 @@ def read_wrfc(path: str) -> Scene:
     return Scene(H=tj["grid"]["n_elevation"], W=tj["grid"]["n_azimuth"], center_raw=cr, cholesky=ch,
                  atten_logit=at, response=rs, width=width, bands_c=bc, bands_p=bp, weights=ws, biases=bs,
                  cutoff=float(cfg.get("cutoff_radius", 3.0)), tile=int(cfg.get("tile", 16)),
-                 bbox_min=tuple(tj["bbox_min"]), bbox_max=tuple(tj["bbox_max"]))
+                 bbox_min=tuple(tj["bbox_min"]), bbox_max=tuple(tj["bbox_max"]),
+                 rssi_cal=(tj["rssi_slope"], tj["rssi_intercept"]) if "rssi_slope" in tj and "rssi_intercept" in tj
+                 else None)
 
 
 # ----------------------------------------------------------- synthetic scenes

@@ -179,7 +179,11 @@ class Checkpoint:
                                       sc.bands_p, C.cast(lw, C.c_void_p) if lw else None,
                                       C.cast(lb, C.c_void_p) if lb else None, C.c_float(sc.cutoff), sc.tile,
                                       bmin.ctypes.data, bmax.ctypes.data, device, C.byref(h)))
-        return cls(h.value)
+        ck = cls(h.value)
+        if getattr(sc, "rssi_cal", None) is not None:
+            ck.set_option("rssi_slope", sc.rssi_cal[0])
+            ck.set_option("rssi_intercept", sc.rssi_cal[1])
+        return ck
 
     def set_manifest_hash(self, h: int) -> None:
         """Fingerprint of the dataset this scene was trained on (checkpoint.cpp:133)."""
@@ -226,6 +230,21 @@ def load_checkpoint(path: str, device: int = 0) -> Checkpoint:
     h = C.c_void_p()
     _check(lib().swr_scene_create_wrfc(path.encode(), device, C.byref(h)))
     return Checkpoint(h.value)
+
+
+def wrfc_peek(path: str) -> dict:
+    """Header + trailer of a WRFC file without a device (swr_wrfc_peek): grid, n,
+    net dims, raster params, bbox, and the RSSI calibration of an RSSI model."""
+    info = _Info()
+    cal = np.zeros(2, np.float64)
+    has = C.c_int(0)
+    L = lib()
+    L.swr_wrfc_peek.argtypes = [C.c_char_p, C.c_void_p, C.c_void_p, C.c_void_p]
+    _check(L.swr_wrfc_peek(path.encode(), C.addressof(info), cal.ctypes.data, C.addressof(has)))
+    return dict(H=info.n_elevation, W=info.n_azimuth, n=info.n, width=info.width, bands_center=info.bands_center,
+                bands_position=info.bands_position, cutoff=info.cutoff_radius, tile=info.tile,
+                bbox_min=tuple(info.bbox_min), bbox_max=tuple(info.bbox_max),
+                rssi_cal=(float(cal[0]), float(cal[1])) if has.value else None)
 
 
 def normalize_position(ck: Checkpoint, pos) -> np.ndarray:

@@ -22,6 +22,8 @@ Fixtures:
                          stream replayed in the shim (acceptance.cpp:130-147, 159-199), with
                          the reference's tiled float rasterize and the criterion's FP64 dense
                          oracle (acceptance.cpp:53-109) for each
+  rssi_model_w32.wrfc    scene_w32 saved as an RSSI model by the reference's save_rssi_model
+                         (tasks.cpp:131-137): rssi_slope / rssi_intercept in the trailer
 """
 import os
 import sys
@@ -98,7 +100,15 @@ def main():
         c[f"{i}_out"] = out
     np.savez_compressed(os.path.join(HERE, "criterion1.npz"), **c)
     criterion1_ref()
+    rssi_model()
     print("golden fixtures written")
+
+
+def rssi_model():
+    ref = O.Reference(path=os.path.join(HERE, "scene_w32.wrfc"))
+    out = os.path.join(HERE, "rssi_model_w32.wrfc")
+    ref.save_rssi_model(out, 17.25, -58.5)
+    assert ref.load_rssi_model(out) == (17.25, -58.5)
 
 
 def criterion1_ref():
@@ -117,7 +127,7 @@ def criterion1_ref():
 
 
 if __name__ == "__main__":
-    if sys.argv[1:] == ["criterion1_ref"]:
-        criterion1_ref()
+    if sys.argv[1:]:  # one fixture by name, e.g. `criterion1_ref` or `rssi_model`
+        globals()[sys.argv[1]]()
     else:
         main()

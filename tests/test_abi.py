@@ -76,3 +76,16 @@ def test_host_side_validation_needs_no_device(tmp_path):
     assert lib.swr_dataset_open(str(tmp_path / "nope").encode(), C.byref(out)) == 2
     with pytest.raises(TypeError):
         swr.TrainConfig(not_a_field=1)
+
+
+def test_wrfc_peek_reads_rssi_calibration_without_a_device():
+    """The trailer of an RSSI model written by the reference's save_rssi_model
+    (tasks.cpp:131-137) carries the affine calibration load_rssi_model reads
+    (tasks.cpp:139-150); a plain checkpoint has none."""
+    gold = os.path.join(ROOT, "tests", "golden")
+    m = swr.wrfc_peek(os.path.join(gold, "rssi_model_w32.wrfc"))
+    assert m["rssi_cal"] == (17.25, -58.5)
+    assert (m["H"], m["W"], m["n"], m["width"]) == (90, 360, 600, 32)
+    assert swr.wrfc_peek(os.path.join(gold, "scene_w32.wrfc"))["rssi_cal"] is None
+    with pytest.raises(swr.SwrError):
+        swr.wrfc_peek(os.path.join(gold, "make_golden.py"))

@@ -42,6 +42,7 @@ def synthetic_residuals(sc, B, seed):
 def big(request):
     n = request.param
     sc = make_scene(n, seed=40 + n // 10000)
+    sc.rssi_cal = (12.5, -61.0)
     ck = swr.Checkpoint.from_scene(sc)
     if n == 10000:
         ck.set_option("chunk", 128)    # the default (1024) would hold all 300 positions in one chunk

@@ -31,7 +31,9 @@ def spec_tol(want):
 
 @pytest.fixture(scope="module")
 def scene2k():
-    return make_scene(2000, seed=1)
+    sc = make_scene(2000, seed=1)
+    sc.rssi_cal = (12.5, -61.0)   # an RSSI model's affine calibration (tasks.cpp:109)
+    return sc
 
 
 @pytest.fixture(scope="module")
@@ -287,6 +289,36 @@ def test_golden_vectors_from_reference(tmp_path):
     cb = swr.bins(ck, None)
     np.testing.assert_array_equal(cb[0][0], g["canonical_tile_offset"])
     np.testing.assert_array_equal(cb[0][1], g["canonical_tile_prims"])
+
+
+def test_rssi_model_from_reference_trailer():
+    """An RSSI model saved by the reference (save_rssi_model): the calibration comes
+    from its trailer (load_rssi_model, tasks.cpp:139-150) and RSSI is
+    slope * pooled + intercept (eval_rssi, tasks.cpp:109), pooled matching the
+    reference's pooled_magnitude of its own render_at within 1e-5."""
+    ck = swr.load_checkpoint(os.path.join(GOLD, "rssi_model_w32.wrfc"))
+    assert ck.get_option("rssi_calibrated") == 1
+    assert (ck.get_option("rssi_slope"), ck.get_option("rssi_intercept")) == (17.25, -58.5)
+    g = np.load(os.path.join(GOLD, "golden_w32.npz"))
+    out = swr.render(ck, g["pos_m"], rssi=True)
+    np.testing.assert_allclose(out["rssi"], 17.25 * out["pooled"] - 58.5, rtol=1e-15, atol=0)
+    np.testing.assert_allclose(out["pooled"], g["pooled"], rtol=1e-5)
+    np.testing.assert_allclose(out["rssi"], 17.25 * g["pooled"] - 58.5, rtol=1e-5)
+
+
+def test_rssi_requires_a_calibration():
+    """A plain checkpoint is not an RSSI model: asking for RSSI fails the way
+    load_rssi_model does (runtime_error), until the calibration is set."""
+    ck = swr.load_checkpoint(os.path.join(GOLD, "scene_w32.wrfc"))
+    assert ck.get_option("rssi_calibrated") == 0
+    pos = random_positions(2, seed=1)
+    with pytest.raises(swr.SwrError):
+        swr.render(ck, pos, rssi=True)
+    swr.render(ck, pos)            # everything else renders
+    ck.set_option("rssi_slope", 2.0)
+    ck.set_option("rssi_intercept", 1.0)
+    out = swr.render(ck, pos, rssi=True)
+    np.testing.assert_allclose(out["rssi"], 2.0 * out["pooled"] + 1.0, rtol=1e-15)
 
 
 def test_chunking_invariance(scene2k):
