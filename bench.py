@@ -165,8 +165,14 @@ def parity_check(ck, scene, pos, idx, spectra, pooled, aoa_rc):
         mx = max(mx, float(err.max()) - tol(want))
         prel = max(prel, abs(float(pooled[k]) - float(rp[k])) / max(abs(float(rp[k])), 1e-300))
         if tuple(aoa_rc[k]) != tuple(rrc[k]):
-            mag = np.sort(np.hypot(want[..., 0].astype(np.float64), want[..., 1]).ravel())[-2:]
-            aoa_ok &= bool(mag[1] - mag[0] <= tol(want))
+            # a different cell is acceptable only if the reference's magnitude there is
+            # within the two-sided bar of its maximum (a near-tie)
+            mag = np.hypot(want[..., 0].astype(np.float64), want[..., 1])
+            gap = float(mag.max() - mag[int(aoa_rc[k][0]), int(aoa_rc[k][1])])
+            aoa_ok &= bool(gap <= 2 * tol(want))
+            out.setdefault("aoa_mismatch", []).append(
+                {"position": int(idx[k]), "gpu": [int(v) for v in aoa_rc[k]], "ref": [int(v) for v in rrc[k]],
+                 "gap_over_tol": gap / tol(want)})
     out.update({"e2e_cells_within_tol": within, "e2e_max_excess_over_tol": mx,
                 "flip_bound": float(np.exp(-4.5) * kmax), "pooled_max_rel": prel, "aoa_ok": aoa_ok,
                 "reference": "oracle/_ref (reference sources), position-parallel render_at"})
@@ -225,6 +231,98 @@ def config_dict(args, scene):
             "l2": "per-step working set (spectra 265 MB + bins ~1 GB) exceeds the 126 MB L2"}
 
 
+def spec_sized_record(args, world, rank, dist, local, flush):
+    """North-star configuration (BASELINE.json: >= 100k spectra/s for a SPEC.md-sized
+    Gaussian set, 10k Gaussians = TrainConfig's default, training.hpp:98) measured in
+    the same run as the headline: 1024 positions per GPU, spectra + RSSI + AoA, same
+    device-timed protocol (L2 flushed between steps, CUDA events, max over ranks) and
+    the same end-to-end host-buffer leg."""
+    import torch
+    from paper_2506_12787_b200 import swr
+    from paper_2506_12787_b200.scene import make_scene, random_positions
+    from paper_2506_12787_b200.shard import max_over_ranks
+    sc = make_scene(10000, seed=0, width=156)
+    sc.rssi_cal = (12.5, -61.0)
+    ck = swr.Checkpoint.from_scene(sc, device=local)
+    ck.set_option("mlp_precision", {"fp32": 0, "fp16x3": 1, "fp16": 2}[args.precision])
+    B = 1024
+    pos = np.ascontiguousarray(random_positions(B * world, seed=7)[rank * B:(rank + 1) * B])
+    stream = torch.cuda.Stream()
+    d_pos = torch.from_numpy(pos).cuda()
+    H, W = sc.H, sc.W
+    d_spec = torch.empty((B, H, W, 2), dtype=torch.float32, device="cuda")
+    d_pooled = torch.empty(B, dtype=torch.float64, device="cuda")
+    d_rssi = torch.empty(B, dtype=torch.float64, device="cuda")
+    d_rc = torch.empty((B, 2), dtype=torch.int32, device="cuda")
+    d_ang = torch.empty((B, 2), dtype=torch.float64, device="cuda")
+    flags = swr.OUT_SPECTRA | swr.OUT_POOLED | swr.OUT_RSSI | swr.OUT_AOA
+
+    def step():
+        swr.render_device(ck, d_pos.data_ptr(), B, flags, d_spec.data_ptr(), d_pooled.data_ptr(),
+                          d_rssi.data_ptr(), d_rc.data_ptr(), d_ang.data_ptr(), stream.cuda_stream)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    ck.set_option("stage_timing", 1)
+    ck.set_option("stage_reset", 1)
+    ms = []
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize()
+    for _ in range(args.steps):
+        with torch.cuda.stream(stream):
+            flush.fill_(1.0)
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+        step()
+        with torch.cuda.stream(stream):
+            e1.record(stream)
+        e1.synchronize()
+        ms.append(e0.elapsed_time(e1))
+    torch.cuda.synchronize()
+    total_ms = max_over_ranks(float(sum(ms)), device="cuda")
+    ck.set_option("stage_timing", 0)
+    stages = ck.stage_times() / float(args.steps)
+    h_pos = torch.from_numpy(pos).pin_memory()
+    h_spec = torch.empty((B, H, W, 2), dtype=torch.float32).pin_memory()
+    h_rc = torch.empty((B, 2), dtype=torch.int32).pin_memory()
+    h_ang = torch.empty((B, 2), dtype=torch.float64).pin_memory()
+    h_pooled = torch.empty(B, dtype=torch.float64).pin_memory()
+    h_rssi = torch.empty(B, dtype=torch.float64).pin_memory()
+    L = swr.lib()
+
+    def host_step():
+        swr._check(L.swr_render(ck.handle, h_pos.data_ptr(), B, flags, h_spec.data_ptr(), h_pooled.data_ptr(),
+                                h_rssi.data_ptr(), h_rc.data_ptr(), h_ang.data_ptr()))
+
+    host_step()
+    if dist:
+        dist.barrier()
+    t0 = time.perf_counter()
+    for _ in range(max(1, args.steps)):
+        host_step()
+    e2e_s = max_over_ranks(time.perf_counter() - t0, device="cuda")
+    out = {"workload": "north_star: SPEC.md-sized set, 10000 Gaussians (training.hpp:98), 1024 TX positions per GPU, "
+                       "90x360 grid, spectra + RSSI + AoA",
+           "gaussians": sc.n, "positions_per_gpu": B, "chunk": int(ck.get_option("chunk")),
+           "value": B * world * args.steps / (total_ms / 1e3), "unit": "spectra/s",
+           "ms_per_step": total_ms / args.steps, "target": 100000.0,
+           "stage_ms": {k: round(float(v), 3) for k, v in zip(["pos_prep", "mlp", "setup", "bin", "raster", "heads"],
+                                                             stages)},
+           "e2e": {"value": B * world * max(1, args.steps) / e2e_s, "unit": "spectra/s",
+                   "h2d_bytes_per_step": int(pos.nbytes) * world,
+                   "d2h_bytes_per_step": world * int(B * H * W * 2 * 4 + B * (8 + 8 + 8 + 16))}}
+    if rank == 0 and not args.no_parity:
+        idx = np.array([0, B - 1])
+        par = parity_check(ck, sc, pos, idx, d_spec[idx].cpu().numpy(), d_pooled[idx].cpu().numpy(),
+                           d_rc[idx].cpu().numpy())
+        out["parity_ok"] = par["ok"]
+        out["parity"] = par
+    return out
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -245,6 +343,8 @@ def main():
                     help="positions per device chunk (default: the library's, ~12.8M Gaussian-position rows)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-parity", action="store_true", help="skip the post-timing oracle check of sampled outputs")
+    ap.add_argument("--no-spec-sized", action="store_true",
+                    help="config 2: skip the extra north-star line (10k Gaussians x 1024 positions, same run)")
     ap.add_argument("--verify", action="store_true",
                     help="N > 1: rank 0 re-renders every rank's positions and checks the gathered spectra bitwise")
     args = ap.parse_args()
@@ -321,7 +421,10 @@ def main():
     d_rc = torch.empty((B, 2), dtype=torch.int32, device="cuda")
     d_ang = torch.empty((B, 2), dtype=torch.float64, device="cuda")
     aoa_only = args.config == 4
-    flags = (swr.OUT_AOA | swr.OUT_POOLED) if aoa_only else (swr.OUT_SPECTRA | swr.OUT_POOLED | swr.OUT_RSSI)
+    # spectra + RSSI (config 2's outputs) and the AoA peak derived from them (north_star):
+    # the heads share the raster's per-tile partials, so AoA costs one tiny kernel
+    flags = (swr.OUT_AOA | swr.OUT_POOLED) if aoa_only else (swr.OUT_SPECTRA | swr.OUT_POOLED | swr.OUT_RSSI
+                                                            | swr.OUT_AOA)
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device="cuda")
 
     # N > 1, full spectra: the one collective (outputs to rank 0 over NVLink, NCCL
@@ -429,6 +532,10 @@ def main():
     e2e_s = max_over_ranks(time.perf_counter() - t0, device="cuda")
     e2e_value = total * max(1, args.steps) / e2e_s
 
+    spec = None
+    if args.config == 2 and not args.no_spec_sized and (args.n or 0) != 10000:
+        spec = spec_sized_record(args, world, rank, dist, local, flush)
+
     if rank != 0:
         if dist:
             dist.destroy_process_group()
@@ -497,11 +604,13 @@ def main():
         "parity_ok": None if parity is None else parity["ok"],
         "parity": parity,
         "e2e": {"value": e2e_value, "unit": "spectra/s", "h2d_bytes_per_step": int(pos.nbytes) * world,
-                "d2h_bytes_per_step": world * (int(B * (16 + 8)) if aoa_only else int(B * H * W * 2 * 4 + 2 * B * 8)),
+                "d2h_bytes_per_step": world * (int(B * (16 + 8)) if aoa_only else int(B * H * W * 2 * 4 + B * (8 + 8 + 8 + 16))),
                 "path": "swr_render (C ABI) with pinned host buffers per rank, H2D positions + D2H outputs inside"},
         "gpu_launches": int(launches),
         "clocks": clk.summary(),
     }
+    if spec is not None:
+        out["spec_sized"] = spec
     print(json.dumps(out), flush=True)
     if dist:
         dist.destroy_process_group()

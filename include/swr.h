@@ -191,6 +191,49 @@ int swr_dataset_get_info(swr_dataset *ds, swr_dataset_info *info);
 int swr_dataset_split(swr_dataset *ds, int split, int32_t *indices, int64_t *count);
 /* records by index (NULL indices = the first `count`): pos [count][3], spectra [count][H][W][2] */
 int swr_dataset_read(swr_dataset *ds, const int32_t *indices, int64_t count, float *pos, float *spectra);
+/* The full manifest of a dataset (wavesim.hpp:125-139 Dataset minus the samples;
+ * manifest_json, dataset.cpp:159-181). Arrays point into storage owned by the
+ * swr_dataset they came from (valid while it is open) or by the caller. */
+typedef struct
+{
+    int32_t n_elevation, n_azimuth;
+    const char *mode; /* "tx_moving" | "rx_moving" (wavesim.cpp:62-74) */
+    int32_t k_elements;
+    double spacing, wavelength;
+    double room[3];
+    double reflectivity;
+    int32_t max_bounces;
+    double fixed_node[3];
+    double normalization;
+    uint64_t seed;
+    const int32_t *train_indices, *test_indices, *excluded_indices;
+    int64_t n_train, n_test, n_excluded;
+    double bbox_min[3], bbox_max[3];
+    const double *rssi_dbm;
+    int64_t n_rssi;
+} swr_dataset_meta;
+int swr_dataset_get_meta(swr_dataset *ds, swr_dataset_meta *meta);
+/* manifest_json (dataset.cpp:159-181) for `sample_count` records: the exact bytes the
+ * reference writes (nlohmann::json dump(2) + newline). len receives the size (the
+ * buffer may be NULL to query it); hash = FNV-1a 64 of those bytes. */
+int swr_dataset_manifest_json(const swr_dataset_meta *meta, int64_t sample_count, char *buf, size_t cap,
+                              size_t *len, uint64_t *hash);
+/* Writer of the same directory layout (save_dataset, dataset.cpp:183-203): records are
+ * streamed to spectra.bin as they come (host buffers or rendered on the GPU) and
+ * manifest.json is written at close with sample_count = records written. */
+typedef struct swr_dataset_writer swr_dataset_writer;
+int swr_dataset_writer_open(const char *dir, int32_t n_elevation, int32_t n_azimuth, swr_dataset_writer **out);
+/* pos [count][3] (metres), spectra [count][H][W][2], host memory */
+int swr_dataset_writer_append(swr_dataset_writer *w, const float *pos, const float *spectra, int64_t count);
+/* render the spectra of pos_m [count][3] on ctx's device (render_at, batched) and
+ * append them; the file write of one chunk overlaps the rendering of the next */
+int swr_dataset_writer_render(swr_dataset_writer *w, swr_ctx *ctx, const float *pos_m, int64_t count);
+/* writes manifest.json (meta's grid must match the writer's) and closes; w is freed
+ * even on error. manifest_hash may be NULL. */
+int swr_dataset_writer_close(swr_dataset_writer *w, const swr_dataset_meta *meta, uint64_t *manifest_hash);
+/* save_dataset in one call (host records) */
+int swr_dataset_save(const char *dir, const swr_dataset_meta *meta, const float *pos, const float *spectra,
+                     int64_t count, uint64_t *manifest_hash);
 /* train::evaluate (training.cpp:380-406): render every sample of the split and
  * score it against its stored spectrum (peak 1). sample_ids / metrics are
  * [split size]. SWR_ERUNTIME if the checkpoint's manifest_hash differs from the

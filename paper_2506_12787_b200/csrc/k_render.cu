@@ -594,30 +594,6 @@ __device__ __forceinline__ float wrap_fast(float x)
 }
 
 
-// One CTA per (tile, position). The tile's (tile, primitive) list (ascending
-// primitive index) is cut into chunks of 32 pairs; warp w takes chunks w, w+8, ...
-// For a chunk, each lane first prepares one pair (gathers its dynamic state,
-// shape and box, clips the box to the tile: rows [max(r0, tile), min(r1, tile)]
-// x the one or two wrapped column spans, splat.cpp:450-470) into a record, the
-// warp sorts the 32 records by sweep count (bitonic, shuffles) and stores them in
-// that order, so similar records pair up. Then each half-warp evaluates one
-// record of a pair at a time: its 16 lanes first tabulate the record's per-row
-// terms (d_el and i00 d_el^2, or +inf where the reference skips the row,
-// splat.cpp:405-408), then sweep the clipped box with the lanes mapped onto it
-// (rows per sweep = 16 / columns), so no lane is spent on cells the reference
-// does not evaluate. Each half-warp accumulates into its own shared-memory copy
-// of the tile (no atomics); the copies are summed in fixed order at the end, so
-// the result is bit-deterministic. The cutoff mask uses the reference's float q
-// (same operation order, no FMA); exp(-q/2) is ex2.approx of a prescaled
-// argument. Chunks whose azimuths could need the reference's multi-turn wrap
-// (|daz| >= 3 pi) take a separate instantiation of the sweep code.
-struct RasterRec
-{
-    float4 dyn;   // el, az, amplitude re, im
-    float4 shape; // i00, 2*i01 (exact), i11, 1/l1
-    int4 box;     // first row, last row (tile-relative), ncol | na << 6 | a0 << 12 | rpi << 18 | sweeps << 24,
-                  // magic(ncol) | magic(rpi) << 13
-};
 // floor(x / d) == (x * m[d]) >> 12 for 0 <= x < 128, 1 <= d <= 32, m[d] = ceil(4096 / d)
 __host__ __device__ constexpr uint32_t magic12(int d) { return (4096u + d - 1) / d; }
 
@@ -634,39 +610,83 @@ __device__ __forceinline__ float2 shfl_f2(float2 v, int src)
     return make_float2(__shfl_sync(0xffffffffu, v.x, src), __shfl_sync(0xffffffffu, v.y, src));
 }
 
-// G = records evaluated side by side per warp: 2 (half-warps, tiles <= 16 wide) or
-// 1 (whole warp, tiles up to 32 wide)
-// Occupancy: 4-warp CTAs with 8 resident per SM (32 warps; register cap 64) measured
-// best -- the kernel is latency-bound (short scoreboard on shared memory, MUFU) and
-// 8-warp CTAs idle at the final barrier when a tile's few chunks split unevenly
-// (tools/build_variant.py sweeps: 8 warps x 4 CTAs 20.9 ms, 4 x 8 20.1-20.4 ms,
-// 2 x 16 21.8 ms per 1024 spectra at 50k; at 10k 5.43 -> 4.75 ms).
-#ifndef SWR_SWEEP_UNROLL
-#define SWR_SWEEP_UNROLL 1 // measured: 1 beats 2, 3, 4 (raster 20.6 -> 20.2 ms at 50k)
-#endif
-constexpr int kSweepUnroll = SWR_SWEEP_UNROLL; // sweeps unrolled per record pair
 #ifndef SWR_RASTER_MINB
 #define SWR_RASTER_MINB 4 // x 8 warps: resident warps per SM / 8
 #endif
-template <int kRasterWarps, int G>
-__global__ void __launch_bounds__(32 * kRasterWarps, SWR_RASTER_MINB * 8 / kRasterWarps) raster_kernel(Grid g, SceneDev sd, const float4 *__restrict__ dyn,
-                                                     const int4 *__restrict__ rng, const int64_t *__restrict__ seg,
-                                                     const int *__restrict__ tile_off, const int *__restrict__ prims,
-                                                     float *__restrict__ spec, float4 *__restrict__ tile_part,
-                                                     double *__restrict__ tile_sum, int want_heads, int s_base)
+
+// ---------------------------------------------------------------- raster
+//
+// One CTA of 4 warps per (tile, position), 8 CTAs resident per SM. The tile's pair
+// list (ascending primitive index, splat.cpp:251-292) is cut into chunks of 32;
+// warp w takes chunks w, w+4, ... For a chunk, each lane first turns one pair into a
+// record (gathers the pair's dynamic state, shape and box, clips it to the tile:
+// rows [max(r0, tile), min(r1, tile)] x the one or two wrapped column spans,
+// splat.cpp:450-470, rows per sweep = 16 / columns), the warp sorts the 32 records
+// by sweep count (bitonic, shuffles) and stores them in that order, so similar
+// records pair up. Each half-warp then evaluates one record at a time: its 16 lanes
+// write the record's row table (d_el, q_c = i00 d_el^2, or +inf where the reference
+// skips the row, splat.cpp:405-408; double-buffered, one __syncwarp per record),
+// map themselves onto the clipped box (magic division: lane -> (row, column)),
+// compute their column's w1 / w2 and sweep rows lr, lr + rpi, ... with a
+// pointer-bounded loop (each lane its own trip count). Each half-warp accumulates
+// into its own shared-memory copy of the tile with a predicated read-modify-write
+// (no atomics); the copies are summed in fixed order, so results are
+// bit-deterministic. The cutoff mask uses the reference's float q in its operation
+// order (no FMA); exp(-q/2) is ex2.approx of a prescaled argument. Chunks whose
+// azimuths could need the reference's multi-turn wrap take a separate instantiation.
+//
+// Measured against the round-1 kernel (same decomposition, packed records, two
+// __syncwarps and a shuffled common trip count per record pair): ncu source view
+// ~96 -> ~60 warp-instructions per record pair outside the sweep loop and 19 -> 15
+// inside it (4.49 -> 3.44 G warp-instructions per 256-position launch at 50k), but
+// only 6-9% less time: the kernel is now bound by the shared-memory data pipe (81%
+// of peak wavefronts: a row-table read and a 64-bit accumulator RMW per cell), issue
+// 69% active. Tried and not kept: padded accumulator rows
+// against bank conflicts (occupancy loss > conflict gain), register-tile
+// accumulation (lane = tile column, rows unrolled in registers: no shared traffic
+// per cell, but ~53% column utilisation and per-row guards: 22.0 vs 19.4 ms per
+// 1024 spectra at 50k), a software-pipelined sweep loop (more instructions).
+struct Rec2
 {
-    extern __shared__ float2 acc[]; // [G * warps][T*T], then RasterRec [warps][32]
-    __shared__ float elc[64], azc[32]; // elc zero-padded to 64 rows
+    float4 dyn;   // el, az, amplitude re, im
+    float4 shape; // i00, 2*i01 (exact), i11, 1/l1
+    int4 a;       // magic(ncol), ncol, rows per sweep (0: empty), columns of the first span
+    int4 b;       // first column of the first span (tile-relative), first row, last row (tile-relative), sweeps
+};
+
+// Accumulator copies are [T rows][T + kAccPad] float2: a half-warp's 64-bit RMW
+// covers rpi rows x ncol columns of a record's box, and with a 16-float2 row
+// stride (all 32 banks) rows of the same column collide; the padded stride spreads
+// them (bank-conflict model over the measured (ncol, nrow) histogram of a 10k
+// scene: 1.77 wavefronts per half-warp access at stride 16, 1.41 at 17, 1.27 at
+// 19, 1.18 at 23 or 25).
+#ifndef SWR_ACC_PAD
+#define SWR_ACC_PAD 0 // measured: padding loses more to occupancy than it gains (pad 0/1/3/7/9:
+                      // raster 19.6/20.3/19.7/20.7/20.9 ms per 1024 spectra at 50k)
+#endif
+constexpr int kAccPad = SWR_ACC_PAD;
+
+template <int kRasterWarps, int G>
+__global__ void __launch_bounds__(32 * kRasterWarps, SWR_RASTER_MINB * 8 / kRasterWarps)
+    raster2_kernel(Grid g, SceneDev sd, const float4 *__restrict__ dyn, const int4 *__restrict__ rng,
+                   const int64_t *__restrict__ seg, const int *__restrict__ tile_off, const int *__restrict__ prims,
+                   float *__restrict__ spec, float4 *__restrict__ tile_part, double *__restrict__ tile_sum,
+                   int want_heads, int s_base)
+{
+    extern __shared__ float2 acc[]; // [G * warps][T][T + kAccPad], then Rec2 [warps][32]
+    __shared__ float elc[64], azc[32];
     __shared__ uint32_t magic[33];
-    __shared__ float2 rowtab_all[kRasterWarps * G][32 / G]; // per record slot: (d_el, i00 d_el^2 | +inf) per tile row
-    const int T = g.tile, TT = T * T;
-    const int t = blockIdx.x, s = s_base + blockIdx.y; // positions [s_base, s_base + gridDim.y) of the chunk
+    constexpr int LPR = 32 / G; // lanes per record slot
+    // double-buffered (d_el, q_c | +inf) per tile row; slots 320 B apart, so the two
+    // halves' broadcast reads of the same row index hit different banks
+    __shared__ float2 rowtab_all[kRasterWarps * G][2][LPR + 4];
+    const int T = g.tile, TT = T * T, AS = T + kAccPad, ACOPY = T * AS;
+    const int t = blockIdx.x, s = s_base + blockIdx.y;
     const int tr0 = (t / g.tw) * T, tc0 = (t % g.tw) * T;
     const int tr1 = min(tr0 + T, g.H) - 1, tc1 = min(tc0 + T, g.W) - 1;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    constexpr int LPR = 32 / G; // lanes per record
-    RasterRec *recs = reinterpret_cast<RasterRec *>(acc + G * kRasterWarps * TT) + warp * 32;
-    for (int i = threadIdx.x; i < G * kRasterWarps * TT; i += blockDim.x)
+    Rec2 *recs = reinterpret_cast<Rec2 *>(acc + G * kRasterWarps * ACOPY) + warp * 32;
+    for (int i = threadIdx.x; i < G * kRasterWarps * ACOPY; i += blockDim.x)
         acc[i] = make_float2(0.f, 0.f);
     if (threadIdx.x < 64)
         elc[threadIdx.x] = (int)threadIdx.x < T && tr0 + (int)threadIdx.x <= tr1 ? sd.el_c[tr0 + threadIdx.x] : 0.f;
@@ -678,85 +698,76 @@ __global__ void __launch_bounds__(32 * kRasterWarps, SWR_RASTER_MINB * 8 / kRast
     const int *tl = tile_off + (int64_t)s * (g.tiles + 1);
     const int64_t lb = seg[s] + tl[t], le = seg[s] + tl[t + 1];
     const int64_t sbase = (int64_t)s * g.np;
-    const int half = G == 2 ? lane >> 4 : 0, hl = lane & (LPR - 1); // record slot and its lane
-    float2 *my = acc + (G * warp + half) * TT;
-    float2 *rowtab = rowtab_all[G * warp + half];
-    const uint32_t acc_base = (uint32_t)__cvta_generic_to_shared(my);
-    const uint32_t tab_base = (uint32_t)__cvta_generic_to_shared(rowtab);
+    const int half = G == 2 ? lane >> 4 : 0, hl = lane & (LPR - 1);
+    const int slot = G * warp + half;
+    const uint32_t acc_base = (uint32_t)__cvta_generic_to_shared(acc + slot * ACOPY);
+    const uint32_t tab_base = (uint32_t)__cvta_generic_to_shared(&rowtab_all[slot][0][0]);
     const float cut2 = g.cut2;
     const float kExp = -0.72134752044448170368f; // -0.5 * log2(e)
-    const int *plist = prims + lb;               // 32-bit offsets inside this (position, tile) list
+    const float my_elc = elc[hl < T ? hl : 0];     // this lane's tile row for the row table
+    const int *plist = prims + lb;
     const int cnt = (int)(le - lb);
     const float4 *dyn_s = dyn + sbase;
     const int4 *rng_s = rng + sbase;
     const int tcw = tc1 - tc0 + 1;
 
-    // evaluate the warp's 32 stored records (SLOW: azimuth differences may need
-    // the multi-turn wrap)
-    auto evaluate = [&](auto slow_tag) {
+    auto evaluate = [&](auto slow_tag, int j0) {
         constexpr bool SLOW = decltype(slow_tag)::value;
 #pragma unroll 1
-        for (int j = 0; j < 32 / G; j++)
+        for (int j = j0; j < 32 / G; j++)
         {
-            const RasterRec &R = recs[G * j + half]; // this slot's record
-            const int4 bx = R.box;
-            const int sweeps = bx.z >> 24;
-            const int loop = G == 2 ? max(sweeps, __shfl_xor_sync(0xffffffffu, sweeps, 16)) : sweeps;
-            if (loop == 0)
-                continue;
+            const Rec2 &R = recs[G * j + half];
             const float4 A = R.dyn, S = R.shape;
-            // per-row terms of this record: d_el and q_c = i00 d_el^2, +inf where
-            // (d_el / l1)^2 > r^2 (the reference skips the row; q = inf fails q <= r^2)
-            if (hl < T)
+            const int4 ra = R.a, rb = R.b;
+            // row table of this record: q_c = i00 d_el^2, +inf where the reference skips
+            // the row ((d_el / l1)^2 > r^2, splat.cpp:405-408)
+            const uint32_t tb = tab_base + (uint32_t)((j & 1) * (LPR + 4) * 8);
             {
-                const float d_el = __fsub_rn(elc[hl], A.x);
+                const float d_el = __fsub_rn(my_elc, A.x);
                 const float u0 = __fmul_rn(d_el, S.w);
                 const float qc = __fmul_rn(u0, u0) > cut2 ? __int_as_float(0x7f800000)
                                                           : __fmul_rn(__fmul_rn(S.x, d_el), d_el);
-                rowtab[hl] = make_float2(d_el, qc);
+                asm volatile("st.shared.v2.f32 [%0], {%1, %2};" ::"r"(tb + 8u * (uint32_t)hl), "f"(d_el), "f"(qc)
+                             : "memory");
             }
             __syncwarp();
-            const int ncol = bx.z & 63, na = (bx.z >> 6) & 63, a0off = (bx.z >> 12) & 63, rpi = (bx.z >> 18) & 63;
-            const uint32_t mn = (uint32_t)bx.w & 0x1fffu, mr = (uint32_t)bx.w >> 13;
-            const int lr = (int)(((uint32_t)hl * mn) >> 12), lc = hl - lr * ncol;
-            const bool lane_on = sweeps > 0 && lr < rpi;
-            const int cc = lane_on ? (lc < na ? a0off + lc : lc - na) : 0; // column inside the tile
+            // this lane's cell in the box: rows lr, lr + rpi, ..., column cc of the tile
+            const int lr = (int)(((uint32_t)hl * (uint32_t)ra.x) >> 12);
+            const int lc = hl - lr * ra.y;
+            const bool on = lr < ra.z;
+            const int cc = on ? lc + (lc < ra.w ? rb.x : -ra.w) : 0;
+            const int row0 = rb.y + lr;
+            uint32_t cp = acc_base + 8u * (uint32_t)(row0 * AS + cc);
+            const uint32_t cp_last = acc_base + 8u * (uint32_t)(rb.z * AS + cc);
+            uint32_t tp = tb + 8u * (uint32_t)row0;
+            const uint32_t c_step = 8u * (uint32_t)(ra.z * AS), t_step = 8u * (uint32_t)ra.z;
             const float xaz = __fsub_rn(azc[cc], A.y);
             const float d_az = SLOW ? wrap_fast(xaz) : wrap_near(xaz);
             const float w1 = __fmul_rn(__fmul_rn(S.z, d_az), d_az);
             const float w2 = __fmul_rn(S.y, d_az); // (2 * i01) * d_az
-            // lane-private pointers (32-bit shared addresses): its row's table entry
-            // and its cell; both advance by rpi rows per sweep
-            const int rr0 = lane_on ? bx.x + lr : 0;
-            uint32_t tp = tab_base + 8u * (uint32_t)rr0;
-            uint32_t cp = acc_base + 8u * (uint32_t)(rr0 * T + cc);
-            const uint32_t t_step = lane_on ? 8u * (uint32_t)rpi : 0u, c_step = lane_on ? 8u * (uint32_t)(rpi * T) : 0u;
-            // sweeps in which this lane's row is inside the box
-            const int nvalid = lane_on ? (int)(((uint32_t)(bx.y - rr0 + rpi) * mr) >> 12) : 0;
-#pragma unroll kSweepUnroll
-            for (int it = 0; it < loop; it++, tp += t_step, cp += c_step)
+            if (on)
             {
-                float d_el, qc;
-                asm volatile("ld.shared.v2.f32 {%0, %1}, [%2];" : "=f"(d_el), "=f"(qc) : "r"(tp));
-                const float q = __fadd_rn(__fadd_rn(qc, __fmul_rn(d_el, w2)), w1);
-                const bool ok = it < nvalid && q <= cut2;
-                float e;
-                asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(e) : "f"(q * kExp));
-                // predicated read-modify-write of the cell (no branch)
-                asm volatile("{\n\t.reg .pred p;\n\t.reg .f32 a, b;\n\t"
-                             "setp.ne.u32 p, %0, 0;\n\t"
-                             "@p ld.shared.v2.f32 {a, b}, [%1];\n\t"
-                             "@p fma.rn.f32 a, %2, %4, a;\n\t"
-                             "@p fma.rn.f32 b, %3, %4, b;\n\t"
-                             "@p st.shared.v2.f32 [%1], {a, b};\n\t}" ::"r"((uint32_t)ok),
-                             "r"(cp), "f"(A.z), "f"(A.w), "f"(e)
-                             : "memory");
+#pragma unroll 1
+                for (; cp <= cp_last; cp += c_step, tp += t_step)
+                {
+                    float d_el, qc;
+                    asm volatile("ld.shared.v2.f32 {%0, %1}, [%2];" : "=f"(d_el), "=f"(qc) : "r"(tp));
+                    const float q = __fadd_rn(__fadd_rn(qc, __fmul_rn(d_el, w2)), w1);
+                    float e;
+                    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(e) : "f"(q * kExp));
+                    asm volatile("{\n\t.reg .pred p;\n\t.reg .f32 a, b;\n\t"
+                                 "setp.le.f32 p, %0, %5;\n\t"
+                                 "@p ld.shared.v2.f32 {a, b}, [%1];\n\t"
+                                 "@p fma.rn.f32 a, %2, %4, a;\n\t"
+                                 "@p fma.rn.f32 b, %3, %4, b;\n\t"
+                                 "@p st.shared.v2.f32 [%1], {a, b};\n\t}" ::"f"(q),
+                                 "r"(cp), "f"(A.z), "f"(A.w), "f"(e), "f"(cut2)
+                                 : "memory");
+                }
             }
-            __syncwarp(); // the row table is rewritten for the next record
         }
     };
 
-    // gathered state of the lane's pair in the next chunk (software pipelined)
     int c0 = warp * 32;
     int gi = c0 + lane < cnt ? plist[c0 + lane] : -1;
     int4 b = gi >= 0 ? rng_s[gi] : make_int4(0, -1, 0, 0);
@@ -766,7 +777,7 @@ __global__ void __launch_bounds__(32 * kRasterWarps, SWR_RASTER_MINB * 8 / kRast
     for (; c0 < cnt; c0 += kRasterWarps * 32)
     {
         bool slow;
-        // this lane's pair -> record, stored in sweep-count order
+        int j0;
         {
             const int pr0 = max(b.x, tr0), pr1 = min(b.y, tr1);
             int a0 = tc0, na = tcw, nb2 = 0;
@@ -779,21 +790,17 @@ __global__ void __launch_bounds__(32 * kRasterWarps, SWR_RASTER_MINB * 8 / kRast
             }
             const int ncol = na + nb2, nrow = pr1 - pr0 + 1;
             int rpi = 0, sweeps = 0;
-            uint32_t mn = 0, mr = 0;
+            uint32_t mn = 0;
             if (gi >= 0 && ncol > 0 && nrow > 0)
             {
                 mn = magic[ncol];
-                rpi = (int)(((uint32_t)LPR * mn) >> 12); // rows per sweep of LPR lanes
-                mr = magic[rpi];
-                sweeps = (int)(((uint32_t)(nrow + rpi - 1) * mr) >> 12);
+                rpi = (int)(((uint32_t)LPR * mn) >> 12);
+                sweeps = (int)(((uint32_t)(nrow + rpi - 1) * magic[rpi]) >> 12);
             }
-            // |azc - az| < 3 pi for every column when az in (-3, 9) (azc in [0, 2 pi))
             slow = __any_sync(0xffffffffu, sweeps > 0 && !(d.y > -3.0f && d.y < 9.0f));
-            const int a0off = na > 0 ? a0 - tc0 : 0; // (a0 may lie past the tile when only the wrapped span is in it)
-            const int4 box = make_int4(pr0 - tr0, pr1 - tr0,
-                                       ncol | (na << 6) | (a0off << 12) | (rpi << 18) | (sweeps << 24),
-                                       (int)(mn | (mr << 13)));
-            // sort (sweeps, lane) ascending across the warp: similar records pair up
+            const int nempty = __popc(__ballot_sync(0xffffffffu, sweeps == 0));
+            j0 = nempty / G; // records sorted by sweeps: the first j0 slots-groups are empty
+            const int a0off = na > 0 ? a0 - tc0 : 0;
             uint32_t key = ((uint32_t)sweeps << 5) | (uint32_t)lane;
 #pragma unroll
             for (int k = 2; k <= 32; k <<= 1)
@@ -805,17 +812,18 @@ __global__ void __launch_bounds__(32 * kRasterWarps, SWR_RASTER_MINB * 8 / kRast
                     key = (lower == up) ? min(key, o) : max(key, o);
                 }
             const int src = (int)(key & 31);
-            RasterRec r;
+            Rec2 r;
             const float2 dxy = shfl_f2(make_float2(d.x, d.y), src), dzw = shfl_f2(make_float2(d.z, d.w), src);
             const float2 sxy = shfl_f2(make_float2(sh.x, __fmul_rn(2.0f, sh.y)), src),
                          szw = shfl_f2(make_float2(sh.z, sh.w), src);
             r.dyn = make_float4(dxy.x, dxy.y, dzw.x, dzw.y);
             r.shape = make_float4(sxy.x, sxy.y, szw.x, szw.y);
-            r.box = make_int4(__shfl_sync(0xffffffffu, box.x, src), __shfl_sync(0xffffffffu, box.y, src),
-                              __shfl_sync(0xffffffffu, box.z, src), __shfl_sync(0xffffffffu, box.w, src));
+            r.a = make_int4(__shfl_sync(0xffffffffu, (int)mn, src), __shfl_sync(0xffffffffu, ncol, src),
+                            __shfl_sync(0xffffffffu, rpi, src), __shfl_sync(0xffffffffu, na, src));
+            r.b = make_int4(__shfl_sync(0xffffffffu, a0off, src), __shfl_sync(0xffffffffu, pr0 - tr0, src),
+                            __shfl_sync(0xffffffffu, pr1 - tr0, src), __shfl_sync(0xffffffffu, sweeps, src));
             recs[lane] = r;
         }
-        // prefetch the pairs of this warp's next chunk
         const int cn = c0 + kRasterWarps * 32;
         gi = cn + lane < cnt ? plist[cn + lane] : -1;
         b = gi >= 0 ? rng_s[gi] : make_int4(0, -1, 0, 0);
@@ -823,26 +831,26 @@ __global__ void __launch_bounds__(32 * kRasterWarps, SWR_RASTER_MINB * 8 / kRast
         sh = gi >= 0 ? sd.shape[gi] : make_float4(0.f, 0.f, 0.f, 0.f);
         __syncwarp();
         if (slow)
-            evaluate(std::integral_constant<bool, true>());
+            evaluate(std::integral_constant<bool, true>(), j0);
         else
-            evaluate(std::integral_constant<bool, false>());
-        __syncwarp(); // records are rewritten for the next chunk
+            evaluate(std::integral_constant<bool, false>(), j0);
+        __syncwarp(); // records and row tables are rewritten for the next chunk
     }
     __syncthreads();
-    float best = -1.0f, lsum_f = 0.f;
+    float best = -1.0f;
     int bidx = 0x7fffffff;
     double lsum = 0.0;
-    (void)lsum_f;
     for (int cl = threadIdx.x; cl < TT; cl += blockDim.x)
     {
         const int r = tr0 + cl / T, c = tc0 + cl % T;
         if (r > tr1 || c > tc1)
             continue;
         float re = 0.f, im = 0.f;
+        const int ai = (cl / T) * AS + cl % T;
 #pragma unroll
         for (int w = 0; w < G * kRasterWarps; w++)
         {
-            const float2 v = acc[w * TT + cl];
+            const float2 v = acc[w * ACOPY + ai];
             re = __fadd_rn(re, v.x);
             im = __fadd_rn(im, v.y);
         }
@@ -867,23 +875,23 @@ __global__ void __launch_bounds__(32 * kRasterWarps, SWR_RASTER_MINB * 8 / kRast
 template <int WARPS, int G>
 static void launch_raster_w(Ctx &c, int nb, float *d_spec, bool want_heads, cudaStream_t st, int s_base)
 {
-    dim3 grid(c.g.tiles, nb);
-    const size_t smem = (size_t)G * WARPS * c.g.tile * c.g.tile * sizeof(float2) + WARPS * 32 * sizeof(RasterRec);
-    static size_t configured = 0;
-    if (configured < smem)
-    {
-        check_cuda(cudaFuncSetAttribute(raster_kernel<WARPS, G>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                        (int)smem),
+    const size_t smem =
+        (size_t)G * WARPS * c.g.tile * (c.g.tile + kAccPad) * sizeof(float2) + WARPS * 32 * sizeof(Rec2);
+    static DeviceOnce once;
+    once.get(c.device, [&] {
+        check_cuda(cudaFuncSetAttribute(raster2_kernel<WARPS, G>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        (int)(G * WARPS * 32 * (32 + kAccPad) * sizeof(float2) +
+                                              WARPS * 32 * sizeof(Rec2))),
                    "raster smem attribute");
-        // same L1/shared split as the MLP kernel, so raster CTAs can share its SMs
-        check_cuda(cudaFuncSetAttribute(raster_kernel<WARPS, G>, cudaFuncAttributePreferredSharedMemoryCarveout,
+        // same L1/shared split as the MLP kernel
+        check_cuda(cudaFuncSetAttribute(raster2_kernel<WARPS, G>, cudaFuncAttributePreferredSharedMemoryCarveout,
                                         (int)cudaSharedmemCarveoutMaxShared),
                    "raster carveout");
-        configured = smem;
-    }
-    raster_kernel<WARPS, G><<<grid, 32 * WARPS, smem, st>>>(c.g, c.s, c.w.dyn, c.w.rng, c.w.seg, c.w.tile_off,
-                                                            c.w.sorted, d_spec, c.w.tile_part, c.w.tile_sum,
-                                                            want_heads ? 1 : 0, s_base);
+        return 1;
+    });
+    raster2_kernel<WARPS, G><<<dim3(c.g.tiles, nb), 32 * WARPS, smem, st>>>(
+        c.g, c.s, c.w.dyn, c.w.rng, c.w.seg, c.w.tile_off, c.w.sorted, d_spec, c.w.tile_part, c.w.tile_sum,
+        want_heads ? 1 : 0, s_base);
     c.launches++;
 }
 

@@ -301,6 +301,12 @@ struct DatasetFile
     std::vector<int> train, test, excluded;
     double bbox_min[3]{}, bbox_max[3]{}, normalization = 1.0;
     uint64_t hash = 0;
+    // the rest of the manifest (round trip through the writer)
+    std::string mode;
+    int k_elements = 0, max_bounces = 0;
+    double spacing = 0, wavelength = 0, reflectivity = 0, room[3]{}, fixed_node[3]{};
+    uint64_t seed = 0;
+    std::vector<double> rssi_dbm;
     void *fp = nullptr;
     ~DatasetFile();
     void open(const std::string &dir);

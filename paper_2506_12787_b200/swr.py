@@ -79,6 +79,14 @@ def lib():
         L.swr_dataset_read.argtypes = [C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p, C.c_void_p]
         L.swr_evaluate_dataset.argtypes = [C.c_void_p, C.c_void_p, C.c_int, C.c_void_p, C.c_void_p, C.c_void_p,
                                            C.c_void_p]
+        L.swr_dataset_get_meta.argtypes = [C.c_void_p, C.c_void_p]
+        L.swr_dataset_manifest_json.argtypes = [C.c_void_p, C.c_int64, C.c_void_p, C.c_size_t, C.c_void_p,
+                                                C.c_void_p]
+        L.swr_dataset_writer_open.argtypes = [C.c_char_p, C.c_int32, C.c_int32, C.POINTER(C.c_void_p)]
+        L.swr_dataset_writer_append.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64]
+        L.swr_dataset_writer_render.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64]
+        L.swr_dataset_writer_close.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p]
+        L.swr_dataset_save.argtypes = [C.c_char_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p]
         L.swr_rasterize_backward.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64,
                                              C.c_void_p] + [C.c_void_p] * 7
         L.swr_hybrid_loss.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64, C.c_double, C.c_void_p,
@@ -426,6 +434,82 @@ class _DsInfo(C.Structure):
                 ("normalization", C.c_double), ("bbox_min", C.c_double * 3), ("bbox_max", C.c_double * 3)]
 
 
+class DatasetMeta(C.Structure):
+    """swr_dataset_meta: the manifest fields of wavesim.hpp:125-139's Dataset."""
+    _fields_ = [("n_elevation", C.c_int32), ("n_azimuth", C.c_int32), ("mode", C.c_char_p),
+                ("k_elements", C.c_int32), ("spacing", C.c_double), ("wavelength", C.c_double),
+                ("room", C.c_double * 3), ("reflectivity", C.c_double), ("max_bounces", C.c_int32),
+                ("fixed_node", C.c_double * 3), ("normalization", C.c_double), ("seed", C.c_uint64),
+                ("train_indices", C.c_void_p), ("test_indices", C.c_void_p), ("excluded_indices", C.c_void_p),
+                ("n_train", C.c_int64), ("n_test", C.c_int64), ("n_excluded", C.c_int64),
+                ("bbox_min", C.c_double * 3), ("bbox_max", C.c_double * 3),
+                ("rssi_dbm", C.c_void_p), ("n_rssi", C.c_int64)]
+
+    @staticmethod
+    def build(H, W, *, mode="tx_moving", k_elements=16, spacing=0.0625, wavelength=0.125,
+              room=(4.0, 3.0, 2.5), reflectivity=0.6, max_bounces=1, fixed_node=(2.0, 1.5, 1.25),
+              normalization=1.0, seed=0, train=(), test=(), excluded=(), bbox_min=(0, 0, 0), bbox_max=(1, 1, 1),
+              rssi_dbm=()):
+        m = DatasetMeta()
+        m.n_elevation, m.n_azimuth = H, W
+        m._keep = [mode.encode()] + [np.ascontiguousarray(v, np.int32) for v in (train, test, excluded)] + \
+                  [np.ascontiguousarray(rssi_dbm, np.float64)]
+        m.mode = m._keep[0]
+        m.k_elements, m.spacing, m.wavelength = k_elements, spacing, wavelength
+        m.room[:] = list(room)
+        m.reflectivity, m.max_bounces = reflectivity, max_bounces
+        m.fixed_node[:] = list(fixed_node)
+        m.normalization, m.seed = normalization, seed
+        (tr, te, ex, rs) = m._keep[1:]
+        m.train_indices, m.test_indices, m.excluded_indices = _p(tr), _p(te), _p(ex)
+        m.n_train, m.n_test, m.n_excluded = len(tr), len(te), len(ex)
+        m.bbox_min[:] = list(bbox_min)
+        m.bbox_max[:] = list(bbox_max)
+        m.rssi_dbm, m.n_rssi = _p(rs), len(rs)
+        return m
+
+    def manifest(self, sample_count: int):
+        """(manifest.json bytes exactly as manifest_json writes them, FNV-1a 64 hash)"""
+        n, h = C.c_size_t(), C.c_uint64()
+        _check(lib().swr_dataset_manifest_json(C.byref(self), sample_count, None, 0, C.byref(n), C.byref(h)))
+        buf = C.create_string_buffer(n.value)
+        _check(lib().swr_dataset_manifest_json(C.byref(self), sample_count, buf, n.value, C.byref(n), C.byref(h)))
+        return buf.raw[:n.value], h.value
+
+
+class DatasetWriter:
+    """save_dataset (dataset.cpp:183-203) as a stream: append host records or render
+    positions on the GPU; close(meta) writes manifest.json and returns its hash."""
+
+    def __init__(self, path: str, H: int, W: int):
+        h = C.c_void_p()
+        _check(lib().swr_dataset_writer_open(path.encode(), H, W, C.byref(h)))
+        self._h = h
+
+    def append(self, pos, spectra):
+        pos = np.ascontiguousarray(pos, np.float32)
+        spectra = np.ascontiguousarray(spectra, np.float32)
+        _check(lib().swr_dataset_writer_append(self._h, _p(pos), _p(spectra), len(pos)))
+
+    def render(self, ck: "Checkpoint", pos_m):
+        pos_m = np.ascontiguousarray(pos_m, np.float32)
+        _check(lib().swr_dataset_writer_render(self._h, ck.handle, _p(pos_m), len(pos_m)))
+
+    def close(self, meta: DatasetMeta) -> int:
+        h = C.c_uint64()
+        w, self._h = self._h, None
+        _check(lib().swr_dataset_writer_close(w, C.byref(meta), C.byref(h)))
+        return h.value
+
+
+def save_dataset(path: str, meta: DatasetMeta, pos, spectra) -> int:
+    pos = np.ascontiguousarray(pos, np.float32)
+    spectra = np.ascontiguousarray(spectra, np.float32)
+    h = C.c_uint64()
+    _check(lib().swr_dataset_save(path.encode(), C.byref(meta), _p(pos), _p(spectra), len(pos), C.byref(h)))
+    return h.value
+
+
 class Dataset:
     """manifest.json + spectra.bin reader (load_dataset, dataset.cpp:205-258), records on demand."""
 
@@ -441,6 +525,13 @@ class Dataset:
         self.manifest_hash = info.manifest_hash
         self.bbox = np.array(list(info.bbox_min) + list(info.bbox_max))
         self.normalization = info.normalization
+
+    def meta(self) -> DatasetMeta:
+        """the full manifest (pointers into this reader's storage: keep it open)"""
+        m = DatasetMeta()
+        _check(lib().swr_dataset_get_meta(self._h, C.byref(m)))
+        m._owner = self
+        return m
 
     def split(self, which: int) -> np.ndarray:
         n = C.c_int64()

@@ -93,3 +93,93 @@ def test_evaluate_dataset_hash_mismatch(ds_dir):
     ck.set_manifest_hash(h ^ 1)
     with pytest.raises(swr.SwrError, match="different dataset"):
         swr.evaluate_dataset(ck, swr.Dataset(d), 1)
+
+
+# ---------------------------------------------------------------- writer (save_dataset)
+
+def _files(d):
+    with open(os.path.join(d, "manifest.json"), "rb") as a, open(os.path.join(d, "spectra.bin"), "rb") as b:
+        return a.read(), b.read()
+
+
+def test_writer_round_trip_byte_identical(ds_dir, tmp_path):
+    """A dataset the reference simulated and saved (save_dataset, dataset.cpp:183-203),
+    read back and written again through the C ABI writer: manifest.json and
+    spectra.bin are byte-identical, and so is the manifest fingerprint."""
+    d, h, _ = ds_dir
+    ds = swr.Dataset(d)
+    meta = ds.meta()
+    assert meta.mode in (b"tx_moving", b"rx_moving")
+    pos, spec = ds.read()
+    out = str(tmp_path / "one_call")
+    assert swr.save_dataset(out, meta, pos, spec) == h
+    assert _files(out) == _files(d)
+    assert meta.manifest(ds.samples) == (_files(d)[0], h)
+    # streamed in uneven chunks
+    out2 = str(tmp_path / "stream")
+    w = swr.DatasetWriter(out2, ds.H, ds.W)
+    for a, b in [(0, 7), (7, 8), (8, 23), (23, ds.samples)]:
+        w.append(pos[a:b], spec[a:b])
+    assert w.close(meta) == h
+    assert _files(out2) == _files(d)
+
+
+def test_reference_loads_written_dataset(ds_dir, tmp_path):
+    """The reference's own load_dataset reads what the writer wrote (a new manifest:
+    other splits, normalisation, bbox, RSSI labels), with the same fingerprint."""
+    d, _, _ = ds_dir
+    ds = swr.Dataset(d)
+    pos, spec = ds.read()
+    n = 12
+    rng = np.random.default_rng(5)
+    meta = swr.DatasetMeta.build(H, W, mode="rx_moving", seed=77, normalization=0.123456789012345,
+                                 train=[i for i in range(n) if i % 3], test=[i for i in range(n) if not i % 3],
+                                 excluded=[4, 19], bbox_min=(0.31, 0.3, 0.29), bbox_max=(3.7, 2.71, 2.2),
+                                 rssi_dbm=rng.normal(-60, 5, n), room=(5.0, 4.0, 3.0), reflectivity=0.35,
+                                 max_bounces=2, fixed_node=(1.0, 2.0, 1.5), k_elements=8, spacing=0.05,
+                                 wavelength=0.1)
+    out = str(tmp_path / "new")
+    hw = swr.save_dataset(out, meta, pos[:n], spec[:n])
+    rh, rpos, rspec = O.load_dataset(out, H, W)
+    assert rh == hw
+    np.testing.assert_array_equal(rpos, pos[:n])
+    np.testing.assert_array_equal(rspec, spec[:n])
+    back = swr.Dataset(out)
+    m2 = back.meta()
+    assert (m2.mode, m2.seed, m2.max_bounces, m2.k_elements) == (b"rx_moving", 77, 2, 8)
+    assert m2.manifest(n)[1] == hw
+
+
+def test_writer_errors(tmp_path):
+    meta = swr.DatasetMeta.build(H, W, mode="sideways")
+    with pytest.raises(ValueError, match="unknown mobility mode"):
+        meta.manifest(0)
+    w = swr.DatasetWriter(str(tmp_path / "g"), H, W)
+    with pytest.raises(ValueError, match="grid differs"):
+        w.close(swr.DatasetMeta.build(H + 1, W))
+    with pytest.raises(ValueError):
+        swr.DatasetWriter(str(tmp_path / "z"), 0, W)
+
+
+@pytest.mark.gpu
+def test_writer_render_equals_render(ds_dir, tmp_path):
+    """Rendered straight into a dataset on the GPU (chunked, file writes overlapped):
+    the records equal swr.render of the same positions bit for bit, and the
+    reference's load_dataset reads the directory."""
+    d, h, bbox = ds_dir
+    sc = _bound_scene(bbox)
+    ck = swr.Checkpoint.from_scene(sc)
+    pos = swr_positions = np.ascontiguousarray(swr.Dataset(d).read()[0][:300])
+    out = str(tmp_path / "rendered")
+    w = swr.DatasetWriter(out, H, W)
+    w.render(ck, pos)
+    meta = swr.DatasetMeta.build(H, W, train=list(range(300)), bbox_min=bbox[:3], bbox_max=bbox[3:])
+    hw = w.close(meta)
+    want = swr.render(ck, swr_positions)["spectra"]
+    back = swr.Dataset(out)
+    p2, s2 = back.read()
+    np.testing.assert_array_equal(p2, pos)
+    np.testing.assert_array_equal(s2, want)
+    rh, _, rspec = O.load_dataset(out, H, W)
+    assert rh == hw
+    np.testing.assert_array_equal(rspec, want)
