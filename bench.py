@@ -105,13 +105,15 @@ class ClockSampler:
         return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": len(sm)}
 
 
-def cpu_reference_rate(scene, positions, threads=None):
+def cpu_reference_rate(scene, positions, threads=None, variant="blas"):
     """The reference library (oracle/_ref, built from the reference sources) on
-    this host's cores, position-parallel (one render_at per thread)."""
+    this host's cores, position-parallel (one render_at per thread). variant
+    "blas": its deform GEMM on a real single-threaded SGEMM (numpy's OpenBLAS;
+    the reference uses Eigen's blocked GEMM, so a plain loop would handicap it),
+    the x86-64-v4 build on AVX-512 hosts; "loop": the round-1 restated loop."""
     import oracle as O
-    kind = "reference"
     try:
-        ref = O.Reference(scene=scene)
+        ref = O.Reference(scene=scene, variant=variant)
     except FileNotFoundError:
         return None
     cores = threads or os.cpu_count()
@@ -120,9 +122,18 @@ def cpu_reference_rate(scene, positions, threads=None):
     t0 = time.perf_counter()
     ref.render_batch(positions, mode=1, spectra=False)
     dt = time.perf_counter() - t0
-    return {"value": len(positions) / dt, "unit": "spectra/s", "cores": cores, "kind": kind,
+    return {"value": len(positions) / dt, "unit": "spectra/s", "cores": cores, "kind": "reference",
+            "variant": variant, "library": os.path.basename(ref.so),
             "sample": f"{len(positions)} positions of the same scene (N={scene.n}), render_at + pooled + AoA, "
                       f"position-parallel OpenMP, {dt:.1f} s"}
+
+
+def cpu_model():
+    try:
+        with open("/proc/cpuinfo") as fh:
+            return next((ln.split(":", 1)[1].strip() for ln in fh if ln.startswith("model name")), None)
+    except OSError:
+        return None
 
 
 def parity_check(ck, scene, pos, idx, spectra, pooled, aoa_rc):
@@ -149,7 +160,7 @@ def parity_check(ck, scene, pos, idx, spectra, pooled, aoa_rc):
     out["raster_max_err_rel_peak"] = worst
     ok = worst <= 1e-5
     try:
-        ref = O.Reference(scene=scene)
+        ref = O.Reference(scene=scene, variant="blas")
         ref.set_threads(os.cpu_count())
         rs, rp, rrc, _ = ref.render_batch(pos[idx], mode=1, spectra=True)
     except FileNotFoundError:
@@ -190,18 +201,20 @@ def run_reference_arm(args, scene, rank):
     res = None
     times = []
     for i in range(args.warmup + args.steps):
-        r = cpu_reference_rate(scene, pos, cores)
+        r = cpu_reference_rate(scene, pos, cores, "blas")
         if r is None:
-            return {"impl": "reference", "unavailable": "oracle/_ref/libwrfref.so not built"}
+            return {"impl": "reference", "unavailable": "oracle/_ref/libwrfref_blas.so not built"}
         if i >= args.warmup:
             times.append(per_step / r["value"])
             res = r
     total = sum(times)
     value = per_step * args.steps / total
+    # the round-1 build (deform GEMM as the restated loop), one step, for continuity
+    loop = cpu_reference_rate(scene, pos, cores, "loop")
     # the reference as shipped, render_at in a loop with its
     # OpenMP inside each call (a bounded sample of 4 positions)
     import oracle as O
-    ref = O.Reference(scene=scene)
+    ref = O.Reference(scene=scene, variant="blas")
     ref.set_threads(cores)
     t0 = time.perf_counter()
     ref.render_batch(pos[:4], mode=0, spectra=False)
@@ -212,8 +225,11 @@ def run_reference_arm(args, scene, rank):
             "impl": "reference",
             "config": config_dict(args, scene),
             "cpu_baseline": {"value": value, "unit": "spectra/s", "cores": cores, "kind": "reference",
+                             "cpu": cpu_model(), "library": res["library"],
                              "sample": f"{per_step} positions per step (bounded sample of the workload), "
-                                       f"position-parallel render_at"},
+                                       f"position-parallel render_at; deform GEMM on single-threaded OpenBLAS "
+                                       f"SGEMM (bit-identical to the restated loop)"},
+            "cpu_restated_loop": None if loop is None else {k: loop[k] for k in ("value", "unit", "cores", "library")},
             "cpu_as_shipped": {"value": shipped, "unit": "spectra/s", "cores": cores,
                                "sample": "4 positions, render_at in a loop, OpenMP inside each call"},
             "e2e": {"value": value, "unit": "spectra/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
@@ -577,7 +593,9 @@ def main():
     cpu = None
     if not args.no_cpu_baseline:
         cores = os.cpu_count()
-        cpu = cpu_reference_rate(scene, random_positions(max(cores, 4), seed=99), cores)
+        cpu = cpu_reference_rate(scene, random_positions(max(cores, 4), seed=99), cores, "blas")
+        if cpu is not None:
+            cpu["cpu"] = cpu_model()
 
     out = {
         "metric": "spectra/sec", "value": value, "unit": "spectra/s", "n_gpus": world, "steps": args.steps,

@@ -19,6 +19,35 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 PORT_SO = os.path.join(HERE, "liboracle.so")
 REF_SO = os.path.join(HERE, "_ref", "libwrfref.so")
 REF_NOFMA_SO = os.path.join(HERE, "_ref", "libwrfref_nofma.so")
+REF_BLAS_SO = os.path.join(HERE, "_ref", "libwrfref_blas.so")
+REF_BLAS_V4_SO = os.path.join(HERE, "_ref", "libwrfref_blas_v4.so")
+
+
+def host_has_avx512() -> bool:
+    try:
+        with open("/proc/cpuinfo") as fh:
+            flags = next((ln for ln in fh if ln.startswith("flags")), "")
+        return all(f in flags.split() for f in ("avx512f", "avx512bw", "avx512vl", "avx512dq"))
+    except OSError:
+        return False
+
+
+def blas_library() -> str | None:
+    """numpy's bundled OpenBLAS (ILP64 CBLAS symbols scipy_cblas_*64_)."""
+    import glob
+    d = os.path.join(os.path.dirname(os.path.dirname(np.__file__)), "numpy.libs")
+    hits = sorted(glob.glob(os.path.join(d, "libscipy_openblas64_*.so")))
+    return hits[0] if hits else None
+
+
+def reference_so(variant: str = "loop") -> str:
+    """loop: the restated GEMM loop (-march=x86-64-v3); blas: real SGEMM, the
+    x86-64-v4 build on AVX-512 hosts; nofma: -ffp-contract=off."""
+    if variant == "nofma":
+        return REF_NOFMA_SO
+    if variant == "blas":
+        return REF_BLAS_V4_SO if host_has_avx512() and os.path.exists(REF_BLAS_V4_SO) else REF_BLAS_SO
+    return REF_SO
 
 _fp = C.POINTER(C.c_float)
 _ip = C.POINTER(C.c_int)
@@ -28,7 +57,7 @@ _dp = C.POINTER(C.c_double)
 def build(ref: bool = True) -> None:
     """Compile the checkers (liboracle.so always; _ref only where the reference sources exist)."""
     targets = ["oracle"] + (["ref"] if ref and os.path.isdir("/root/reference/proj/src") else [])
-    subprocess.run(["make", "-s", "-C", HERE] + targets, check=True)
+    subprocess.run(["make", "-s", "-j4", "-C", HERE] + targets, check=True)
 
 
 def _f(a):
@@ -151,10 +180,17 @@ class Port:
 class Reference:
     """The reference library built from /root/reference sources (oracle/_ref)."""
 
-    def __init__(self, scene=None, path=None, nofma=False, handle=None):
-        so = REF_NOFMA_SO if nofma else REF_SO
+    def __init__(self, scene=None, path=None, nofma=False, handle=None, variant=None):
+        variant = variant or ("nofma" if nofma else "loop")
+        so = reference_so(variant)
         if not os.path.exists(so):
             raise FileNotFoundError(f"{so} missing: run `make -C oracle ref` where /root/reference exists")
+        if variant == "blas":
+            lib = blas_library()
+            if lib is None:
+                raise FileNotFoundError("numpy's OpenBLAS not found (the blas reference variant needs it)")
+            os.environ["WREF_BLAS_LIB"] = lib
+        self.variant, self.so = variant, so
         self.lib = L = C.CDLL(so)
         L.wref_ck_load.restype = C.c_void_p
         L.wref_ck_create.restype = C.c_void_p

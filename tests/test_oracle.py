@@ -228,3 +228,24 @@ def test_reference_backward_shim_field_order():
             assert abs(fd - g["response"][n, c]) <= 1e-4 * max(1.0, abs(fd)), (n, c)
     terms, grad = ref.hybrid_loss(base.astype(np.float32), np.zeros((16, 32, 2), np.float32), 0.8)
     assert abs(terms[0] - terms[1] - terms[2]) <= 1e-12 and grad.shape == (16, 32, 2)
+
+
+@pytest.mark.skipif(not has_ref() or O.blas_library() is None, reason="reference build or numpy OpenBLAS absent")
+def test_reference_blas_build_equals_loop_build():
+    """The CPU-baseline build of the reference (deform GEMM on a real SGEMM, bench.py
+    --impl reference) computes the same residuals and spectra as the restated-loop
+    build, bit for bit: both accumulate each output in K order with FMA from zero and
+    add the bias afterwards."""
+    sc = make_scene(1500, seed=12)
+    pos = random_positions(3, seed=13)
+    outs = []
+    for v in ("loop", "blas"):
+        r = O.Reference(scene=sc, variant=v)
+        r.set_threads(2)
+        outs.append((r.predict(r.normalize(pos[0])), r.render_batch(pos, mode=1, spectra=True)))
+    (ra, (sa, pa, ca, _)), (rb, (sb, pb, cb, _)) = outs
+    for x, y in zip(ra, rb):
+        np.testing.assert_array_equal(x, y)
+    np.testing.assert_array_equal(sa, sb)
+    np.testing.assert_array_equal(pa, pb)
+    np.testing.assert_array_equal(ca, cb)
