@@ -111,11 +111,49 @@ int swr_render(swr_ctx *ctx, const float *pos_m, int64_t B, uint32_t flags, floa
                double *pooled, double *rssi_dbm, int32_t *aoa_rc, double *aoa_ang);
 
 /* Same with device pointers, stream-ordered on `stream` (a cudaStream_t;
- * NULL = the context's stream). No host synchronisation except one 8-byte
- * read of the pair count per chunk. */
+ * NULL = the context's stream). No host synchronisation: the bin buffers are
+ * sized to the scene's pair bound (any residuals) and an fp16 overflow re-runs a
+ * chunk's MLP in FP32 through device-gated kernels (scenes whose bound exceeds
+ * min(24 GiB, memory / 4) per chunk read the pair count back instead). */
 int swr_render_device(swr_ctx *ctx, const float *d_pos_m, int64_t B, uint32_t flags,
                       float *d_spectra, double *d_pooled, double *d_rssi, int32_t *d_aoa_rc,
                       double *d_aoa_ang, void *stream);
+
+/* ---- multi-GPU (csrc/group.cpp) ------------------------------
+ * Positions split contiguously (B / P per device, the first B % P one more: shard.py's
+ * shard_range), the scene and weights
+ * replicated on every device, no inter-device dependency while rendering, one
+ * gather of the outputs. */
+typedef struct swr_group swr_group;
+/* one context per device from the same WRFC file (devices[0] is the root) */
+int swr_group_create_wrfc(const char *path, const int *devices, int n_dev, swr_group **out);
+/* over existing contexts (borrowed: they outlive the group; ctxs[0] is the root) */
+int swr_group_create(swr_ctx *const *ctxs, int n, swr_group **out);
+void swr_group_destroy(swr_group *g);
+int swr_group_size(swr_group *g, int *n);
+int swr_group_context(swr_group *g, int i, swr_ctx **out); /* options per member */
+/* host buffers: every device renders its shard into its slice (one host thread each) */
+int swr_group_render(swr_group *g, const float *pos_m, int64_t B, uint32_t flags, float *spectra,
+                     double *pooled, double *rssi_dbm, int32_t *aoa_rc, double *aoa_ang);
+/* device buffers on the root, stream-ordered on `stream` (root device): positions
+ * scattered peer to peer, each shard rendered chunk by chunk, each chunk sent to the
+ * root as it completes (NCCL ncclSend/ncclRecv, one communicator per device; peer
+ * copies when a device is listed twice), overlapping the next chunk's rendering */
+int swr_group_render_device(swr_group *g, const float *d_pos_m, int64_t B, uint32_t flags, float *d_spectra,
+                            double *d_pooled, double *d_rssi, int32_t *d_aoa_rc, double *d_aoa_ang,
+                            void *stream);
+/* between processes (one process per GPU): rank 0 makes an ncclUniqueId (128 bytes)
+ * and shares it; each rank builds a communicator over its context */
+typedef struct swr_comm swr_comm;
+int swr_nccl_unique_id(void *id128);
+int swr_comm_create(swr_ctx *ctx, const void *id128, int nranks, int rank, swr_comm **out);
+void swr_comm_destroy(swr_comm *comm);
+/* every rank renders its counts[rank] positions (d_pos on its device, shards in rank
+ * order); rank 0 receives all spectra into d_spec_root [sum counts][H][W][2] chunk by
+ * chunk (its own shard rendered in place) and its own pooled magnitudes into
+ * d_pooled_root (may be NULL). flags: SWR_OUT_SPECTRA and/or SWR_OUT_POOLED. */
+int swr_render_gather(swr_comm *comm, const float *d_pos_m, const int64_t *counts, uint32_t flags,
+                      float *d_spec_root, double *d_pooled_root, void *stream);
 
 /* ---- per-stage parity hooks (host buffers, synchronous) ---------------- */
 

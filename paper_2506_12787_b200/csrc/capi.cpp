@@ -213,6 +213,11 @@ void build_scene(Ctx &c, const HostScene &hs, int device)
                          std::to_string(prop.minor));
     check_cuda(cudaSetDevice(device), "cudaSetDevice");
     c.device = device;
+    {
+        size_t free_b = 0, total_b = 0;
+        check_cuda(cudaMemGetInfo(&free_b, &total_b), "cudaMemGetInfo");
+        c.mem_total = total_b;
+    }
     check_cuda(cudaStreamCreateWithFlags(&c.stream, cudaStreamNonBlocking), "cudaStreamCreate");
 
     const int tile = hs.tile < 1 ? 16 : hs.tile; // splat.cpp:166
@@ -427,6 +432,11 @@ void ensure_work(Ctx &c, int64_t nb)
     w.tile_sum = dalloc<double>(c, size_t(nb) * tiles);
     if (!w.stats)
         w.stats = dalloc<int64_t>(c, 3);
+    if (!w.reruns)
+    {
+        w.reruns = dalloc<unsigned long long>(c, 1);
+        check_cuda(cudaMemset(w.reruns, 0, sizeof(unsigned long long)), "rerun counter");
+    }
     if (!w.host_pairs)
         check_cuda(cudaHostAlloc((void **)&w.host_pairs, 4 * sizeof(int64_t), cudaHostAllocDefault), "host alloc");
     w.max_chunks = 0; // chunk histogram re-sized on demand
@@ -522,7 +532,7 @@ static void resolve_stage_times(Ctx &c, bool keep)
 static void run_chunk(Ctx &c, const float *d_pos, int nb, bool normalized, bool use_mlp, bool with_res,
                       float *d_spec, bool heads, uint32_t flags, double *d_pooled, double *d_rssi, int32_t *d_aoa_rc,
                       double *d_aoa_ang, cudaStream_t st, int raster_sub = 0,
-                      const std::function<void(int, int)> &after_raster = {})
+                      const std::function<void(int, int)> &after_raster = {}, bool host_pairs = false)
 {
     Timer tm(c, st);
     tm.mark();
@@ -542,31 +552,71 @@ static void run_chunk(Ctx &c, const float *d_pos, int nb, bool normalized, bool 
     launch_setup(c, nb, use_mlp || with_res, st);
     tm.mark();
     launch_bin_count(c, nb, st);
-    check_cuda(cudaMemcpyAsync(c.w.host_pairs, c.w.stats, 3 * sizeof(int64_t), cudaMemcpyDeviceToHost, st),
-               "D2H pair count");
-    check_cuda(cudaStreamSynchronize(st), "pair count");
-    if (use_mlp && c.mlp_precision != 0 && c.w.host_pairs[2] != 0)
+    // Pair buffers sized to the scene's bound (pair_bound: any residuals) when that
+    // fits the budget: then nothing in the chunk waits for the host -- the sort grid
+    // covers the bound (CTAs past a segment exit), and an fp16 overflow of the
+    // tensor-core MLP (a non-finite residual flagged by setup) re-runs the chunk's
+    // MLP in FP32 through kernels gated on that device flag. Otherwise (huge
+    // scenes) the pair count is read back and the buffers sized to it.
+    const int64_t bound = int64_t(nb) * c.pairs_per_pos_max;
+    const int64_t budget = std::min<int64_t>(int64_t(24) << 30, int64_t(c.mem_total / 4));
+    const bool async = !host_pairs && bound * (c.w.want_perm ? 14 : 10) <= budget;
+    if (async)
     {
-        // a non-finite residual from the fp16 tensor-core MLP (an activation above
-        // 65504): redo this chunk's MLP on the FP32 CUDA-core kernel
-        c.mlp_reruns++;
-        const int keep = c.mlp_precision;
-        c.mlp_precision = 0;
-        launch_pos_prep(c, d_pos, nb, normalized, st); // unscaled position terms
-        launch_mlp(c, nb, st);
-        c.mlp_precision = keep;
-        launch_setup(c, nb, true, st);
-        launch_bin_count(c, nb, st);
-        check_cuda(cudaMemcpyAsync(c.w.host_pairs, c.w.stats, 2 * sizeof(int64_t), cudaMemcpyDeviceToHost, st),
+        if (use_mlp && mlp_uses_tc(c))
+        {
+            const int keep = c.mlp_precision;
+            c.gate = c.w.stats + 2;
+            c.mlp_precision = 0;
+            try
+            {
+                launch_pos_prep(c, d_pos, nb, normalized, st); // unscaled position terms
+                launch_mlp(c, nb, st);
+                launch_setup(c, nb, true, st);
+                launch_bin_count(c, nb, st);
+            }
+            catch (...)
+            {
+                c.gate = nullptr;
+                c.mlp_precision = keep;
+                throw;
+            }
+            c.gate = nullptr;
+            c.mlp_precision = keep;
+        }
+        ensure_pairs(c, bound, nb, c.pairs_per_pos_max);
+        c.pairs_on_host = false;
+        launch_bin_sort(c, nb, bound, int(std::min<int64_t>(c.pairs_per_pos_max, INT32_MAX)), st);
+    }
+    else
+    {
+        check_cuda(cudaMemcpyAsync(c.w.host_pairs, c.w.stats, 3 * sizeof(int64_t), cudaMemcpyDeviceToHost, st),
                    "D2H pair count");
         check_cuda(cudaStreamSynchronize(st), "pair count");
+        if (use_mlp && c.mlp_precision != 0 && c.w.host_pairs[2] != 0)
+        {
+            // a non-finite residual from the fp16 tensor-core MLP (an activation above
+            // 65504): redo this chunk's MLP on the FP32 CUDA-core kernel
+            c.mlp_reruns++;
+            const int keep = c.mlp_precision;
+            c.mlp_precision = 0;
+            launch_pos_prep(c, d_pos, nb, normalized, st); // unscaled position terms
+            launch_mlp(c, nb, st);
+            c.mlp_precision = keep;
+            launch_setup(c, nb, true, st);
+            launch_bin_count(c, nb, st);
+            check_cuda(cudaMemcpyAsync(c.w.host_pairs, c.w.stats, 2 * sizeof(int64_t), cudaMemcpyDeviceToHost, st),
+                       "D2H pair count");
+            check_cuda(cudaStreamSynchronize(st), "pair count");
+        }
+        const int64_t pairs = c.w.host_pairs[0], max_seg = c.w.host_pairs[1];
+        if (pairs > INT32_MAX) // cannot happen within chunk_cap (pair_bound); the sort's offsets are 32-bit
+            throw std::runtime_error("pair list of a chunk exceeds 2^31 entries");
+        c.pairs_last = pairs;
+        c.pairs_on_host = true;
+        ensure_pairs(c, pairs, nb, max_seg);
+        launch_bin_sort(c, nb, pairs, int(max_seg), st);
     }
-    const int64_t pairs = c.w.host_pairs[0], max_seg = c.w.host_pairs[1];
-    if (pairs > INT32_MAX) // cannot happen within chunk_cap (pair_bound); the sort's offsets are 32-bit
-        throw std::runtime_error("pair list of a chunk exceeds 2^31 entries");
-    c.pairs_last = pairs;
-    ensure_pairs(c, pairs, nb, max_seg);
-    launch_bin_sort(c, nb, pairs, int(max_seg), st);
     tm.mark();
     const int sub = raster_sub > 0 ? std::min(raster_sub, nb) : nb;
     for (int s0 = 0; s0 < nb; s0 += sub)
@@ -1009,7 +1059,8 @@ int swr_scene_get_meta(swr_ctx *ctx, int64_t *iteration, uint64_t *manifest_hash
 
 int swr_scene_get_info(swr_ctx *ctx, swr_scene_info *info)
 {
-    const Ctx &c = ctx->c;
+    return guarded([&] {
+    Ctx &c = ctx->c;
     info->n_elevation = c.g.H;
     info->n_azimuth = c.g.W;
     info->n = c.g.n;
@@ -1023,8 +1074,20 @@ int swr_scene_get_info(swr_ctx *ctx, swr_scene_info *info)
         info->bbox_min[a] = c.bbox_min[a];
         info->bbox_max[a] = c.bbox_max[a];
     }
+    if (!c.pairs_on_host && c.w.stats)
+    {
+        // the async chunk path leaves the count on the device (ordered after the last call)
+        int64_t p = 0;
+        check_cuda(cudaSetDevice(c.device), "cudaSetDevice");
+        check_cuda(cudaStreamSynchronize(c.stream), "pair count");
+        if (c.order_pending)
+            check_cuda(cudaEventSynchronize(c.order_ev), "pair count");
+        check_cuda(cudaMemcpy(&p, c.w.stats, sizeof(p), cudaMemcpyDeviceToHost), "pair count");
+        c.pairs_last = p;
+        c.pairs_on_host = true;
+    }
     info->pairs_last = c.pairs_last;
-    return SWR_OK;
+    });
 }
 
 int swr_set_option(swr_ctx *ctx, const char *key, double value)
@@ -1085,9 +1148,20 @@ int swr_get_option(swr_ctx *ctx, const char *key, double *value)
         else if (k == "stage_timing")
             *value = c.stage_timing ? 1.0 : 0.0;
         else if (k == "mlp_reruns")
-            *value = double(c.mlp_reruns);
+        {
+            unsigned long long d = 0;
+            if (c.w.reruns)
+            {
+                check_cuda(cudaSetDevice(c.device), "cudaSetDevice");
+                check_cuda(cudaDeviceSynchronize(), "rerun count");
+                check_cuda(cudaMemcpy(&d, c.w.reruns, sizeof(d), cudaMemcpyDeviceToHost), "rerun count");
+            }
+            *value = double(c.mlp_reruns + int64_t(d));
+        }
         else if (k == "chunk_cap")
             *value = c.chunk_cap;
+        else if (k == "device")
+            *value = c.device;
         else if (k == "pairs_per_position_max")
             *value = double(c.pairs_per_pos_max);
         else if (k == "rssi_calibrated")
@@ -1347,7 +1421,7 @@ static void bins_for(Ctx &c, const float *dc, const float *dr, const float *da, 
         if (with_res)
             upload_residuals(c, dc, dr, da, b0, nb);
         run_chunk(c, nullptr, nb, true, false, with_res, d_spec, false, 0, nullptr, nullptr, nullptr, nullptr,
-                  c.stream);
+                  c.stream, 0, {}, true);
         const int64_t pairs = c.pairs_last;
         if (tile_offset)
             check_cuda(cudaMemcpyAsync(tile_offset + size_t(b0) * (tiles + 1), c.w.tile_off,

@@ -32,12 +32,15 @@ struct PosArgs
     double bmin0, bmin1, bmin2, bmax0, bmax1, bmax2;
     int normalized, bands_p, dp, wp, width;
     float pscale[4]; // powers of two: the tensor-core MLP's activation scales 2^k_l of layers 0/2/4/6, else 1
+    const int64_t *gate; // non-null: run only if *gate != 0 (device-side FP32 re-run, capi.cpp run_chunk)
 };
 
 __global__ void __launch_bounds__(256) pos_prep_kernel(PosArgs a)
 {
     __shared__ float v[3];
     __shared__ float xp[64];
+    if (a.gate && *a.gate == 0)
+        return;
     const int s = blockIdx.x;
     const int t = threadIdx.x;
     if (t < 3)
@@ -106,6 +109,7 @@ void launch_pos_prep(Ctx &c, const float *d_pos, int nb, bool normalized, cudaSt
     a.width = c.net.width;
     for (int j = 0; j < 4; j++)
         a.pscale[j] = mlp_uses_tc(c) ? std::ldexp(1.0f, c.net.tc_ascale[2 * j]) : 1.0f;
+    a.gate = c.gate;
     pos_prep_kernel<<<nb, 256, 0, st>>>(a);
     c.launches++;
 }
@@ -152,6 +156,8 @@ struct MlpArgs
     float *res;          // [5][cap_b][np]
     int n, np, nb, cap_b, width, n_gblk, n_sblk;
     unsigned *amax;      // optional [8]: max activation of each trunk layer (float bits; scene-load probe)
+    const int64_t *gate; // non-null: run only if *gate != 0 (device-side FP32 re-run)
+    unsigned long long *reruns; // with gate: bumped once per gated launch that runs
 };
 
 // Tile = GB Gaussians x 8 positions = TM rows; 256 threads as 16 row groups x
@@ -171,6 +177,13 @@ __global__ void __launch_bounds__(256) mlp_fp32_kernel(MlpArgs a)
     const int tid = threadIdx.x;
     const int cg = tid & 15, rg = tid >> 4;
     const int ntiles = a.n_gblk * a.n_sblk;
+    if (a.gate)
+    {
+        if (*a.gate == 0)
+            return;
+        if (blockIdx.x == 0 && tid == 0 && a.reruns)
+            atomicAdd(a.reruns, 1ull);
+    }
 
     for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x)
     {
@@ -337,6 +350,8 @@ static void run_mlp(Ctx &c, int nb, cudaStream_t st, unsigned *amax = nullptr)
     a.n_gblk = (c.g.n + TM / 8 - 1) / (TM / 8);
     a.n_sblk = (nb + 7) / 8;
     a.amax = amax;
+    a.gate = c.gate;
+    a.reruns = c.w.reruns;
     int dev_sms = 148;
     cudaDeviceGetAttribute(&dev_sms, cudaDevAttrMultiProcessorCount, c.device);
     int per_sm = 0;

@@ -113,8 +113,11 @@ __device__ __forceinline__ int4 bbox_of(const Grid &g, float el, float az, float
 // row/column ranges and the tile count.
 __global__ void __launch_bounds__(256) setup_kernel(Grid g, SceneDev sd, const float *__restrict__ res, int64_t plane,
                                                     float4 *__restrict__ dyn, int4 *__restrict__ rng, int *__restrict__ cnt,
-                                                    int with_res, int64_t *__restrict__ nonfinite)
+                                                    int with_res, int64_t *__restrict__ nonfinite,
+                                                    const int64_t *__restrict__ gate)
 {
+    if (gate && *gate == 0)
+        return;
     const int s = blockIdx.y;
     const int g4 = (blockIdx.x * blockDim.x + threadIdx.x) * 4;
     if (g4 >= g.np)
@@ -179,7 +182,7 @@ void launch_setup(Ctx &c, int nb, bool with_res, cudaStream_t st)
 {
     dim3 grid((c.g.np / 4 + 255) / 256, nb);
     setup_kernel<<<grid, 256, 0, st>>>(c.g, c.s, c.w.res, c.w.cap_b * c.g.np, c.w.dyn, c.w.rng, c.w.cnt, with_res,
-                                       with_res ? c.w.stats + 2 : nullptr);
+                                       with_res ? c.w.stats + 2 : nullptr, c.gate);
     c.launches++;
 }
 
@@ -263,9 +266,12 @@ __device__ __forceinline__ int block_excl_scan(int v, int *warp_sums, int &total
 // One CTA per position: exclusive scan of per-primitive tile counts (the pair
 // offsets of each primitive inside its position's segment).
 __global__ void __launch_bounds__(1024) seg_scan_kernel(const int *__restrict__ cnt, int *__restrict__ poff,
-                                                        int64_t *__restrict__ seg_len, int np, int n)
+                                                        int64_t *__restrict__ seg_len, int np, int n,
+                                                        const int64_t *__restrict__ gate)
 {
     __shared__ int ws[32];
+    if (gate && *gate == 0)
+        return;
     const int s = blockIdx.x;
     const int *c = cnt + (int64_t)s * np;
     int *o = poff + (int64_t)s * np;
@@ -297,10 +303,13 @@ __global__ void __launch_bounds__(1024) seg_scan_kernel(const int *__restrict__ 
 
 // Exclusive scan over the position segments (one CTA): seg[s] = first pair of
 // position s, seg[nb] = total; out[0] = total, out[1] = longest segment.
-__global__ void __launch_bounds__(1024) seg_base_kernel(int64_t *__restrict__ seg, int nb, int64_t *__restrict__ out)
+__global__ void __launch_bounds__(1024) seg_base_kernel(int64_t *__restrict__ seg, int nb, int64_t *__restrict__ out,
+                                                        const int64_t *__restrict__ gate)
 {
     __shared__ int64_t part[1024];
     __shared__ int64_t mx[1024];
+    if (gate && *gate == 0)
+        return;
     const int t = threadIdx.x;
     const int per = (nb + blockDim.x - 1) / blockDim.x;
     int64_t sum = 0, m = 0;
@@ -348,8 +357,8 @@ __global__ void __launch_bounds__(1024) seg_base_kernel(int64_t *__restrict__ se
 void launch_bin_count(Ctx &c, int nb, cudaStream_t st)
 {
     // seg[] first receives the per-position lengths, then their exclusive scan
-    seg_scan_kernel<<<nb, 1024, 0, st>>>(c.w.cnt, c.w.poff, c.w.seg, c.g.np, c.g.n);
-    seg_base_kernel<<<1, 1024, 0, st>>>(c.w.seg, nb, c.w.stats);
+    seg_scan_kernel<<<nb, 1024, 0, st>>>(c.w.cnt, c.w.poff, c.w.seg, c.g.np, c.g.n, c.gate);
+    seg_base_kernel<<<1, 1024, 0, st>>>(c.w.seg, nb, c.w.stats, c.gate);
     c.launches += 2;
 }
 

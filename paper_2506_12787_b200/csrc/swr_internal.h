@@ -94,7 +94,8 @@ struct Work
     bool want_perm = false;
     float4 *tile_part = nullptr; // [cap_b][tiles] (max |A|, argmax cell as float bits, sum |A| hi, lo)
     double *tile_sum = nullptr; // [cap_b][tiles]
-    int64_t *stats = nullptr;      // device: (total pairs, longest segment) of the current chunk
+    int64_t *stats = nullptr;      // device: (total pairs, longest segment, non-finite residual flag) of the current chunk
+    unsigned long long *reruns = nullptr; // device: chunks whose fp16 MLP overflowed and re-ran in FP32 (gated path)
     // evaluation metrics (k_metrics.cu): SSIM scratch, non-finite flag, outputs, staging
     int met_cap = 0;
     double *met_tmp = nullptr, *met_out = nullptr;
@@ -127,7 +128,10 @@ struct Ctx
     Work w;
     int64_t launches = 0;
     int64_t pairs_last = 0;
-    int64_t mlp_reruns = 0;             // chunks whose fp16 tensor-core MLP overflowed and re-ran in FP32
+    int64_t mlp_reruns = 0;             // chunks whose fp16 tensor-core MLP overflowed and re-ran in FP32 (sync path)
+    bool pairs_on_host = true;          // pairs_last is host-known (sync path) or still in w.stats (async path)
+    const int64_t *gate = nullptr;      // set while launching the FP32 re-run chain: kernels run only if *gate != 0
+    size_t mem_total = 0;               // device memory, bytes (async pair-buffer budget)
     double stage_ms[6]{};               // accumulated while stage_timing is on (swr_stage_times resolves)
     std::vector<std::array<cudaEvent_t, 7>> stage_pending; // recorded per chunk, read lazily
     std::vector<void *> allocs;

@@ -79,6 +79,20 @@ def lib():
         L.swr_dataset_read.argtypes = [C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p, C.c_void_p]
         L.swr_evaluate_dataset.argtypes = [C.c_void_p, C.c_void_p, C.c_int, C.c_void_p, C.c_void_p, C.c_void_p,
                                            C.c_void_p]
+        L.swr_group_create.argtypes = [C.c_void_p, C.c_int, C.POINTER(C.c_void_p)]
+        L.swr_group_create_wrfc.argtypes = [C.c_char_p, C.c_void_p, C.c_int, C.POINTER(C.c_void_p)]
+        L.swr_group_destroy.argtypes = [C.c_void_p]
+        L.swr_group_destroy.restype = None
+        L.swr_group_size.argtypes = [C.c_void_p, C.c_void_p]
+        L.swr_group_context.argtypes = [C.c_void_p, C.c_int, C.POINTER(C.c_void_p)]
+        L.swr_group_render.argtypes = [C.c_void_p, C.c_void_p, C.c_int64, C.c_uint32] + [C.c_void_p] * 5
+        L.swr_group_render_device.argtypes = [C.c_void_p, C.c_void_p, C.c_int64, C.c_uint32] + [C.c_void_p] * 6
+        L.swr_nccl_unique_id.argtypes = [C.c_void_p]
+        L.swr_comm_create.argtypes = [C.c_void_p, C.c_void_p, C.c_int, C.c_int, C.POINTER(C.c_void_p)]
+        L.swr_comm_destroy.argtypes = [C.c_void_p]
+        L.swr_comm_destroy.restype = None
+        L.swr_render_gather.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_uint32, C.c_void_p, C.c_void_p,
+                                        C.c_void_p]
         L.swr_dataset_get_meta.argtypes = [C.c_void_p, C.c_void_p]
         L.swr_dataset_manifest_json.argtypes = [C.c_void_p, C.c_int64, C.c_void_p, C.c_size_t, C.c_void_p,
                                                 C.c_void_p]
@@ -291,6 +305,82 @@ def render_device(ck: Checkpoint, d_pos_ptr: int, B: int, flags: int, d_spec=0, 
     """Stream-ordered render on device pointers (e.g. torch tensors' data_ptr())."""
     _check(lib().swr_render_device(ck.handle, d_pos_ptr, B, flags, d_spec or None, d_pooled or None,
                                    d_rssi or None, d_aoa_rc or None, d_aoa_ang or None, stream or None))
+
+
+class Group:
+    """Multi-GPU render (csrc/group.cpp): one context per device, positions split
+    contiguously, outputs gathered to the root (members[0])."""
+
+    def __init__(self, members):
+        self.members = list(members)
+        arr = (C.c_void_p * len(self.members))(*[m.handle.value for m in self.members])
+        h = C.c_void_p()
+        _check(lib().swr_group_create(arr, len(self.members), C.byref(h)))
+        self._h = h
+        self.H, self.W = self.members[0].H, self.members[0].W
+
+    def render(self, positions, spectra=True, pooled=True, rssi=False, aoa=True):
+        pos = _f32(positions).reshape(-1, 3)
+        B = pos.shape[0]
+        flags = (OUT_SPECTRA if spectra else 0) | (OUT_POOLED if pooled else 0) | (OUT_RSSI if rssi else 0) \
+            | (OUT_AOA if aoa else 0)
+        sp = np.zeros((B, self.H, self.W, 2), np.float32) if spectra else None
+        pl = np.zeros(B, np.float64) if pooled else None
+        rs = np.zeros(B, np.float64) if rssi else None
+        rc = np.zeros((B, 2), np.int32) if aoa else None
+        ang = np.zeros((B, 2), np.float64) if aoa else None
+        _check(lib().swr_group_render(self._h, _p(pos), B, flags, _p(sp), _p(pl), _p(rs), _p(rc), _p(ang)))
+        return {k: v for k, v in (("spectra", sp), ("pooled", pl), ("rssi", rs), ("aoa_rc", rc), ("aoa_ang", ang))
+                if v is not None}
+
+    def render_device(self, d_pos_ptr, B, flags, d_spec=0, d_pooled=0, d_rssi=0, d_aoa_rc=0, d_aoa_ang=0, stream=0):
+        _check(lib().swr_group_render_device(self._h, d_pos_ptr, B, flags, d_spec or None, d_pooled or None,
+                                             d_rssi or None, d_aoa_rc or None, d_aoa_ang or None, stream or None))
+
+    def close(self):
+        if getattr(self, "_h", None):
+            lib().swr_group_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def nccl_unique_id() -> bytes:
+    buf = C.create_string_buffer(128)
+    _check(lib().swr_nccl_unique_id(buf))
+    return buf.raw
+
+
+class Comm:
+    """Between processes (one per GPU): a communicator over one context;
+    render_gather renders this rank's shard and gathers every rank's spectra to rank 0."""
+
+    def __init__(self, ck: Checkpoint, unique_id: bytes, nranks: int, rank: int):
+        self.ck, self.nranks, self.rank = ck, nranks, rank
+        idb = C.create_string_buffer(bytes(unique_id), 128)
+        h = C.c_void_p()
+        _check(lib().swr_comm_create(ck.handle, idb, nranks, rank, C.byref(h)))
+        self._h = h
+
+    def render_gather(self, d_pos_ptr, counts, flags, d_spec_root=0, d_pooled_root=0, stream=0):
+        cnt = np.ascontiguousarray(counts, np.int64)
+        _check(lib().swr_render_gather(self._h, d_pos_ptr or None, _p(cnt), flags, d_spec_root or None,
+                                       d_pooled_root or None, stream or None))
+
+    def close(self):
+        if getattr(self, "_h", None):
+            lib().swr_comm_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
 
 
 def predict_residuals(ck: Checkpoint, pos01) -> Residuals:

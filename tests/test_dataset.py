@@ -169,11 +169,12 @@ def test_writer_render_equals_render(ds_dir, tmp_path):
     d, h, bbox = ds_dir
     sc = _bound_scene(bbox)
     ck = swr.Checkpoint.from_scene(sc)
-    pos = swr_positions = np.ascontiguousarray(swr.Dataset(d).read()[0][:300])
+    rng = np.random.default_rng(3)
+    pos = swr_positions = (bbox[:3] + rng.random((600, 3)) * (bbox[3:] - bbox[:3])).astype(np.float32)
     out = str(tmp_path / "rendered")
     w = swr.DatasetWriter(out, H, W)
-    w.render(ck, pos)
-    meta = swr.DatasetMeta.build(H, W, train=list(range(300)), bbox_min=bbox[:3], bbox_max=bbox[3:])
+    w.render(ck, pos)          # 600 positions: three 256-position chunks, the file writes overlapped
+    meta = swr.DatasetMeta.build(H, W, train=list(range(600)), bbox_min=bbox[:3], bbox_max=bbox[3:])
     hw = w.close(meta)
     want = swr.render(ck, swr_positions)["spectra"]
     back = swr.Dataset(out)

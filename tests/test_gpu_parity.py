@@ -495,3 +495,34 @@ def _assert_aoa(rc, want, port):
         mag = np.hypot(want[..., 0].astype(np.float64), want[..., 1])
         top = np.sort(mag.ravel())[-2:]
         assert top[1] - top[0] <= spec_tol(want), (tuple(rc), (r, c))
+
+
+def test_render_device_async_overflow_gated_rerun(scene2k):
+    """swr_render_device never waits for the host: an fp16 overflow is re-run in FP32
+    through kernels gated on the device flag, so the outputs still equal the FP32
+    path's bit for bit, and the pair count stays on the device until asked for."""
+    import torch
+    ck32 = swr.Checkpoint.from_scene(scene2k)
+    ck32.set_option("mlp_precision", swr.MLP_FP32)
+    ck16 = swr.Checkpoint.from_scene(scene2k)
+    ck16.set_option("mlp_precision", swr.MLP_FP16X3)
+    ck16.set_option("chunk", 8)
+    ckh = swr.Checkpoint.from_scene(scene2k)
+    ckh.set_option("mlp_precision", swr.MLP_FP16X3)
+    ckh.set_option("chunk", 8)
+    pos = random_positions(24, seed=5)
+    pos[9:11] += np.float32(3e4)
+    want = swr.render(ckh, pos)           # same chunks through the host-buffer entry
+    w32 = swr.render(ck32, pos[8:16])     # the overflowing chunk re-runs on the FP32 kernel
+    d_pos = torch.from_numpy(pos).cuda()
+    d_spec = torch.zeros((24, scene2k.H, scene2k.W, 2), device="cuda")
+    d_pooled = torch.zeros(24, dtype=torch.float64, device="cuda")
+    st = torch.cuda.Stream()
+    swr.render_device(ck16, d_pos.data_ptr(), 24, swr.OUT_SPECTRA | swr.OUT_POOLED, d_spec.data_ptr(),
+                      d_pooled.data_ptr(), stream=st.cuda_stream)
+    st.synchronize()
+    assert np.array_equal(d_spec.cpu().numpy(), want["spectra"])
+    assert np.array_equal(d_pooled.cpu().numpy(), want["pooled"])
+    assert np.array_equal(d_spec.cpu().numpy()[8:16], w32["spectra"])
+    assert ck16.get_option("mlp_reruns") == 1          # only the chunk holding the far positions
+    assert ck16.pairs_last() > 0
