@@ -586,7 +586,8 @@ static void run_chunk(Ctx &c, const float *d_pos, int nb, bool normalized, bool 
         }
         ensure_pairs(c, bound, nb, c.pairs_per_pos_max);
         c.pairs_on_host = false;
-        launch_bin_sort(c, nb, bound, int(std::min<int64_t>(c.pairs_per_pos_max, INT32_MAX)), st);
+        // sort grid for ~45% of the bound (measured segments: ~40% of it)
+        launch_bin_sort(c, nb, -1, int(std::min<int64_t>(c.pairs_per_pos_max * 9 / 20 + 1, INT32_MAX)), st);
     }
     else
     {

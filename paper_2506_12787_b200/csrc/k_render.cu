@@ -409,17 +409,25 @@ __global__ void __launch_bounds__(kSortThreads) sort_hist_kernel(const uint16_t 
                                                                  int max_chunks, int tiles)
 {
     extern __shared__ int h[];
-    const int c = blockIdx.x, s = blockIdx.y;
-    for (int t = threadIdx.x; t < tiles; t += blockDim.x)
-        h[t] = 0;
-    __syncthreads();
-    const int64_t b = seg[s] + (int64_t)c * kSort, e = min(seg[s + 1], b + kSort);
-    for (int64_t i = b + threadIdx.x; i < e; i += blockDim.x)
-        atomicAdd(&h[keys[i]], 1);
-    __syncthreads();
-    int *out = hist + ((int64_t)s * max_chunks + c) * tiles;
-    for (int t = threadIdx.x; t < tiles; t += blockDim.x)
-        out[t] = h[t];
+    const int s = blockIdx.y;
+    // chunks c = blockIdx.x, + gridDim.x, ... of this position's segment (the grid may
+    // be sized below the segment's chunk count: the async path launches without it)
+    for (int c = blockIdx.x;; c += gridDim.x)
+    {
+        const int64_t b = seg[s] + (int64_t)c * kSort, e = min(seg[s + 1], b + kSort);
+        if (b >= e && c > 0)
+            break;
+        for (int t = threadIdx.x; t < tiles; t += blockDim.x)
+            h[t] = 0;
+        __syncthreads();
+        for (int64_t i = b + threadIdx.x; i < e; i += blockDim.x)
+            atomicAdd(&h[keys[i]], 1);
+        __syncthreads();
+        int *out = hist + ((int64_t)s * max_chunks + c) * tiles;
+        for (int t = threadIdx.x; t < tiles; t += blockDim.x)
+            out[t] = h[t];
+        __syncthreads();
+    }
 }
 
 // Per position: CSR tile offsets (exclusive scan over tiles) and, in place,
@@ -463,11 +471,14 @@ __global__ void __launch_bounds__(kSortThreads) sort_scatter_kernel(const uint16
 {
     extern __shared__ int whist[]; // [8][tiles]
     constexpr int kWarps = kSortThreads / 32, kRounds = kSort / kSortThreads;
-    const int c = blockIdx.x, s = blockIdx.y;
+    const int s = blockIdx.y;
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    for (int c = blockIdx.x;; c += gridDim.x)
+    {
     const int64_t b = seg[s] + (int64_t)c * kSort, e = min(seg[s + 1], b + kSort);
     if (b >= e)
         return;
+    __syncthreads(); // the previous chunk's ranks are consumed
     for (int i = threadIdx.x; i < kWarps * tiles; i += blockDim.x)
         whist[i] = 0;
     __syncthreads();
@@ -512,11 +523,12 @@ __global__ void __launch_bounds__(kSortThreads) sort_scatter_kernel(const uint16
         const int64_t i = b + (int64_t)w * (kSort / kWarps) + k * 32 + lane;
         if (i < e)
         {
-            const int dst = (int)(seg[s] + wh[ky[k]] + rk[k]);
+            const int64_t dst = seg[s] + wh[ky[k]] + rk[k];
             out[dst] = vals[i];
             if (perm) // CSR slot of each emitted pair (the backward merges per primitive)
-                perm[i] = dst;
+                perm[i] = (int)dst;
         }
+    }
     }
 }
 
@@ -525,7 +537,11 @@ void launch_bin_sort(Ctx &c, int nb, int64_t pairs, int max_seg, cudaStream_t st
     const int tiles = c.g.tiles;
     dim3 ge((c.g.n + 255) / 256, nb);
     emit_kernel<<<ge, 256, 0, st>>>(c.g, c.w.rng, c.w.poff, c.w.seg, c.w.keys, c.w.vals);
+    // sort CTAs per position: the chunk count of max_seg -- the longest segment when the
+    // host knows it, else an estimate (the CTAs loop over chunks, so a longer segment
+    // is still covered, only with fewer CTAs)
     const int nch = std::max(1, (max_seg + kSort - 1) / kSort);
+    (void)pairs;
     dim3 gs(nch, nb);
     sort_hist_kernel<<<gs, kSortThreads, tiles * sizeof(int), st>>>(c.w.keys, c.w.seg, c.w.chunk_hist, c.w.max_chunks,
                                                                     tiles);
@@ -788,7 +804,21 @@ __global__ void __launch_bounds__(32 * kRasterWarps, SWR_RASTER_MINB * 8 / kRast
         bool slow;
         int j0;
         {
-            const int pr0 = max(b.x, tr0), pr1 = min(b.y, tr1);
+            int pr0 = max(b.x, tr0), pr1 = min(b.y, tr1);
+            // drop the rows the reference skips ((d_el / l1)^2 > r^2, splat.cpp:405-408):
+            // u0 is monotonic in the row, so they sit at the two ends of the box
+            // (~12% of box cells at the reference grid); same float ops as the row table
+            if (gi >= 0)
+            {
+                const auto skipped = [&](int r) {
+                    const float u0 = __fmul_rn(__fsub_rn(elc[r - tr0], d.x), sh.w);
+                    return __fmul_rn(u0, u0) > cut2;
+                };
+                while (pr0 <= pr1 && skipped(pr0))
+                    pr0++;
+                while (pr1 >= pr0 && skipped(pr1))
+                    pr1--;
+            }
             int a0 = tc0, na = tcw, nb2 = 0;
             if (b.w < g.W)
             {

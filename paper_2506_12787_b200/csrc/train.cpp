@@ -406,7 +406,9 @@ struct Trainer
         launch_gather_target(c, d_spectra, sc, d_target, st);
         launch_setup(c, 1, with_res, st);
         launch_bin_count(c, 1, st);
-        launch_bin_sort(c, 1, pair_cap, int(pair_cap), st);
+        // the graph-captured step cannot know the pair count: the sort CTAs loop over
+        // chunks, sized for ~4 pairs per primitive (measured ~3.3) instead of the cap
+        launch_bin_sort(c, 1, -1, int(std::min<int64_t>(pair_cap, int64_t(4) * c.g.n + 1)), st);
         launch_raster(c, 1, d_pred, false, st);
         launch_hybrid_loss(c, d_pred, d_target, 1, cfg.lambda1, d_terms, d_lgrad, d_tmp, d_bad, st);
         launch_state_out(c, 1, with_res, d_state, st);

@@ -29,7 +29,7 @@ int main(int argc, char **argv)
             for (float v : spectra[b].data)
                 sum += v;
             const auto aoa = w::tasks::aoa_extract(ck, spectra[b]);
-            std::printf("%zu %.9g %.9g %d %d\n", b, sum, w::tasks::pooled_magnitude(ck, spectra[b]), aoa.row, aoa.col);
+            std::printf("%zu %.9g %.17g %d %d\n", b, sum, w::tasks::pooled_magnitude(ck, spectra[b]), aoa.row, aoa.col);
         }
         // single-position path, residuals and rasterize parity with render_at
         const auto p01 = w::train::normalize_position(ck, pos[0]);

@@ -1,6 +1,6 @@
 """Summarise ncu outputs into profiles/ (run here, no GPU needed).
 
-    python tools/ncu_summary.py gpurun_out/prof_round.ncu-rep gpurun_out/launches.csv profiles/r01
+    python tools/ncu_summary.py gpurun_out/prof_round.ncu-rep[,more.ncu-rep] gpurun_out/launches.csv profiles/r01
 
 writes <prefix>_kernels.md / .json (per-kernel metrics of the --set full capture)
 and <prefix>_launches.md (share of each kernel in the launch list).
@@ -83,11 +83,12 @@ def launches(path):
 
 
 def main(rep, launch_csv, prefix):
-    ks = kernels(rep)
+    reps = rep.split(",")
+    ks = [k for r in reps for k in kernels(r)]
     with open(prefix + "_kernels.json", "w") as fh:
         json.dump(ks, fh, indent=1)
     with open(prefix + "_kernels.md", "w") as fh:
-        fh.write(f"# ncu --set full summary ({rep.split('/')[-1]})\n\n")
+        fh.write(f"# ncu --set full summary ({', '.join(r.split('/')[-1] for r in reps)})\n\n")
         fh.write("| kernel | ms | DRAM rd MB | DRAM wr MB | DRAM % | SM % | tensor % | FMA % | ALU % | L2 % | occ % | regs |\n")
         fh.write("|---|---|---|---|---|---|---|---|---|---|---|---|\n")
         for d in ks:
