@@ -616,7 +616,12 @@ def main():
                      "timing": "CUDA events on the render stream around every MLP launch of the timed steps",
                      # what the tensor pipe executes: padded shapes (K 48/160, N 160/32) x 3 split passes
                      "issued_flop_per_row": issued, "issued_tflops": (issued * rows / (mlp_ms / 1e3) / 1e12)
-                     if mlp_ms > 0 and issued else None},
+                     if mlp_ms > 0 and issued else None,
+                     # FP32-grade products need 3 fp16 passes over 160-padded layers and 32-wide
+                     # heads: the pipe's peak caps algorithmic throughput at peak * fmin / issued
+                     "fp32_grade_ceiling": (peak * fmin / issued) if issued else None,
+                     "frac_of_fp32_grade_ceiling": (achieved / (peak * fmin / issued)) if issued and achieved
+                     else None},
         "stage_ms": {k: round(float(v), 3) for k, v in zip(["pos_prep", "mlp", "setup", "bin", "raster", "heads"], stages)},
         "cpu_baseline": cpu,
         "parity_ok": None if parity is None else parity["ok"],
