@@ -374,8 +374,8 @@ def main():
     preset = {2: (50000, 1024, 156), 3: (100000, None, 156), 4: (50000, None, 156), 5: (1000000, 16, 512)}[args.config]
     args.n = args.n or preset[0]
     width = preset[2]
-    if args.config == 5:
-        args.precision = "fp32"  # the tensor-core MLP is built for width <= 160
+    if args.config == 5 and args.precision == "fp16":
+        args.precision = "fp16x3"  # the width-512 tensor-core MLP has no single-pass tier
     scene = make_scene(args.n, seed=0, width=width)
     scene.rssi_cal = (12.5, -61.0)  # the RSSI model's affine calibration (tasks.cpp:109), synthetic
     if args.config == 3:

@@ -372,7 +372,7 @@ void build_scene(Ctx &c, const HostScene &hs, int device)
     launch_center_terms(c, d_cenc, c.stream);
     check_cuda(cudaStreamSynchronize(c.stream), "centre terms");
     dfree(c, d_cenc);
-    if (mlp_tc_available() && WP == 160 && n > 0)
+    if (mlp_tc_available() && (WP == 160 || WP == 512) && n > 0)
     {
         // activation scale of the tensor-core MLP: the largest ReLU output over all
         // Gaussians x 16 probe positions (bbox corners + interior points), FP32 kernel
@@ -401,7 +401,10 @@ void build_scene(Ctx &c, const HostScene &hs, int device)
                 k = std::min(10, std::max(-20, int(std::floor(std::log2(65504.0 / 64.0 / double(m))))));
             c.net.tc_ascale[l] = k;
         }
-        prepare_tc2_weights(c, whT, heads, bias);
+        if (WP == 160)
+            prepare_tc2_weights(c, whT, heads, bias);
+        else
+            prepare_wide_weights(c, whT, heads, bias);
         c.mlp_precision = 1; // FP32-grade tensor-core MLP by default (SWR_MLP_FP32 remains an option)
     }
 }
@@ -1101,8 +1104,10 @@ int swr_set_option(swr_ctx *ctx, const char *key, double value)
             const int v = int(value);
             if (v < 0 || v > 2)
                 throw std::invalid_argument("mlp_precision must be 0 (fp32), 1 (fp16x3) or 2 (fp16)");
-            if (v != 0 && !(mlp_tc_available() && c.has_net && c.net.wp == 160))
-                throw std::invalid_argument("tensor-core MLP unavailable for this scene (width must be <= 160)");
+            if (v != 0 && !(mlp_tc_available() && c.has_net && (c.net.wp == 160 || c.net.wp == 512)))
+                throw std::invalid_argument("tensor-core MLP unavailable for this scene");
+            if (v == 2 && c.net.wp == 512)
+                throw std::invalid_argument("the single-pass fp16 tier exists for widths <= 160 only");
             c.mlp_precision = v;
         }
         else if (k == "chunk")
@@ -1123,6 +1128,12 @@ int swr_set_option(swr_ctx *ctx, const char *key, double value)
         }
         else if (k == "stage_timing")
             c.stage_timing = value != 0.0;
+        else if (k == "wide_block_rows")
+        {
+            if (value < 256)
+                throw std::invalid_argument("wide_block_rows must be >= 256");
+            c.wide_block_rows = int64_t(value);
+        }
         else if (k == "stage_reset")
         {
             resolve_stage_times(c, false);
@@ -1163,6 +1174,8 @@ int swr_get_option(swr_ctx *ctx, const char *key, double *value)
             *value = c.chunk_cap;
         else if (k == "device")
             *value = c.device;
+        else if (k == "wide_block_rows")
+            *value = double(c.wide_block_rows);
         else if (k == "pairs_per_position_max")
             *value = double(c.pairs_per_pos_max);
         else if (k == "rssi_calibrated")

@@ -364,7 +364,8 @@ static void run_mlp(Ctx &c, int nb, cudaStream_t st, unsigned *amax = nullptr)
 
 bool mlp_uses_tc(const Ctx &c)
 {
-    return c.mlp_precision != 0 && mlp_tc_available() && c.net.wp == 160 && c.net.w_tc2 != nullptr;
+    return c.mlp_precision != 0 && mlp_tc_available() &&
+           ((c.net.wp == 160 && c.net.w_tc2 != nullptr) || (c.net.wp == 512 && c.net.w_wide != nullptr));
 }
 
 // Largest ReLU output of every trunk layer over all Gaussians x the first nb
@@ -389,7 +390,10 @@ void launch_mlp(Ctx &c, int nb, cudaStream_t st)
 {
     if (mlp_uses_tc(c))
     {
-        launch_mlp_tc2(c, nb, st);
+        if (c.net.wp == 512)
+            launch_mlp_wide(c, nb, st);
+        else
+            launch_mlp_tc2(c, nb, st);
         return;
     }
     if (c.net.wp <= 160)

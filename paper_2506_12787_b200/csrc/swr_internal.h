@@ -69,7 +69,8 @@ struct NetDev
     int tc_exp[9] = {};         // per-layer weight scale exponents (index l = 1..7), [8] heads
     int tc_ascale[8] = {};      // activation scale exponent k_l of each trunk layer's output (scene-load probe)
     float tc_amax[8] = {};      // the probe's largest ReLU output per trunk layer
-    float *bias_tc = nullptr;   // [8][160] bias_l x 2^k_l (layers 1, 3, 5, 7 read by the tensor-core epilogue)
+    float *bias_tc = nullptr;   // [8][wp] bias_l x 2^k_l (read by the tensor-core epilogues)
+    uint16_t *w_wide = nullptr; // width-512 tensor-core MLP (k_mlp_wide.cu): packed fp16 hi/lo weights, layers 1..7
 };
 
 // Per-chunk scratch (positions per chunk = cap_b).
@@ -102,6 +103,8 @@ struct Work
     int *met_bad = nullptr;
     float *met_pred = nullptr, *met_target = nullptr;
     int64_t *host_pairs = nullptr; // pinned mirror of stats
+    uint16_t *wide_act[2] = {nullptr, nullptr}; // width-512 MLP activations (fp16 hi/lo, UMMA layout)
+    int64_t wide_rows = 0;
 };
 
 struct HostScene;
@@ -132,6 +135,7 @@ struct Ctx
     bool pairs_on_host = true;          // pairs_last is host-known (sync path) or still in w.stats (async path)
     const int64_t *gate = nullptr;      // set while launching the FP32 re-run chain: kernels run only if *gate != 0
     size_t mem_total = 0;               // device memory, bytes (async pair-buffer budget)
+    int64_t wide_block_rows = int64_t(1) << 21; // width-512 MLP: rows per layer-GEMM block (option "wide_block_rows")
     double stage_ms[6]{};               // accumulated while stage_timing is on (swr_stage_times resolves)
     std::vector<std::array<cudaEvent_t, 7>> stage_pending; // recorded per chunk, read lazily
     std::vector<void *> allocs;
@@ -279,6 +283,9 @@ bool mlp_tc_available();
 bool mlp_uses_tc(const Ctx &c);
 void probe_activations(Ctx &c, int nb, float out[8], cudaStream_t st);
 void launch_mlp_tc2(Ctx &c, int nb, cudaStream_t st);
+void launch_mlp_wide(Ctx &c, int nb, cudaStream_t st);
+void prepare_wide_weights(Ctx &c, const std::vector<float> &whT, const std::vector<float> &heads,
+                          const std::vector<float> &bias);
 int mlp_tc2_trace(long long *out);
 void prepare_tc2_weights(Ctx &c, const std::vector<float> &whT, const std::vector<float> &heads,
                          const std::vector<float> &bias);
