@@ -529,12 +529,12 @@ static void resolve_stage_times(Ctx &c, bool keep)
 // Render one chunk of nb positions whose (device) coordinates are d_pos.
 // Residuals come from the MLP (use_mlp), the caller (already in w.res) or are
 // zero. d_spec may be null (heads only).
-// raster_sub > 0: the raster runs in launches of raster_sub positions and
-// after_raster(first, count) is called after each (the host-buffer path queues
-// that slice's D2H there, so only the last slice's copy is left exposed)
+// slices (non-empty): the raster runs in launches of these many positions (summing to
+// nb) and after_raster(first, count) is called after each (the host-buffer path
+// queues that slice's D2H there, so the copies overlap the following slices)
 static void run_chunk(Ctx &c, const float *d_pos, int nb, bool normalized, bool use_mlp, bool with_res,
                       float *d_spec, bool heads, uint32_t flags, double *d_pooled, double *d_rssi, int32_t *d_aoa_rc,
-                      double *d_aoa_ang, cudaStream_t st, int raster_sub = 0,
+                      double *d_aoa_ang, cudaStream_t st, const std::vector<int> &slices = {},
                       const std::function<void(int, int)> &after_raster = {}, bool host_pairs = false)
 {
     Timer tm(c, st);
@@ -622,14 +622,20 @@ static void run_chunk(Ctx &c, const float *d_pos, int nb, bool normalized, bool 
         launch_bin_sort(c, nb, pairs, int(max_seg), st);
     }
     tm.mark();
-    const int sub = raster_sub > 0 ? std::min(raster_sub, nb) : nb;
-    for (int s0 = 0; s0 < nb; s0 += sub)
+    if (slices.empty())
     {
-        const int n = std::min(sub, nb - s0);
-        launch_raster(c, n, d_spec, heads, st, 0, s0);
+        launch_raster(c, nb, d_spec, heads, st, 0, 0);
         if (after_raster)
-            after_raster(s0, n);
+            after_raster(0, nb);
     }
+    else
+        for (int s0 = 0, i = 0; s0 < nb; s0 += slices[size_t(i)], i++)
+        {
+            const int n = std::min(slices[size_t(i)], nb - s0);
+            launch_raster(c, n, d_spec, heads, st, 0, s0);
+            if (after_raster)
+                after_raster(s0, n);
+        }
     tm.mark();
     if (heads)
         launch_heads(c, nb, flags, d_pooled, d_rssi, d_aoa_rc, d_aoa_ang, st);
@@ -639,6 +645,25 @@ static void run_chunk(Ctx &c, const float *d_pos, int nb, bool normalized, bool 
 }
 
 constexpr int kCopySlice = 256; // positions per raster launch + D2H slice in swr_render (chunks above 256)
+
+// Raster launches of a chunk in swr_render, each slice's spectra copied out right
+// behind it: 256-position slices, except that the call's LAST chunk ends in halving
+// slices (.., 128, 64, 32, 32), so only ~32 spectra's copy is left exposed after
+// the last raster (a uniform small slice costs launch tails on every slice).
+static std::vector<int> copy_slices(int nb, bool last)
+{
+    std::vector<int> v;
+    int r = nb;
+    while (r > 0)
+    {
+        int n = std::min(r, kCopySlice);
+        if (last && r <= kCopySlice && r > 64)
+            n = std::max(32, r / 2);
+        v.push_back(n);
+        r -= n;
+    }
+    return v;
+}
 
 static bool is_pinned(const void *p)
 {
@@ -1228,7 +1253,13 @@ int swr_render(swr_ctx *ctx, const float *pos_m, int64_t B, uint32_t flags, floa
         check_cuda(cudaSetDevice(c.device), "cudaSetDevice");
         cudaStream_t st = c.stream;
         StreamOrder order(c, st);
-        const int64_t chunk = std::max<int64_t>(1, std::min<int64_t>(B, c.chunk));
+        // host buffers: chunks of at most 256 positions once the batch exceeds that, so
+        // every chunk's spectra copy out while the next chunk's MLP runs (the copy of a
+        // 1,024-position batch takes ~4.7 ms at ~56 GB/s -- longer than the raster alone
+        // at 10k Gaussians, 4.3 ms -- so copies left to the end would stay exposed)
+        int64_t chunk = std::max<int64_t>(1, std::min<int64_t>(B, c.chunk));
+        if ((flags & SWR_OUT_SPECTRA) && spectra && chunk > kCopySlice)
+            chunk = kCopySlice;
         ensure_work(c, chunk);
         const size_t per = size_t(2) * c.g.H * c.g.W;
         // device staging (kept in the context across calls): positions, two
@@ -1263,7 +1294,7 @@ int swr_render(swr_ctx *ctx, const float *pos_m, int64_t B, uint32_t flags, floa
             };
             run_chunk(c, d_pos + 3 * b0, nb, false, use_mlp, false, want_spec ? d_spec[k] : nullptr, heads, flags,
                       d_pooled + b0, d_rssi + b0, d_rc + 2 * b0, d_ang + 2 * b0, st,
-                      want_spec && nb > kCopySlice ? kCopySlice : 0,
+                      want_spec ? copy_slices(nb, b0 + chunk >= B) : std::vector<int>(),
                       want_spec ? std::function<void(int, int)>(copy_slice) : std::function<void(int, int)>());
             if (want_spec)
                 check_cuda(cudaEventRecord(freed[k], copy_st), "record");
@@ -1435,7 +1466,7 @@ static void bins_for(Ctx &c, const float *dc, const float *dr, const float *da, 
         if (with_res)
             upload_residuals(c, dc, dr, da, b0, nb);
         run_chunk(c, nullptr, nb, true, false, with_res, d_spec, false, 0, nullptr, nullptr, nullptr, nullptr,
-                  c.stream, 0, {}, true);
+                  c.stream, {}, {}, true);
         const int64_t pairs = c.pairs_last;
         if (tile_offset)
             check_cuda(cudaMemcpyAsync(tile_offset + size_t(b0) * (tiles + 1), c.w.tile_off,
