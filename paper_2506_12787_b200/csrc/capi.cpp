@@ -562,7 +562,8 @@ static void run_chunk(Ctx &c, const float *d_pos, int nb, bool normalized, bool 
     // MLP in FP32 through kernels gated on that device flag. Otherwise (huge
     // scenes) the pair count is read back and the buffers sized to it.
     const int64_t bound = int64_t(nb) * c.pairs_per_pos_max;
-    const int64_t budget = std::min<int64_t>(int64_t(24) << 30, int64_t(c.mem_total / 4));
+    const int64_t budget =
+        c.async_pair_budget >= 0 ? c.async_pair_budget : std::min<int64_t>(int64_t(24) << 30, int64_t(c.mem_total / 4));
     const bool async = !host_pairs && bound * (c.w.want_perm ? 14 : 10) <= budget;
     if (async)
     {
@@ -1153,6 +1154,8 @@ int swr_set_option(swr_ctx *ctx, const char *key, double value)
         }
         else if (k == "stage_timing")
             c.stage_timing = value != 0.0;
+        else if (k == "async_pair_budget") // bytes; < 0: the default min(24 GiB, memory / 4); 0 forces the sync path
+            c.async_pair_budget = int64_t(value);
         else if (k == "wide_block_rows")
         {
             if (value < 256)
@@ -1902,16 +1905,17 @@ int swr_debug_overlap(swr_ctx *ctx, double *out)
             return (double)ms;
         };
         out[0] = timed([&] { launch_mlp(c, nb, a); });
-        out[1] = timed([&] { launch_raster(c, nb, nullptr, false, b, 8); });
+        out[1] = timed([&] { launch_raster(c, nb, nullptr, false, b, 2); });
         out[2] = timed([&] { launch_raster(c, nb, nullptr, false, b, 4); });
         out[3] = timed([&] {
             launch_mlp(c, nb, a);
             std::this_thread::sleep_for(std::chrono::microseconds(2000)); // MLP CTAs resident first
-            launch_raster(c, nb, nullptr, false, b, 4);
+            launch_raster(c, nb, nullptr, false, b, 2);
         });
         out[4] = timed([&] {
             launch_mlp(c, nb, a);
-            launch_raster(c, nb, nullptr, false, b, 8);
+            std::this_thread::sleep_for(std::chrono::microseconds(2000));
+            launch_raster(c, nb, nullptr, false, b, 4);
         });
         out[5] = nb;
         check_cuda(cudaStreamSynchronize(a), "overlap");

@@ -526,3 +526,23 @@ def test_render_device_async_overflow_gated_rerun(scene2k):
     assert np.array_equal(d_spec.cpu().numpy()[8:16], w32["spectra"])
     assert ck16.get_option("mlp_reruns") == 1          # only the chunk holding the far positions
     assert ck16.pairs_last() > 0
+
+
+@pytest.mark.parametrize("precision", [swr.MLP_FP16X3, swr.MLP_FP32], ids=["fp16x3", "fp32"])
+def test_sync_and_async_chunk_paths_agree(scene2k, precision):
+    """Scenes whose pair bound exceeds the per-chunk budget read the pair count back
+    and size the bin buffers to it (the round-1 path); the default sizes them to the
+    bound and never waits for the host. Both give the same bits, including an
+    overflow chunk's FP32 re-run."""
+    pos = random_positions(40, seed=14)
+    pos[20] += np.float32(3e4)
+    outs = []
+    for budget in (-1, 0):
+        ck = swr.Checkpoint.from_scene(scene2k)
+        ck.set_option("mlp_precision", precision)
+        ck.set_option("chunk", 16)
+        ck.set_option("async_pair_budget", budget)
+        outs.append(swr.render(ck, pos, rssi=False))
+        assert ck.pairs_last() > 0
+    for k in outs[0]:
+        assert np.array_equal(outs[0][k], outs[1][k]), k

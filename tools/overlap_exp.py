@@ -14,4 +14,4 @@ for n, nb in ((50000, 256), (10000, 256)):
     L = swr.lib()
     for _ in range(3):
         rc = L.swr_debug_overlap(ck.handle, out.ctypes.data_as(C.c_void_p))
-        print(n, rc, "mlp %.2f r8 %.2f r4 %.2f mlp||r4 %.2f mlp||r8 %.2f nb %d" % tuple(out), flush=True)
+        print(n, rc, "mlp %.2f r2 %.2f r4 %.2f mlp||r2 %.2f mlp||r4 %.2f nb %d" % tuple(out), flush=True)
