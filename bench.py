@@ -572,9 +572,12 @@ def main():
     wp = 160 if scene.width <= 160 else 512
     issued = None
     if args.precision != "fp32" and wp == 160:
-        # UMMA work per row: 7 hidden layers 160x160 + heads 160x32 (the centre-encoding
-        # terms enter as tcgen05.cp copies, no UMMAs), x3 split passes for fp16x3
+        # UMMA work per row: 7 hidden layers 160x160 + heads 160x32 (the encoding terms
+        # are added by the epilogue, no UMMAs), x3 split passes for fp16x3
         issued = (3 if args.precision == "fp16x3" else 1) * 2 * (7 * wp * wp + wp * 32)
+    elif args.precision != "fp32":
+        # width-512 layer GEMMs (k_mlp_wide.cu): 7 x 512 x 512 x 3 passes; heads on CUDA cores
+        issued = 3 * 2 * 7 * wp * wp
     traffic = None
     prof = os.path.join(ROOT, "profiles", "ncu_mlp_traffic.json")
     if os.path.exists(prof) and args.chunk == 256 and args.config == 2:
@@ -606,8 +609,10 @@ def main():
         "residuals within 2e-6 of FP64)" if args.precision == "fp16x3" else "fp16 MLP (fast tier, not FP32-grade)",
         "data": "synthetic (seeded scene + TX positions)",
         "config": config_dict(args, scene),
-        "roofline": {"bound": bound, "kernel": "deform MLP (mlp_tc2_kernel)" if args.precision != "fp32"
-                     else "deform MLP (mlp_fp32_kernel)", "achieved": achieved, "peak": peak,
+        "roofline": {"bound": bound, "kernel": "deform MLP (" + ("mlp_fp32_kernel" if args.precision == "fp32" else
+                                                                  "mlp_tc2_kernel" if wp == 160 else
+                                                                  "mlp_wide_kernel") + ")",
+                     "achieved": achieved, "peak": peak,
                      "unit": "TFLOP/s", "frac": (achieved / peak) if achieved else None, "traffic": traffic,
                      "traffic_unit": "DRAM bytes per launch (256-position chunk), ncu --set full",
                      "peak_source": peak_note,

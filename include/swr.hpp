@@ -460,6 +460,45 @@ inline Spectrum render_at(const Checkpoint &ck, const std::array<float, 3> &posi
 {
     return render_batch(ck, {position}).front();
 }
+
+// Multi-GPU: the same checkpoint on several devices (devices[0] is the root); a batch
+// of positions is split contiguously over them and every spectrum comes back in
+// order (csrc/group.cpp; no reference counterpart: the reference renders on one CPU)
+class DeviceGroup
+{
+  public:
+    DeviceGroup(const std::string &path, const std::vector<int> &devices)
+    {
+        swr_group *g = nullptr;
+        detail::check(swr_group_create_wrfc(path.c_str(), devices.data(), int(devices.size()), &g));
+        g_.reset(g);
+        swr_ctx *c = nullptr;
+        detail::check(swr_group_context(g, 0, &c));
+        swr_scene_info info{};
+        detail::check(swr_scene_get_info(c, &info));
+        grid_ = AngularGrid{info.n_elevation, info.n_azimuth};
+    }
+    std::vector<Spectrum> render_batch(const std::vector<std::array<float, 3>> &positions) const
+    {
+        const size_t per = size_t(2) * grid_.cells();
+        std::vector<float> flat(per * positions.size());
+        if (!positions.empty())
+            detail::check(swr_group_render(g_.get(), positions.front().data(), int64_t(positions.size()),
+                                           SWR_OUT_SPECTRA, flat.data(), nullptr, nullptr, nullptr, nullptr));
+        std::vector<Spectrum> out(positions.size());
+        for (size_t b = 0; b < positions.size(); b++)
+        {
+            out[b].grid = grid_;
+            out[b].data.assign(flat.begin() + per * b, flat.begin() + per * (b + 1));
+        }
+        return out;
+    }
+    swr_group *handle() const { return g_.get(); }
+
+  private:
+    std::unique_ptr<swr_group, void (*)(swr_group *)> g_{nullptr, &swr_group_destroy};
+    AngularGrid grid_;
+};
 } // namespace train
 
 namespace splat

@@ -81,3 +81,31 @@ def test_reference_callers_match_python(tmp_path):
     off, prims = swr.bins(ck, None)[0]
     assert int(bench[1]) == len(prims) == int(bench[3])
     assert float(bench[2]) == pytest.approx(float(canon.astype(np.float64).sum()), rel=1e-6, abs=1e-6)
+
+
+def build_group_demo(out):
+    cmd = ["/usr/bin/g++", "-std=c++17", "-O2", "-Wall", "-Werror", f"-I{ROOT}/include",
+           os.path.join(ROOT, "tests", "cpp", "group_demo.cpp"), f"-L{PKG}", "-lswr", f"-Wl,-rpath,{PKG}", "-o", out]
+    subprocess.run(cmd, check=True)
+
+
+def test_group_demo_builds(tmp_path):
+    build_group_demo(str(tmp_path / "group_demo"))
+    assert os.path.exists(tmp_path / "group_demo")
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("members", [1, 3])
+def test_cpp_group_render_equals_single_context(tmp_path, members):
+    """A C++ caller shards a batch through train::DeviceGroup (swr_group_*); the
+    spectra equal one context's render_batch bit for bit."""
+    exe = str(tmp_path / "group_demo")
+    build_group_demo(exe)
+    sc = make_scene(1200, seed=19)
+    p = str(tmp_path / "g.wrfc")
+    write_wrfc(p, sc)
+    pos = random_positions(7, seed=21)
+    out = subprocess.run([exe, p, str(members)] + [f"{v:.9g}" for v in pos.ravel()], check=True,
+                         capture_output=True, text=True).stdout.strip().splitlines()
+    assert len(out) == 8
+    assert out[-1] == "max-diff-vs-render_batch 0"
