@@ -675,22 +675,20 @@ struct Rec2
 {
     float4 dyn;   // el, az, amplitude re, im
     float4 shape; // i00, 2*i01 (exact), i11, 1/l1
-    int4 a;       // magic(ncol), ncol, rows per sweep (0: empty), columns of the first span
-    int4 b;       // first column of the first span (tile-relative), first row, last row (tile-relative), sweeps
+    int4 a;       // magic(ncol); ncol | rows per sweep (0: empty) << 8 | columns of the first span << 16;
+                  // first column of the first span (tile-relative) | first row << 8 | last row << 16; sweeps
 };
 
-// Accumulator copies are [T rows][T + kAccPad] float2: a half-warp's 64-bit RMW
-// covers rpi rows x ncol columns of a record's box, and with a 16-float2 row
-// stride (all 32 banks) rows of the same column collide; the padded stride spreads
-// them (bank-conflict model over the measured (ncol, nrow) histogram of a 10k
-// scene: 1.77 wavefronts per half-warp access at stride 16, 1.41 at 17, 1.27 at
-// 19, 1.18 at 23 or 25).
-#ifndef SWR_ACC_PAD
-#define SWR_ACC_PAD 0 // measured: padding loses more to occupancy than it gains (pad 0/1/3/7/9:
-                      // raster 19.6/20.3/19.7/20.7/20.9 ms per 1024 spectra at 50k)
-#endif
-constexpr int kAccPad = SWR_ACC_PAD;
-
+// Accumulator copies are [T rows][TS slots] float2 (TS = 16 for tiles <= 16, else
+// 32) with cell (r, c) in slot c ^ brev(r): a half-warp's 64-bit read-modify-write
+// covers rpi rows x ncol columns of a record's box, and in a plain row-major copy
+// (16 float2 = all 32 banks per row) rows of the same column collide. XOR-ing the
+// column with the bit-reversed row sends consecutive rows to disjoint slot sets
+// (bank-conflict model over the measured (ncol, nrow) histogram of a 10k scene: 1.14
+// wavefronts per half-warp access instead of 1.77; padding the rows instead costs
+// the occupancy the accumulator copies already bound: pad 0/1/3/7/9 measured
+// 19.6/20.3/19.7/20.7/20.9 ms per 1024 spectra at 50k). The row table carries each
+// row's swizzled base address, so a cell's address is one XOR per sweep.
 template <int kRasterWarps, int G>
 __global__ void __launch_bounds__(32 * kRasterWarps, SWR_RASTER_MINB * 8 / kRasterWarps)
     raster2_kernel(Grid g, SceneDev sd, const float4 *__restrict__ dyn, const int4 *__restrict__ rng,
@@ -698,14 +696,14 @@ __global__ void __launch_bounds__(32 * kRasterWarps, SWR_RASTER_MINB * 8 / kRast
                    float *__restrict__ spec, float4 *__restrict__ tile_part, double *__restrict__ tile_sum,
                    int want_heads, int s_base)
 {
-    extern __shared__ float2 acc[]; // [G * warps][T][T + kAccPad], then Rec2 [warps][32]
+    extern __shared__ __align__(1024) float2 acc[]; // [G * warps][T][TS], then Rec2 [warps][32]
     __shared__ float elc[64], azc[32];
     __shared__ uint32_t magic[33];
     constexpr int LPR = 32 / G; // lanes per record slot
-    // double-buffered (d_el, q_c | +inf) per tile row; slots 320 B apart, so the two
-    // halves' broadcast reads of the same row index hit different banks
-    __shared__ float2 rowtab_all[kRasterWarps * G][2][LPR + 4];
-    const int T = g.tile, TT = T * T, AS = T + kAccPad, ACOPY = T * AS;
+    // double-buffered (d_el, q_c | +inf, swizzled row address) per tile row
+    __shared__ __align__(16) float4 rowtab_all[kRasterWarps * G][2][LPR];
+    const int T = g.tile, TT = T * T, TS = T <= 16 ? 16 : 32, ACOPY = T * TS;
+    const int swz_shift = T <= 16 ? 28 : 27; // brev(r) >> shift = r's low 4 (5) bits reversed
     const int t = blockIdx.x, s = s_base + blockIdx.y;
     const int tr0 = (t / g.tw) * T, tc0 = (t % g.tw) * T;
     const int tr1 = min(tr0 + T, g.H) - 1, tc1 = min(tc0 + T, g.W) - 1;
@@ -725,11 +723,13 @@ __global__ void __launch_bounds__(32 * kRasterWarps, SWR_RASTER_MINB * 8 / kRast
     const int64_t sbase = (int64_t)s * g.np;
     const int half = G == 2 ? lane >> 4 : 0, hl = lane & (LPR - 1);
     const int slot = G * warp + half;
-    const uint32_t acc_base = (uint32_t)__cvta_generic_to_shared(acc + slot * ACOPY);
+    const uint32_t acc_base = (uint32_t)__cvta_generic_to_shared(acc + slot * ACOPY); // TS * 8-byte aligned
     const uint32_t tab_base = (uint32_t)__cvta_generic_to_shared(&rowtab_all[slot][0][0]);
     const float cut2 = g.cut2;
     const float kExp = -0.72134752044448170368f; // -0.5 * log2(e)
     const float my_elc = elc[hl < T ? hl : 0];     // this lane's tile row for the row table
+    // this lane's row's swizzled base address in its slot's copy (row table entry)
+    const uint32_t my_row_addr = acc_base + 8u * (uint32_t)(hl * TS) + 8u * (__brev((uint32_t)hl) >> swz_shift);
     const int *plist = prims + lb;
     const int cnt = (int)(le - lb);
     const float4 *dyn_s = dyn + sbase;
@@ -743,29 +743,31 @@ __global__ void __launch_bounds__(32 * kRasterWarps, SWR_RASTER_MINB * 8 / kRast
         {
             const Rec2 &R = recs[G * j + half];
             const float4 A = R.dyn, S = R.shape;
-            const int4 ra = R.a, rb = R.b;
+            const int4 ra = R.a;
+            const int ncol = ra.y & 255, rpi = (ra.y >> 8) & 255, na = ra.y >> 16;
+            const int a0off = ra.z & 255, rfirst = (ra.z >> 8) & 255, rlast = ra.z >> 16;
             // row table of this record: q_c = i00 d_el^2, +inf where the reference skips
-            // the row ((d_el / l1)^2 > r^2, splat.cpp:405-408)
-            const uint32_t tb = tab_base + (uint32_t)((j & 1) * (LPR + 4) * 8);
+            // the row ((d_el / l1)^2 > r^2, splat.cpp:405-408), and the row's swizzled address
+            const uint32_t tb = tab_base + (uint32_t)((j & 1) * LPR * 16);
             {
                 const float d_el = __fsub_rn(my_elc, A.x);
                 const float u0 = __fmul_rn(d_el, S.w);
                 const float qc = __fmul_rn(u0, u0) > cut2 ? __int_as_float(0x7f800000)
                                                           : __fmul_rn(__fmul_rn(S.x, d_el), d_el);
-                asm volatile("st.shared.v2.f32 [%0], {%1, %2};" ::"r"(tb + 8u * (uint32_t)hl), "f"(d_el), "f"(qc)
+                asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(tb + 16u * (uint32_t)hl),
+                             "r"(__float_as_uint(d_el)), "r"(__float_as_uint(qc)), "r"(my_row_addr), "r"(0u)
                              : "memory");
             }
             __syncwarp();
             // this lane's cell in the box: rows lr, lr + rpi, ..., column cc of the tile
             const int lr = (int)(((uint32_t)hl * (uint32_t)ra.x) >> 12);
-            const int lc = hl - lr * ra.y;
-            const bool on = lr < ra.z;
-            const int cc = on ? lc + (lc < ra.w ? rb.x : -ra.w) : 0;
-            const int row0 = rb.y + lr;
-            uint32_t cp = acc_base + 8u * (uint32_t)(row0 * AS + cc);
-            const uint32_t cp_last = acc_base + 8u * (uint32_t)(rb.z * AS + cc);
-            uint32_t tp = tb + 8u * (uint32_t)row0;
-            const uint32_t c_step = 8u * (uint32_t)(ra.z * AS), t_step = 8u * (uint32_t)ra.z;
+            const int lc = hl - lr * ncol;
+            const bool on = lr < rpi;
+            const int cc = on ? lc + (lc < na ? a0off : -na) : 0;
+            const int row0 = rfirst + lr;
+            const uint32_t cc8 = 8u * (uint32_t)cc;
+            uint32_t tp = tb + 16u * (uint32_t)row0;
+            const uint32_t tp_last = tb + 16u * (uint32_t)rlast, t_step = 16u * (uint32_t)rpi;
             const float xaz = __fsub_rn(azc[cc], A.y);
             const float d_az = SLOW ? wrap_fast(xaz) : wrap_near(xaz);
             const float w1 = __fmul_rn(__fmul_rn(S.z, d_az), d_az);
@@ -773,10 +775,14 @@ __global__ void __launch_bounds__(32 * kRasterWarps, SWR_RASTER_MINB * 8 / kRast
             if (on)
             {
 #pragma unroll 1
-                for (; cp <= cp_last; cp += c_step, tp += t_step)
+                for (; tp <= tp_last; tp += t_step)
                 {
                     float d_el, qc;
-                    asm volatile("ld.shared.v2.f32 {%0, %1}, [%2];" : "=f"(d_el), "=f"(qc) : "r"(tp));
+                    uint32_t raddr, pad;
+                    asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];"
+                                 : "=f"(d_el), "=f"(qc), "=r"(raddr), "=r"(pad)
+                                 : "r"(tp));
+                    const uint32_t cp = raddr ^ cc8;
                     const float q = __fadd_rn(__fadd_rn(qc, __fmul_rn(d_el, w2)), w1);
                     float e;
                     asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(e) : "f"(q * kExp));
@@ -857,10 +863,10 @@ __global__ void __launch_bounds__(32 * kRasterWarps, SWR_RASTER_MINB * 8 / kRast
                          szw = shfl_f2(make_float2(sh.z, sh.w), src);
             r.dyn = make_float4(dxy.x, dxy.y, dzw.x, dzw.y);
             r.shape = make_float4(sxy.x, sxy.y, szw.x, szw.y);
-            r.a = make_int4(__shfl_sync(0xffffffffu, (int)mn, src), __shfl_sync(0xffffffffu, ncol, src),
-                            __shfl_sync(0xffffffffu, rpi, src), __shfl_sync(0xffffffffu, na, src));
-            r.b = make_int4(__shfl_sync(0xffffffffu, a0off, src), __shfl_sync(0xffffffffu, pr0 - tr0, src),
-                            __shfl_sync(0xffffffffu, pr1 - tr0, src), __shfl_sync(0xffffffffu, sweeps, src));
+            r.a = make_int4(__shfl_sync(0xffffffffu, (int)mn, src),
+                            __shfl_sync(0xffffffffu, ncol | (rpi << 8) | (na << 16), src),
+                            __shfl_sync(0xffffffffu, a0off | ((pr0 - tr0) << 8) | ((pr1 - tr0) << 16), src),
+                            __shfl_sync(0xffffffffu, sweeps, src));
             recs[lane] = r;
         }
         const int cn = c0 + kRasterWarps * 32;
@@ -885,7 +891,7 @@ __global__ void __launch_bounds__(32 * kRasterWarps, SWR_RASTER_MINB * 8 / kRast
         if (r > tr1 || c > tc1)
             continue;
         float re = 0.f, im = 0.f;
-        const int ai = (cl / T) * AS + cl % T;
+        const int rr = cl / T, ai = rr * TS + ((cl % T) ^ (int)(__brev((uint32_t)rr) >> swz_shift));
 #pragma unroll
         for (int w = 0; w < G * kRasterWarps; w++)
         {
@@ -915,11 +921,11 @@ template <int WARPS, int G>
 static void launch_raster_w(Ctx &c, int nb, float *d_spec, bool want_heads, cudaStream_t st, int s_base)
 {
     const size_t smem =
-        (size_t)G * WARPS * c.g.tile * (c.g.tile + kAccPad) * sizeof(float2) + WARPS * 32 * sizeof(Rec2);
+        (size_t)G * WARPS * c.g.tile * (c.g.tile <= 16 ? 16 : 32) * sizeof(float2) + WARPS * 32 * sizeof(Rec2);
     static DeviceOnce once;
     once.get(c.device, [&] {
         check_cuda(cudaFuncSetAttribute(raster2_kernel<WARPS, G>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                        (int)(G * WARPS * 32 * (32 + kAccPad) * sizeof(float2) +
+                                        (int)(G * WARPS * 32 * 32 * sizeof(float2) +
                                               WARPS * 32 * sizeof(Rec2))),
                    "raster smem attribute");
         // same L1/shared split as the MLP kernel
