@@ -1,0 +1,7 @@
+for v in default u2 u4; do
+  if [ $v = default ]; then L=""; else L=tools/libswr_$v.so; fi
+  for n in 50000 10000; do
+    SWR_LIB=$L timeout -s KILL 300 python bench.py --n $n --no-cpu-baseline --no-parity --no-spec-sized > gpurun_out/ur_${v}_$n.log 2>&1
+    tail -1 gpurun_out/ur_${v}_$n.log | python -c "import json,sys; d=json.loads(sys.stdin.read()); print('$v', $n, round(d['value']), d['stage_ms']['raster'])"
+  done
+done
