@@ -40,6 +40,11 @@
 // meanwhile. Each weight stage (one per layer, full N = 160, half the columns
 // per CTA) serves both tiles.
 //
+// Heads: each tile has its own N = 16 heads accumulator (TMEM columns 480-495 / 496-511),
+// so heads Y never waits for heads X's readout, and the group-0 warps read the previous
+// super-tile's heads out while the tensor core runs the next layer 1 (round 2; the
+// clock64 trace, tools/tc2_trace.py: super-tile period 40.8k -> 40.6k cycles).
+//
 // Layer 0 has no UMMA: the epilogue writes ReLU(cterm0 + pterm0) (fp16 hi/lo)
 // straight into TMEM from a cterm block in shared memory. Layers 2, 4, 6 add
 // their cterm block in the epilogue too (round 1 seeded those accumulators with
@@ -86,9 +91,9 @@ constexpr int TM = 128;                   // rows per CTA: 32 Gaussians x 4 posi
 constexpr int TG = 32, TS = 4;
 constexpr int SUPER_S = 16;               // positions per super-tile (tiles X, Y x 2 CTAs x 4)
 constexpr int WPC = 160, KSTEPS = 10, NL = 8, NHEADS = 5;
-constexpr int NHEAD_N = 32;               // heads UMMA N (5 real columns)
-constexpr int HEAD_COL = 3 * WPC;         // heads accumulator: TMEM columns 480-511
-constexpr int HB_BYTES = KSTEPS * 2 * (NHEAD_N / 2) * 16 * 2; // heads B operand per CTA: 10 KB
+constexpr int NHEAD_N = 16;               // heads UMMA N (5 real columns; the N granularity of a CTA pair)
+constexpr int HEAD_COL = 3 * WPC;         // heads accumulators: TMEM columns 480-495 (tile X), 496-511 (tile Y)
+constexpr int HB_BYTES = KSTEPS * 2 * (NHEAD_N / 2) * 16 * 2; // heads B operand per CTA: 5 KB
 constexpr int KB = WPC / 2 * 16 * 2;      // one K step, one operand (hi or lo), this CTA's 80 columns: 2.5 KB
 constexpr int W_BYTES = KSTEPS * 2 * KB;  // one layer's weights per CTA: 50 KB
 constexpr int C_BLOCK = WPC * TG * 4;     // one layer's cterm block: [40 column groups][32 rows][4] f32
@@ -107,8 +112,8 @@ constexpr int SMEM_RING = NSTAGE * SLOT;
 constexpr int SMEM_CRING = NCSTAGE * C_BLOCK;
 constexpr int SMEM_P = 2 * 2 * TS * PROW * 4;         // [buffer][tile][4 positions][640]
 constexpr int SMEM_CONST = (8 * WPC + 8) * 4;
-// w_full[2], w_empty[2], c_full[2], c_empty[2], acc[2 tiles], a_ready[2 tiles], acc_h[2 tiles], h_free
-constexpr int NBARS = 2 * NSTAGE + 2 * NCSTAGE + 2 + 2 + 2 + 1;
+// w_full[2], w_empty[2], c_full[2], c_empty[2], acc[2 tiles], a_ready[2 tiles], acc_h[2 tiles], h_free[2 tiles]
+constexpr int NBARS = 2 * NSTAGE + 2 * NCSTAGE + 2 + 2 + 2 + 2;
 constexpr int SMEM_BYTES = SMEM_RING + SMEM_CRING + SMEM_P + HB_BYTES + SMEM_CONST + NBARS * 8 + 16 + 1024;
 static_assert(SMEM_BYTES <= 227 * 1024, "shared memory budget");
 
@@ -265,7 +270,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1) mlp_tc2_
     uint64_t *acc = c_empty + NCSTAGE;                  // [tile]: a layer's accumulator complete
     uint64_t *a_ready = acc + 2;                        // [tile] (leader): a layer converted, both CTAs
     uint64_t *acc_h = a_ready + 2;                      // [tile]: heads accumulator complete
-    uint64_t *h_free = acc_h + 2;                       // (leader) heads accumulator read out, both CTAs
+    uint64_t *h_free = acc_h + 2;                       // [tile] (leader) heads accumulator read out, both CTAs
     uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(bars + NBARS);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -288,7 +293,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1) mlp_tc2_
             tc::mbar_init(&a_ready[t], 2 * EPI_WARPS);
             tc::mbar_init(&acc_h[t], 1);
         }
-        tc::mbar_init(h_free, 2 * 4); // the 4 group-0 warps of both CTAs
+        for (int t = 0; t < 2; t++)
+            tc::mbar_init(&h_free[t], 2 * 4); // the 4 group-0 warps of both CTAs
         tc::fence_mbar_init();
     }
     for (int i = threadIdx.x; i < 8 * WPC; i += THREADS)
@@ -375,8 +381,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1) mlp_tc2_
     else if (warp == kMmaWarp)
     {
         int stage = 0;
-        uint32_t ph = 0, aph = 0, hph = 0; // aph bit t: phase of a_ready[t]; hph: h_free
-        int nheads = 0;                    // heads issued so far
+        uint32_t ph = 0, aph = 0, hph = 0; // aph / hph bit t: phase of a_ready[t] / h_free[t]
+        int nheads = 0;                    // super-tiles whose heads were issued
         const uint32_t r_base = tc::smem_u32(ring), hb_base = tc::smem_u32(hb);
         auto wait_ready = [&](int t) {
             MBAR_WAIT_PLAIN(&a_ready[t], (aph >> t) & 1);
@@ -387,17 +393,18 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1) mlp_tc2_
             wait_ready(t); // layer 7 of this tile converted
             if (nheads > 0)
             {
-                MBAR_WAIT_PLAIN(h_free, hph); // the previous heads were read out
-                hph ^= 1;
+                MBAR_WAIT_PLAIN(&h_free[t], (hph >> t) & 1); // this tile's previous heads were read out
+                hph ^= 1u << t;
             }
             tc::tc_fence_after();
             if (tc::elect_one())
             {
-                issue_heads<SPLIT>(tmem + HEAD_COL, hb_base, tmem + (m7 % 3) * WPC);
+                issue_heads<SPLIT>(tmem + HEAD_COL + NHEAD_N * t, hb_base, tmem + (m7 % 3) * WPC);
                 tc::mma2_commit(&acc_h[t], 3);
             }
             __syncwarp();
-            nheads++;
+            if (t == 1)
+                nheads++;
         };
         int m = 0; // layer steps (tile = m & 1; layer 0 steps are the epilogue's alone)
         for (int it = 0; it < mine; it++)
@@ -508,11 +515,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1) mlp_tc2_
         // super-tile at (g0, s0); acc_h[t] already waited
         auto heads_out = [&](int t, int g0, int s0) {
             float v[16];
-            tc::tmem_ld16(tmem + HEAD_COL + lane_off, v);
+            tc::tmem_ld16(tmem + HEAD_COL + NHEAD_N * t + lane_off, v);
             tc::tc_fence_before();
             __syncwarp();
             if (lane == 0)
-                tc::mbar_arrive_remote_relaxed(tc::mapa(h_free, 0));
+                tc::mbar_arrive_remote_relaxed(tc::mapa(&h_free[t], 0));
             const int g = g0 + lane, s = s0 + t * 2 * TS + (int)rank * TS + q;
             if (g < a.n && s < a.nb)
             {
@@ -556,16 +563,22 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1) mlp_tc2_
                         // layer 0 = ReLU(cterm + pterm), no UMMA. X0's region held the previous
                         // super-tile's Y6 (read by Y7, done: acc[Y] waited before Y7's conversion),
                         // Y0's held X7 (read by heads X); waiting for the previous super-tile's
-                        // heads here also keeps a_ready at most one phase ahead of its waiter
+                        // heads here also keeps a_ready at most one phase ahead of its waiter.
+                        // Each tile has its own heads accumulator, so heads Y never waits
+                        // for heads X's readout
                         if (it > 0)
                         {
                             wait_heads(t);
-                            if (grp == 0)
-                                heads_out(t, pg0, ps0);
                         }
                     }
                     else
                     {
+                        // the previous super-tile's heads of this tile, read out while the
+                        // tensor core runs this tile's layer 1 (the group-0 warps would
+                        // otherwise wait here anyway): off the path from layer 7 to the next
+                        // layer 1 (~1,600 cycles per boundary measured in that position)
+                        if (l == 1 && it > 0 && grp == 0)
+                            heads_out(t, pg0, ps0);
                         MBAR_WAIT_PLAIN(&acc[t], (fph >> t) & 1);
                         fph ^= 1u << t;
                         tc::tc_fence_after();
@@ -710,19 +723,20 @@ void prepare_tc2_weights(Ctx &c, const std::vector<float> &whT, const std::vecto
                 at += 2 * NC * 16;
             }
     }
-    // heads B operand: per rank its 16 of the 32 UMMA columns (heads 0-4 real)
+    // heads B operand: per rank its NHEAD_N / 2 of the UMMA columns (heads 0-4 real, all in rank 0's)
+    constexpr int HN = NHEAD_N / 2;
     const float hsc = std::ldexp(1.0f, c.net.tc_exp[8]);
     std::vector<uint16_t> hpk((size_t)2 * HB_BYTES / 2, 0);
     for (int rk = 0; rk < 2; rk++)
         for (int k = 0; k < KSTEPS; k++)
         {
-            uint16_t *hi = hpk.data() + ((size_t)rk * KSTEPS + k) * 2 * 16 * 16, *lo = hi + 16 * 16;
-            for (int nl = 0; nl < 16; nl++)
+            uint16_t *hi = hpk.data() + ((size_t)rk * KSTEPS + k) * 2 * HN * 16, *lo = hi + HN * 16;
+            for (int nl = 0; nl < HN; nl++)
                 for (int kk = 0; kk < 16; kk++)
                 {
-                    const int h = rk * 16 + nl;
+                    const int h = rk * HN + nl;
                     const float w = h < NHEADS ? heads[(size_t)h * WP + k * 16 + kk] : 0.0f;
-                    put_split(hi, lo, (size_t)((kk / 8) * 2 + nl / 8) * 64 + (nl % 8) * 8 + kk % 8, w, hsc);
+                    put_split(hi, lo, (size_t)((kk / 8) * (HN / 8) + nl / 8) * 64 + (nl % 8) * 8 + kk % 8, w, hsc);
                 }
         }
     void *dh = nullptr;
