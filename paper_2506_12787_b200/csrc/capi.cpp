@@ -1280,10 +1280,23 @@ int swr_render(swr_ctx *ctx, const float *pos_m, int64_t B, uint32_t flags, floa
         const bool use_mlp = c.has_net && !(flags & SWR_NO_RESIDUALS);
         const bool heads = flags & (SWR_OUT_POOLED | SWR_OUT_RSSI | SWR_OUT_AOA);
         int k = 0;
-        for (int64_t b0 = 0; b0 < B; b0 += chunk, k ^= 1)
+        // chunk sizes: `chunk` each; with spectra going to the host, the last one is halved,
+        // so the copy backlog it leaves behind the last raster slice is shorter (at 10k
+        // Gaussians PCIe moves ~216k spectra/s, the raster ~250k/s)
+        std::vector<int64_t> sizes;
+        for (int64_t b0 = 0; b0 < B; b0 += chunk)
+            sizes.push_back(std::min<int64_t>(chunk, B - b0));
+        if (want_spec && sizes.size() > 1 && sizes.back() >= 2 * 64)
         {
-            const int nb = int(std::min<int64_t>(chunk, B - b0));
-            if (want_spec && b0 >= 2 * chunk)
+            const int64_t last = sizes.back();
+            sizes.back() = last - last / 2;
+            sizes.push_back(last / 2);
+        }
+        int64_t b0 = 0;
+        for (size_t ci = 0; ci < sizes.size(); b0 += sizes[ci], ci++, k ^= 1)
+        {
+            const int nb = int(sizes[ci]);
+            if (want_spec && ci >= 2)
                 check_cuda(cudaStreamWaitEvent(st, freed[k], 0), "wait copy");
             // the raster of a chunk above 256 positions runs in 256-position slices, each
             // slice's spectra copied out right behind it (smaller slices lengthen the
@@ -1297,7 +1310,7 @@ int swr_render(swr_ctx *ctx, const float *pos_m, int64_t B, uint32_t flags, floa
             };
             run_chunk(c, d_pos + 3 * b0, nb, false, use_mlp, false, want_spec ? d_spec[k] : nullptr, heads, flags,
                       d_pooled + b0, d_rssi + b0, d_rc + 2 * b0, d_ang + 2 * b0, st,
-                      want_spec ? copy_slices(nb, b0 + chunk >= B) : std::vector<int>(),
+                      want_spec ? copy_slices(nb, ci + 1 == sizes.size()) : std::vector<int>(),
                       want_spec ? std::function<void(int, int)>(copy_slice) : std::function<void(int, int)>());
             if (want_spec)
                 check_cuda(cudaEventRecord(freed[k], copy_st), "record");
