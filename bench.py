@@ -349,7 +349,8 @@ def main():
                     help="BASELINE.json config: 2 = 50k Gaussians x 1024 positions/GPU, spectra+RSSI (headline); "
                          "3 = 100k x 65536 positions sharded; 4 = AoA sweep over a 64x32x32 TX grid; "
                          "5 = 1M Gaussians, width-512 MLP")
-    ap.add_argument("--n", type=int, default=None)
+    ap.add_argument("--n", "--gaussians", dest="n", type=int, default=None,
+                    help="Gaussians (--gaussians under torchrun, whose own parser would take --n)")
     ap.add_argument("--batch", type=int, default=None, help="positions per GPU (configs 2 and 5)")
     ap.add_argument("--precision", default=os.environ.get("SWR_BENCH_PRECISION", "fp16x3"),
                     choices=["fp32", "fp16x3", "fp16"],
