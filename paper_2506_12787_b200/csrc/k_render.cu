@@ -740,25 +740,38 @@ __global__ void __launch_bounds__(32 * kRasterWarps, SWR_RASTER_MINB * 8 / kRast
     const int4 *rng_s = rng + sbase;
     const int tcw = tc1 - tc0 + 1;
 
+    // 32-bit shared addresses kept in registers across the record loop (the compiler
+    // otherwise rebuilds them from the shared window base per record)
+    const uint32_t rec0 = (uint32_t)__cvta_generic_to_shared(recs + half);
+    const uint32_t azc_base = (uint32_t)__cvta_generic_to_shared(azc);
+    const uint32_t my_tab0 = tab_base + 16u * (uint32_t)hl, my_tab1 = my_tab0 + 16u * LPR;
+
     auto evaluate = [&](auto slow_tag, int j0) {
         constexpr bool SLOW = decltype(slow_tag)::value;
+        uint32_t ra_addr = rec0 + (uint32_t)(G * j0) * (uint32_t)sizeof(Rec2);
 #pragma unroll 1
-        for (int j = j0; j < 32 / G; j++)
+        for (int j = j0; j < 32 / G; j++, ra_addr += G * (uint32_t)sizeof(Rec2))
         {
-            const Rec2 &R = recs[G * j + half];
-            const float4 A = R.dyn, S = R.shape;
-            const int4 ra = R.a;
+            float4 A, S;
+            int4 ra;
+            asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
+                         : "=f"(A.x), "=f"(A.y), "=f"(A.z), "=f"(A.w) : "r"(ra_addr));
+            asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4+16];"
+                         : "=f"(S.x), "=f"(S.y), "=f"(S.z), "=f"(S.w) : "r"(ra_addr));
+            asm volatile("ld.shared.v4.s32 {%0, %1, %2, %3}, [%4+32];"
+                         : "=r"(ra.x), "=r"(ra.y), "=r"(ra.z), "=r"(ra.w) : "r"(ra_addr));
             const int ncol = ra.y & 255, rpi = (ra.y >> 8) & 255, na = ra.y >> 16;
             const int a0off = ra.z & 255, rfirst = (ra.z >> 8) & 255, rlast = ra.z >> 16;
             // row table of this record: q_c = i00 d_el^2, +inf where the reference skips
             // the row ((d_el / l1)^2 > r^2, splat.cpp:405-408), and the row's swizzled address
-            const uint32_t tb = tab_base + (uint32_t)((j & 1) * LPR * 16);
+            const bool odd = j & 1;
+            const uint32_t tb = odd ? tab_base + 16u * LPR : tab_base;
             {
                 const float d_el = __fsub_rn(my_elc, A.x);
                 const float u0 = __fmul_rn(d_el, S.w);
                 const float qc = __fmul_rn(u0, u0) > cut2 ? __int_as_float(0x7f800000)
                                                           : __fmul_rn(__fmul_rn(S.x, d_el), d_el);
-                asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(tb + 16u * (uint32_t)hl),
+                asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(odd ? my_tab1 : my_tab0),
                              "r"(__float_as_uint(d_el)), "r"(__float_as_uint(qc)), "r"(my_row_addr), "r"(0u)
                              : "memory");
             }
@@ -772,7 +785,9 @@ __global__ void __launch_bounds__(32 * kRasterWarps, SWR_RASTER_MINB * 8 / kRast
             const uint32_t cc8 = 8u * (uint32_t)cc;
             uint32_t tp = tb + 16u * (uint32_t)row0;
             const uint32_t tp_last = tb + 16u * (uint32_t)rlast, t_step = 16u * (uint32_t)rpi;
-            const float xaz = __fsub_rn(azc[cc], A.y);
+            float azc_c;
+            asm volatile("ld.shared.f32 %0, [%1];" : "=f"(azc_c) : "r"(azc_base + 4u * (uint32_t)cc));
+            const float xaz = __fsub_rn(azc_c, A.y);
             const float d_az = SLOW ? wrap_fast(xaz) : wrap_near(xaz);
             const float w1 = __fmul_rn(__fmul_rn(S.z, d_az), d_az);
             const float w2 = __fmul_rn(S.y, d_az); // (2 * i01) * d_az
