@@ -675,6 +675,22 @@ constexpr int kSweepUnroll = SWR_SWEEP_UNROLL;
 // accumulation (lane = tile column, rows unrolled in registers: no shared traffic
 // per cell, but ~53% column utilisation and per-row guards: 22.0 vs 19.4 ms per
 // 1024 spectra at 50k), a software-pipelined sweep loop (more instructions).
+#ifndef SWR_RASTER_SLIM
+#define SWR_RASTER_SLIM 1 // 40-byte records (separate int2 array), single-buffered row tables: 9 CTAs per SM
+                          // (measured 1-3% faster than 48-byte records + double buffers at 8 CTAs)
+#endif
+#if SWR_RASTER_SLIM
+struct Rec2
+{
+    float4 dyn;   // el, az, amplitude re, im
+    float4 shape; // i00, 2*i01 (exact), i11, 1/l1
+};
+// + a parallel int2 array (6-bit fields: tiles up to 32): magic(ncol) | ncol << 13 |
+// rows per sweep << 19 | columns of the first span << 25; first column of the first
+// span | first row << 6 | (last row + 1) << 12
+constexpr int kRecExtra = 8;
+constexpr int kRasterCtas = 9;
+#else
 struct Rec2
 {
     float4 dyn;   // el, az, amplitude re, im
@@ -682,6 +698,9 @@ struct Rec2
     int4 a;       // magic(ncol); ncol | rows per sweep (0: empty) << 8 | columns of the first span << 16;
                   // first column of the first span (tile-relative) | first row << 8 | last row << 16; sweeps
 };
+constexpr int kRecExtra = 0;
+constexpr int kRasterCtas = 8;
+#endif
 
 // Accumulator copies are [T rows][TS slots] float2 (TS = 16 for tiles <= 16, else
 // 32) with cell (r, c) in slot c ^ brev(r): a half-warp's 64-bit read-modify-write
@@ -694,18 +713,19 @@ struct Rec2
 // 19.6/20.3/19.7/20.7/20.9 ms per 1024 spectra at 50k). The row table carries each
 // row's swizzled base address, so a cell's address is one XOR per sweep.
 template <int kRasterWarps, int G>
-__global__ void __launch_bounds__(32 * kRasterWarps, SWR_RASTER_MINB * 8 / kRasterWarps)
+__global__ void __launch_bounds__(32 * kRasterWarps, kRasterCtas * 4 / kRasterWarps)
     raster2_kernel(Grid g, SceneDev sd, const float4 *__restrict__ dyn, const int4 *__restrict__ rng,
                    const int64_t *__restrict__ seg, const int *__restrict__ tile_off, const int *__restrict__ prims,
                    float *__restrict__ spec, float4 *__restrict__ tile_part, double *__restrict__ tile_sum,
                    int want_heads, int s_base)
 {
-    extern __shared__ __align__(1024) float2 acc[]; // [G * warps][T][TS], then Rec2 [warps][32]
-    __shared__ float elc[64], azc[32];
+    extern __shared__ __align__(256) float2 acc[]; // [G * warps][T][TS], then Rec2 [warps][32]
+    __shared__ float elc[32], azc[32];
     __shared__ uint32_t magic[33];
     constexpr int LPR = 32 / G; // lanes per record slot
     // double-buffered (d_el, q_c | +inf, swizzled row address) per tile row
-    __shared__ __align__(16) float4 rowtab_all[kRasterWarps * G][2][LPR];
+    constexpr int kTabBufs = SWR_RASTER_SLIM ? 1 : 2;
+    __shared__ __align__(16) float4 rowtab_all[kRasterWarps * G][kTabBufs][LPR];
     const int T = g.tile, TT = T * T, TS = T <= 16 ? 16 : 32, ACOPY = T * TS;
     const int swz_shift = T <= 16 ? 28 : 27; // brev(r) >> shift = r's low 4 (5) bits reversed
     const int t = blockIdx.x, s = s_base + blockIdx.y;
@@ -715,7 +735,7 @@ __global__ void __launch_bounds__(32 * kRasterWarps, SWR_RASTER_MINB * 8 / kRast
     Rec2 *recs = reinterpret_cast<Rec2 *>(acc + G * kRasterWarps * ACOPY) + warp * 32;
     for (int i = threadIdx.x; i < G * kRasterWarps * ACOPY; i += blockDim.x)
         acc[i] = make_float2(0.f, 0.f);
-    if (threadIdx.x < 64)
+    if (threadIdx.x < 32)
         elc[threadIdx.x] = (int)threadIdx.x < T && tr0 + (int)threadIdx.x <= tr1 ? sd.el_c[tr0 + threadIdx.x] : 0.f;
     if (threadIdx.x < T)
         azc[threadIdx.x] = tc0 + (int)threadIdx.x <= tc1 ? sd.az_c[tc0 + threadIdx.x] : 0.f;
@@ -743,8 +763,12 @@ __global__ void __launch_bounds__(32 * kRasterWarps, SWR_RASTER_MINB * 8 / kRast
     // 32-bit shared addresses kept in registers across the record loop (the compiler
     // otherwise rebuilds them from the shared window base per record)
     const uint32_t rec0 = (uint32_t)__cvta_generic_to_shared(recs + half);
+    int2 *recx = reinterpret_cast<int2 *>(reinterpret_cast<Rec2 *>(acc + G * kRasterWarps * ACOPY) + kRasterWarps * 32) +
+                 warp * 32; // SWR_RASTER_SLIM: the records' packed integer fields
+    const uint32_t recx0 = (uint32_t)__cvta_generic_to_shared(recx + half);
+    (void)recx0;
     const uint32_t azc_base = (uint32_t)__cvta_generic_to_shared(azc);
-    const uint32_t my_tab0 = tab_base + 16u * (uint32_t)hl, my_tab1 = my_tab0 + 16u * LPR;
+    const uint32_t my_tab0 = tab_base + 16u * (uint32_t)hl, my_tab1 = my_tab0 + 16u * LPR * (kTabBufs - 1);
 
     auto evaluate = [&](auto slow_tag, int j0) {
         constexpr bool SLOW = decltype(slow_tag)::value;
@@ -758,13 +782,26 @@ __global__ void __launch_bounds__(32 * kRasterWarps, SWR_RASTER_MINB * 8 / kRast
                          : "=f"(A.x), "=f"(A.y), "=f"(A.z), "=f"(A.w) : "r"(ra_addr));
             asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4+16];"
                          : "=f"(S.x), "=f"(S.y), "=f"(S.z), "=f"(S.w) : "r"(ra_addr));
+#if SWR_RASTER_SLIM
+            {
+                int p0, p1;
+                asm volatile("ld.shared.v2.s32 {%0, %1}, [%2];" : "=r"(p0), "=r"(p1)
+                             : "r"(recx0 + 8u * (uint32_t)(G * j)));
+                ra.x = p0 & 0x1fff;
+                ra.y = ((p0 >> 13) & 63) | (((p0 >> 19) & 63) << 8) | ((p0 >> 25) << 16);
+                ra.z = (p1 & 63) | (((p1 >> 6) & 63) << 8) | ((((p1 >> 12) & 63) - 1) << 16);
+                ra.w = 0;
+            }
+            __syncwarp(); // single-buffered row table: every lane is done with the previous record
+#else
             asm volatile("ld.shared.v4.s32 {%0, %1, %2, %3}, [%4+32];"
                          : "=r"(ra.x), "=r"(ra.y), "=r"(ra.z), "=r"(ra.w) : "r"(ra_addr));
+#endif
             const int ncol = ra.y & 255, rpi = (ra.y >> 8) & 255, na = ra.y >> 16;
             const int a0off = ra.z & 255, rfirst = (ra.z >> 8) & 255, rlast = ra.z >> 16;
             // row table of this record: q_c = i00 d_el^2, +inf where the reference skips
             // the row ((d_el / l1)^2 > r^2, splat.cpp:405-408), and the row's swizzled address
-            const bool odd = j & 1;
+            const bool odd = kTabBufs == 2 && (j & 1);
             const uint32_t tb = odd ? tab_base + 16u * LPR : tab_base;
             {
                 const float d_el = __fsub_rn(my_elc, A.x);
@@ -882,10 +919,16 @@ __global__ void __launch_bounds__(32 * kRasterWarps, SWR_RASTER_MINB * 8 / kRast
                          szw = shfl_f2(make_float2(sh.z, sh.w), src);
             r.dyn = make_float4(dxy.x, dxy.y, dzw.x, dzw.y);
             r.shape = make_float4(sxy.x, sxy.y, szw.x, szw.y);
+#if SWR_RASTER_SLIM
+            recx[lane] = make_int2(__shfl_sync(0xffffffffu, (int)mn | (ncol << 13) | (rpi << 19) | (na << 25), src),
+                                   __shfl_sync(0xffffffffu,
+                                               a0off | ((pr0 - tr0) << 6) | ((max(pr1 - tr0 + 1, 0) & 63) << 12), src));
+#else
             r.a = make_int4(__shfl_sync(0xffffffffu, (int)mn, src),
                             __shfl_sync(0xffffffffu, ncol | (rpi << 8) | (na << 16), src),
                             __shfl_sync(0xffffffffu, a0off | ((pr0 - tr0) << 8) | ((pr1 - tr0) << 16), src),
                             __shfl_sync(0xffffffffu, sweeps, src));
+#endif
             recs[lane] = r;
         }
         const int cn = c0 + kRasterWarps * 32;
@@ -940,12 +983,13 @@ template <int WARPS, int G>
 static void launch_raster_w(Ctx &c, int nb, float *d_spec, bool want_heads, cudaStream_t st, int s_base)
 {
     const size_t smem =
-        (size_t)G * WARPS * c.g.tile * (c.g.tile <= 16 ? 16 : 32) * sizeof(float2) + WARPS * 32 * sizeof(Rec2);
+        (size_t)G * WARPS * c.g.tile * (c.g.tile <= 16 ? 16 : 32) * sizeof(float2) +
+        WARPS * 32 * (sizeof(Rec2) + kRecExtra);
     static DeviceOnce once;
     once.get(c.device, [&] {
         check_cuda(cudaFuncSetAttribute(raster2_kernel<WARPS, G>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                         (int)(G * WARPS * 32 * 32 * sizeof(float2) +
-                                              WARPS * 32 * sizeof(Rec2))),
+                                              WARPS * 32 * (sizeof(Rec2) + kRecExtra))),
                    "raster smem attribute");
         // same L1/shared split as the MLP kernel
         check_cuda(cudaFuncSetAttribute(raster2_kernel<WARPS, G>, cudaFuncAttributePreferredSharedMemoryCarveout,
