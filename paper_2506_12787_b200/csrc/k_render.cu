@@ -420,8 +420,19 @@ __global__ void __launch_bounds__(kSortThreads) sort_hist_kernel(const uint16_t 
         for (int t = threadIdx.x; t < tiles; t += blockDim.x)
             h[t] = 0;
         __syncthreads();
-        for (int64_t i = b + threadIdx.x; i < e; i += blockDim.x)
-            atomicAdd(&h[keys[i]], 1);
+        // all of this thread's keys in flight first, then the shared-memory counts
+        constexpr int kPer = kSort / kSortThreads;
+        uint32_t kv[kPer];
+#pragma unroll
+        for (int r = 0; r < kPer; r++)
+        {
+            const int64_t i = b + threadIdx.x + (int64_t)r * kSortThreads;
+            kv[r] = i < e ? (uint32_t)keys[i] : 0xffffffffu;
+        }
+#pragma unroll
+        for (int r = 0; r < kPer; r++)
+            if (kv[r] != 0xffffffffu)
+                atomicAdd(&h[kv[r]], 1);
         __syncthreads();
         int *out = hist + ((int64_t)s * max_chunks + c) * tiles;
         for (int t = threadIdx.x; t < tiles; t += blockDim.x)
