@@ -409,6 +409,9 @@ def main():
     dist = None
     if world > 1:
         import torch.distributed as dist
+        # communicator setup visible in the log (one line per rank: the scaling run's rank check)
+        os.environ.setdefault("NCCL_DEBUG", "INFO")
+        os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
         if backend == "nccl":
             dist.init_process_group("nccl", device_id=torch.device("cuda", local))
         else:
