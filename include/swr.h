@@ -114,7 +114,13 @@ int swr_render(swr_ctx *ctx, const float *pos_m, int64_t B, uint32_t flags, floa
  * NULL = the context's stream). No host synchronisation: the bin buffers are
  * sized to the scene's pair bound (any residuals) and an fp16 overflow re-runs a
  * chunk's MLP in FP32 through device-gated kernels (scenes whose bound exceeds
- * min(24 GiB, memory / 4) per chunk read the pair count back instead). */
+ * min(24 GiB, memory / 4) per chunk read the pair count back instead).
+ * Capturable into a CUDA graph (cudaStreamBeginCapture on `stream`) once an
+ * uncaptured call with the same or a larger B has sized the work buffers; the
+ * graph's replays then re-read d_pos_m and rewrite the outputs in place. Replays
+ * share the context's work buffers, so the caller orders them against other calls
+ * on the same context (same stream, or events). Every other entry point
+ * synchronises with the host and refuses capture (SWR_EINVAL). */
 int swr_render_device(swr_ctx *ctx, const float *d_pos_m, int64_t B, uint32_t flags,
                       float *d_spectra, double *d_pooled, double *d_rssi, int32_t *d_aoa_rc,
                       double *d_aoa_ang, void *stream);

@@ -44,10 +44,28 @@ void check_cuda(cudaError_t e, const char *what)
 // the previous call's last work (an event), then records its own.
 struct StreamOrder
 {
+    // Orders this call after the previous C-ABI call on the context (the two may run
+    // on different streams and share the context's work buffers). Under CUDA-graph
+    // capture of `st` (swr_render_device only) the cross-call event is neither waited
+    // on nor recorded -- an event of uncaptured work cannot enter a graph -- and
+    // ordering the graph's replays against other calls on the context is the
+    // caller's (as for any graph); allocation and host syncs are refused meanwhile.
     Ctx &c;
     cudaStream_t st;
-    StreamOrder(Ctx &cx, cudaStream_t s) : c(cx), st(s)
+    bool captured = false;
+    StreamOrder(Ctx &cx, cudaStream_t s, bool allow_capture = false) : c(cx), st(s)
     {
+        cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+        check_cuda(cudaStreamIsCapturing(st, &cs), "capture status");
+        if (cs != cudaStreamCaptureStatusNone)
+        {
+            if (!allow_capture)
+                throw std::invalid_argument("this call synchronises with the host and cannot be captured into a "
+                                            "CUDA graph (swr_render_device can)");
+            captured = true;
+            c.capturing = true;
+            return;
+        }
         if (!c.order_ev)
             check_cuda(cudaEventCreateWithFlags(&c.order_ev, cudaEventDisableTiming), "order event");
         else if (c.order_pending)
@@ -55,6 +73,11 @@ struct StreamOrder
     }
     ~StreamOrder()
     {
+        if (captured)
+        {
+            c.capturing = false;
+            return;
+        }
         if (cudaEventRecord(c.order_ev, st) == cudaSuccess)
             c.order_pending = true;
     }
@@ -484,7 +507,7 @@ struct Timer
     cudaEvent_t ev[7];
     int k = 0;
     bool on;
-    Timer(Ctx &cx, cudaStream_t s) : c(cx), st(s), on(cx.stage_timing)
+    Timer(Ctx &cx, cudaStream_t s) : c(cx), st(s), on(cx.stage_timing && !cx.capturing)
     {
         if (on)
             for (auto &e : ev)
@@ -595,6 +618,10 @@ static void run_chunk(Ctx &c, const float *d_pos, int nb, bool normalized, bool 
     }
     else
     {
+        if (c.capturing)
+            throw std::invalid_argument("swr_render_device under CUDA-graph capture: this batch's pair bound exceeds "
+                                        "async_pair_budget, so the chunk would read its pair count on the host; "
+                                        "capture smaller batches or raise the budget");
         check_cuda(cudaMemcpyAsync(c.w.host_pairs, c.w.stats, 3 * sizeof(int64_t), cudaMemcpyDeviceToHost, st),
                    "D2H pair count");
         check_cuda(cudaStreamSynchronize(st), "pair count");
@@ -1238,7 +1265,7 @@ int swr_render_device(swr_ctx *ctx, const float *d_pos, int64_t B, uint32_t flag
             return;
         check_cuda(cudaSetDevice(c.device), "cudaSetDevice");
         cudaStream_t st = stream ? (cudaStream_t)stream : c.stream;
-        StreamOrder order(c, st);
+        StreamOrder order(c, st, true);
         device_render(c, d_pos, B, flags, d_spec, d_pooled, d_rssi, d_aoa_rc, d_aoa_ang, st);
     });
 }

@@ -144,6 +144,9 @@ struct Ctx
     std::shared_ptr<const HostScene> host; // the scene as loaded (reference layouts), for swr_scene_get_*
     cudaEvent_t order_ev = nullptr; // last work of the previous C-ABI call (StreamOrder, capi.cpp)
     bool order_pending = false;
+    // a swr_render_device call is being captured into a CUDA graph (StreamOrder): no
+    // allocation, host synchronisation or cross-call event may happen inside it
+    bool capturing = false;
 };
 
 void check_cuda(cudaError_t e, const char *what);
@@ -169,6 +172,9 @@ template <class T>
 inline T *dalloc(Ctx &c, size_t count)
 {
     void *p = nullptr;
+    if (c.capturing)
+        throw std::invalid_argument("swr_render_device under CUDA-graph capture needs its work buffers sized "
+                                    "first: make one uncaptured call with the same (or a larger) batch");
     check_cuda(cudaMalloc(&p, std::max<size_t>(count, 1) * sizeof(T)), "cudaMalloc");
     c.allocs.push_back(p);
     return static_cast<T *>(p);
@@ -178,6 +184,8 @@ inline void dfree(Ctx &c, void *p)
 {
     if (!p)
         return;
+    if (c.capturing)
+        throw std::invalid_argument("swr_render_device under CUDA-graph capture cannot re-size work buffers");
     cudaFree(p);
     c.allocs.erase(std::remove(c.allocs.begin(), c.allocs.end(), p), c.allocs.end());
 }

@@ -546,3 +546,49 @@ def test_sync_and_async_chunk_paths_agree(scene2k, precision):
         assert ck.pairs_last() > 0
     for k in outs[0]:
         assert np.array_equal(outs[0][k], outs[1][k]), k
+
+
+def test_render_device_cuda_graph_replay(scene2k):
+    """swr_render_device captured into a CUDA graph (after one uncaptured call sized
+    the buffers): each replay re-reads the position buffer and matches an uncaptured
+    call bit for bit -- spectra, pooled, AoA -- including a chunk whose fp16 MLP
+    overflows (the device-gated FP32 re-run is part of the graph)."""
+    import torch
+    flags = swr.OUT_SPECTRA | swr.OUT_POOLED | swr.OUT_AOA
+    ck = swr.Checkpoint.from_scene(scene2k)
+    ck.set_option("chunk", 8)
+    ref = swr.Checkpoint.from_scene(scene2k)
+    ref.set_option("chunk", 8)
+    B, H, W = 20, scene2k.H, scene2k.W
+    st = torch.cuda.Stream()
+    d_pos = torch.from_numpy(random_positions(B, seed=40)).cuda()
+    outs = dict(spec=torch.zeros((B, H, W, 2), device="cuda"), pooled=torch.zeros(B, dtype=torch.float64, device="cuda"),
+                rc=torch.zeros((B, 2), dtype=torch.int32, device="cuda"),
+                ang=torch.zeros((B, 2), dtype=torch.float64, device="cuda"))
+
+    def call(c, o):
+        swr.render_device(c, d_pos.data_ptr(), B, flags, o["spec"].data_ptr(), o["pooled"].data_ptr(), 0,
+                          o["rc"].data_ptr(), o["ang"].data_ptr(), stream=st.cuda_stream)
+
+    with torch.cuda.stream(st):
+        call(ck, outs)                      # sizes the work buffers
+        st.synchronize()
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=st):
+            call(ck, outs)
+    for seed, far in ((41, False), (42, True), (43, False)):
+        p = random_positions(B, seed=seed)
+        if far:
+            p[9:11] += np.float32(3e4)      # an fp16 overflow in the second chunk
+        with torch.cuda.stream(st):
+            d_pos.copy_(torch.from_numpy(p))
+            for v in outs.values():
+                v.zero_()
+            g.replay()
+            want = {k: torch.zeros_like(v) for k, v in outs.items()}
+            call(ref, want)
+        st.synchronize()
+        for k in outs:
+            assert torch.equal(outs[k], want[k]), (seed, k)
+        assert float(outs["spec"].abs().max()) > 0
+    assert ck.get_option("mlp_reruns") == 1
