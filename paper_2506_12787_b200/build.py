@@ -22,6 +22,10 @@ ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 OUT = os.path.join(PKG, "libswr.so")
 BUILD = os.path.join(PKG, "_build")
+# checked build: the same library with the device-side SWR_DCHECK bounds / race
+# checks compiled in (tests/test_checked.py runs render cases against it)
+OUT_CHECKED = os.path.join(PKG, "libswr_checked.so")
+BUILD_CHECKED = os.path.join(PKG, "_build_checked")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 JSON_INC = os.environ.get(
     "SWR_JSON_INC",
@@ -49,8 +53,8 @@ def _digest(path: str, flags) -> str:
     return h.hexdigest()[:16]
 
 
-def _compile(src: str, flags) -> str:
-    obj = os.path.join(BUILD, os.path.basename(src) + ".o")
+def _compile(src: str, flags, build_dir: str = BUILD) -> str:
+    obj = os.path.join(build_dir, os.path.basename(src) + ".o")
     stamp = obj + ".sha"
     dig = _digest(src, flags)
     if os.path.exists(obj) and os.path.exists(stamp) and open(stamp).read() == dig:
@@ -68,20 +72,39 @@ def _compile(src: str, flags) -> str:
     return obj
 
 
-def build(verbose: bool = False) -> str:
-    os.makedirs(BUILD, exist_ok=True)
-    flags = _flags()
-    srcs = _sources()
-    with cf.ThreadPoolExecutor(max_workers=min(8, len(srcs))) as ex:
-        objs = list(ex.map(lambda s: _compile(s, flags), srcs))
+def _link(out: str, objs) -> None:
     newest = max(os.path.getmtime(o) for o in objs)
-    if not os.path.exists(OUT) or os.path.getmtime(OUT) < newest:
-        cmd = [NVCC] + ARCH + ["-shared", "-cudart", "static", "-ccbin", HOST_CXX, "-o", OUT] + objs
+    if not os.path.exists(out) or os.path.getmtime(out) < newest:
+        cmd = [NVCC] + ARCH + ["-shared", "-cudart", "static", "-ccbin", HOST_CXX, "-o", out] + objs
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:
             raise RuntimeError(f"link failed:\n{r.stdout}\n{r.stderr}")
+
+
+def _uses_checks(src: str) -> bool:
+    with open(src) as fh:
+        return "SWR_DCHECK(" in fh.read()
+
+
+def build(verbose: bool = False, checked: bool = True) -> str:
+    """libswr.so, and (checked=True) libswr_checked.so: the sources that hold device
+    checks recompiled with -DSWR_CHECKED, linked with the other objects."""
+    os.makedirs(BUILD, exist_ok=True)
+    flags = _flags()
+    srcs = _sources()
+    jobs = [(s, flags, BUILD) for s in srcs]
+    chk = [s for s in srcs if _uses_checks(s)] if checked else []
+    if chk:
+        os.makedirs(BUILD_CHECKED, exist_ok=True)
+        jobs += [(s, ["-DSWR_CHECKED"] + flags, BUILD_CHECKED) for s in chk]
+    with cf.ThreadPoolExecutor(max_workers=min(8, len(jobs))) as ex:
+        objs = list(ex.map(lambda j: _compile(*j), jobs))
+    _link(OUT, objs[:len(srcs)])
+    if chk:
+        repl = dict(zip(chk, objs[len(srcs):]))
+        _link(OUT_CHECKED, [repl.get(s, o) for s, o in zip(srcs, objs[:len(srcs)])])
     if verbose:
-        print(f"built {OUT}")
+        print(f"built {OUT}" + (f" and {OUT_CHECKED}" if chk else ""))
     return OUT
 
 

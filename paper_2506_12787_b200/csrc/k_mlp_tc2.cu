@@ -523,6 +523,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1) mlp_tc2_
             const int g = g0 + lane, s = s0 + t * 2 * TS + (int)rank * TS + q;
             if (g < a.n && s < a.nb)
             {
+                SWR_DCHECK(s < a.cap_b && g < a.np, "mlp heads: residual index outside the work buffer");
                 const size_t plane = (size_t)a.cap_b * a.np;
 #pragma unroll
                 for (int h = 0; h < NHEADS; h++)

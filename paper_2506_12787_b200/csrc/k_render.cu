@@ -368,8 +368,9 @@ void launch_bin_count(Ctx &c, int nb, cudaStream_t st)
 // one primitive follow the reference's visit order (splat.cpp:255-282).
 __global__ void __launch_bounds__(256) emit_kernel(Grid g, const int4 *__restrict__ rng, const int *__restrict__ poff,
                                                    const int64_t *__restrict__ seg, uint16_t *__restrict__ keys,
-                                                   int *__restrict__ vals)
+                                                   int *__restrict__ vals, int64_t cap)
 {
+    (void)cap;
     const int s = blockIdx.y;
     const int gi = blockIdx.x * blockDim.x + threadIdx.x;
     if (gi >= g.n)
@@ -382,6 +383,8 @@ __global__ void __launch_bounds__(256) emit_kernel(Grid g, const int4 *__restric
     auto col = [&](int tc) {
         for (int tr = tr0; tr <= tr1; tr++)
         {
+            SWR_DCHECK(o >= seg[s] && o < seg[s + 1] && o < cap, "emit: pair outside its position's segment / buffer");
+            SWR_DCHECK(tc >= 0 && tc < g.tw && tr >= 0 && tr < g.th, "emit: tile outside the grid");
             keys[o] = (uint16_t)(tr * g.tw + tc);
             vals[o] = gi;
             o++;
@@ -432,8 +435,12 @@ __global__ void __launch_bounds__(kSortThreads) sort_hist_kernel(const uint16_t 
 #pragma unroll
         for (int r = 0; r < kPer; r++)
             if (kv[r] != 0xffffffffu)
+            {
+                SWR_DCHECK((int)kv[r] < tiles, "sort_hist: tile key out of range");
                 atomicAdd(&h[kv[r]], 1);
+            }
         __syncthreads();
+        SWR_DCHECK(c < max_chunks, "sort_hist: chunk histogram overflow");
         int *out = hist + ((int64_t)s * max_chunks + c) * tiles;
         for (int t = threadIdx.x; t < tiles; t += blockDim.x)
             out[t] = h[t];
@@ -450,6 +457,7 @@ __global__ void __launch_bounds__(1024) sort_scan_kernel(const int64_t *__restri
     const int s = blockIdx.x, t = threadIdx.x;
     const int64_t len = seg[s + 1] - seg[s];
     const int nch = (int)((len + kSort - 1) / kSort);
+    SWR_DCHECK(nch <= max_chunks, "sort_scan: more chunks than the histogram holds");
     int *hs = hist + (int64_t)s * max_chunks * tiles;
     int total_t = 0;
     if (t < tiles)
@@ -478,8 +486,10 @@ __global__ void __launch_bounds__(kSortThreads) sort_scatter_kernel(const uint16
                                                                     const int *__restrict__ vals,
                                                                     const int64_t *__restrict__ seg,
                                                                     const int *__restrict__ hist, int *__restrict__ out,
-                                                                    int *__restrict__ perm, int max_chunks, int tiles)
+                                                                    int *__restrict__ perm, int max_chunks, int tiles,
+                                                                    int64_t cap)
 {
+    (void)cap;
     extern __shared__ int whist[]; // [8][tiles]
     constexpr int kWarps = kSortThreads / 32, kRounds = kSort / kSortThreads;
     const int s = blockIdx.y;
@@ -535,6 +545,7 @@ __global__ void __launch_bounds__(kSortThreads) sort_scatter_kernel(const uint16
         if (i < e)
         {
             const int64_t dst = seg[s] + wh[ky[k]] + rk[k];
+            SWR_DCHECK(dst >= seg[s] && dst < seg[s + 1] && dst < cap, "sort_scatter: slot outside the segment");
             out[dst] = vals[i];
             if (perm) // CSR slot of each emitted pair (the backward merges per primitive)
                 perm[i] = (int)dst;
@@ -547,7 +558,7 @@ void launch_bin_sort(Ctx &c, int nb, int64_t pairs, int max_seg, cudaStream_t st
 {
     const int tiles = c.g.tiles;
     dim3 ge((c.g.n + 255) / 256, nb);
-    emit_kernel<<<ge, 256, 0, st>>>(c.g, c.w.rng, c.w.poff, c.w.seg, c.w.keys, c.w.vals);
+    emit_kernel<<<ge, 256, 0, st>>>(c.g, c.w.rng, c.w.poff, c.w.seg, c.w.keys, c.w.vals, c.w.cap_pairs);
     // sort CTAs per position: the chunk count of max_seg -- the longest segment when the
     // host knows it, else an estimate (the CTAs loop over chunks, so a longer segment
     // is still covered, only with fewer CTAs)
@@ -560,7 +571,7 @@ void launch_bin_sort(Ctx &c, int nb, int64_t pairs, int max_seg, cudaStream_t st
     sort_scatter_kernel<<<gs, kSortThreads, 8 * tiles * sizeof(int), st>>>(c.w.keys, c.w.vals, c.w.seg,
                                                                            c.w.chunk_hist, c.w.sorted,
                                                                            c.w.want_perm ? c.w.perm : nullptr,
-                                                                           c.w.max_chunks, tiles);
+                                                                           c.w.max_chunks, tiles, c.w.cap_pairs);
     c.launches += 4;
 }
 
@@ -755,6 +766,7 @@ __global__ void __launch_bounds__(32 * kRasterWarps, kRasterCtas * 4 / kRasterWa
     __syncthreads();
     const int *tl = tile_off + (int64_t)s * (g.tiles + 1);
     const int64_t lb = seg[s] + tl[t], le = seg[s] + tl[t + 1];
+    SWR_DCHECK(lb >= seg[s] && lb <= le && le <= seg[s + 1], "raster: tile list outside its position's segment");
     const int64_t sbase = (int64_t)s * g.np;
     const int half = G == 2 ? lane >> 4 : 0, hl = lane & (LPR - 1);
     const int slot = G * warp + half;
@@ -810,6 +822,9 @@ __global__ void __launch_bounds__(32 * kRasterWarps, kRasterCtas * 4 / kRasterWa
 #endif
             const int ncol = ra.y & 255, rpi = (ra.y >> 8) & 255, na = ra.y >> 16;
             const int a0off = ra.z & 255, rfirst = (ra.z >> 8) & 255, rlast = ra.z >> 16;
+            SWR_DCHECK(rpi == 0 || (ncol >= 1 && ncol <= T && rpi * ncol <= LPR && rfirst <= rlast && rlast < T &&
+                                    na <= ncol && a0off + na <= T),
+                       "raster: record box outside the tile");
             // row table of this record: q_c = i00 d_el^2, +inf where the reference skips
             // the row ((d_el / l1)^2 > r^2, splat.cpp:405-408), and the row's swizzled address
             const bool odd = kTabBufs == 2 && (j & 1);
@@ -850,6 +865,14 @@ __global__ void __launch_bounds__(32 * kRasterWarps, kRasterCtas * 4 / kRasterWa
                                  : "=f"(d_el), "=f"(qc), "=r"(raddr), "=r"(pad)
                                  : "r"(tp));
                     const uint32_t cp = raddr ^ cc8;
+#ifdef SWR_CHECKED
+                    // own copy of the tile, 8-byte slot, and no two lanes of the warp on the
+                    // same cell in this sweep step (the read-modify-write is race-free)
+                    SWR_DCHECK(cp >= acc_base && cp < acc_base + 8u * (uint32_t)ACOPY && (cp & 7u) == 0u,
+                               "raster: accumulator address outside the slot's copy");
+                    SWR_DCHECK(tp >= tb && tp < tb + 16u * (uint32_t)LPR, "raster: row table index");
+                    SWR_DCHECK(__popc(__match_any_sync(__activemask(), cp)) == 1, "raster: two lanes on one cell");
+#endif
                     const float q = __fadd_rn(__fadd_rn(qc, __fmul_rn(d_el, w2)), w1);
                     float e;
                     asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(e) : "f"(q * kExp));
@@ -868,6 +891,7 @@ __global__ void __launch_bounds__(32 * kRasterWarps, kRasterCtas * 4 / kRasterWa
 
     int c0 = warp * 32;
     int gi = c0 + lane < cnt ? plist[c0 + lane] : -1;
+    SWR_DCHECK(gi < g.n, "raster: primitive index");
     int4 b = gi >= 0 ? rng_s[gi] : make_int4(0, -1, 0, 0);
     float4 d = gi >= 0 ? dyn_s[gi] : make_float4(0.f, 0.f, 0.f, 0.f);
     float4 sh = gi >= 0 ? sd.shape[gi] : make_float4(0.f, 0.f, 0.f, 0.f);
@@ -944,6 +968,7 @@ __global__ void __launch_bounds__(32 * kRasterWarps, kRasterCtas * 4 / kRasterWa
         }
         const int cn = c0 + kRasterWarps * 32;
         gi = cn + lane < cnt ? plist[cn + lane] : -1;
+        SWR_DCHECK(gi < g.n, "raster: primitive index");
         b = gi >= 0 ? rng_s[gi] : make_int4(0, -1, 0, 0);
         d = gi >= 0 ? dyn_s[gi] : make_float4(0.f, 0.f, 0.f, 0.f);
         sh = gi >= 0 ? sd.shape[gi] : make_float4(0.f, 0.f, 0.f, 0.f);

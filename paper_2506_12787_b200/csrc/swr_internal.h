@@ -3,6 +3,29 @@
 
 #include <cuda_runtime.h>
 
+// Device-side checks of the checked build (libswr_checked.so, build.py --checked):
+// an index or invariant that fails prints where and traps the kernel. compute-sanitizer
+// is unavailable on the GPU pool, so these stand in for memcheck / racecheck on the
+// render path (tests/test_checked.py). Compiled out of the product library.
+#if defined(SWR_CHECKED) && defined(__CUDACC__)
+#include <cstdio>
+#define SWR_DCHECK(cond, what)                                                                                    \
+    do                                                                                                             \
+    {                                                                                                              \
+        if (!(cond))                                                                                               \
+        {                                                                                                          \
+            printf("swr check failed: %s (%s:%d) block (%d,%d) thread %d\n", what, __FILE__, __LINE__, blockIdx.x, \
+                   blockIdx.y, threadIdx.x);                                                                        \
+            __trap();                                                                                              \
+        }                                                                                                          \
+    } while (0)
+#else
+#define SWR_DCHECK(cond, what)                                                                                    \
+    do                                                                                                             \
+    {                                                                                                              \
+    } while (0)
+#endif
+
 #include <cstdint>
 #include <string>
 #include <algorithm>
