@@ -140,7 +140,7 @@ constexpr bool kHooks = false;
 __device__ __forceinline__ void stamp2(const Tc2Args &a, int kind, int m)
 {
     if (kHooks && a.trace && blockIdx.x == 0 && m >= 16 && m < 64)
-        a.trace[kind * 48 + m - 16] = clock64();
+        a.trace[kind * 48 + m - 16] = clock64(); // kinds 0-2 MMA warp, 3-6 epilogue (tools/tc2_trace.py)
     (void)kind;
 }
 
@@ -454,6 +454,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1) mlp_tc2_
         const uint32_t lane_off = (uint32_t)(q * 32) << 16;
         uint32_t fph = 0, hph = 0, cph = 0; // acc[t] phases (bit t), acc_h[t] phases (bit t), c_full phase
         int cstage = 0;
+        int cur_m = 0; // the step being converted (trace stamps of the hooks build)
 
         auto prefetch = [&](int it) {
             int g0, s0;
@@ -497,6 +498,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1) mlp_tc2_
             if (from_acc)
             {
                 tc::tmem_ld_wait();
+                if (e == 0 && lane == 0 && chunk == grp)
+                    stamp2(a, 4, cur_m); // first chunk's accumulator in registers
 #pragma unroll
                 for (int i = 0; i < 16; i++)
                     v[i] = __uint_as_float(raw[i]);
@@ -590,10 +593,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1) mlp_tc2_
                     const float *prow = pbuf + ((it & 1) * 2 + t) * TS * PROW + q * PROW;
                     const float *add = has_xc(l) ? prow + (l / 2) * WPC : sbias + l * WPC; // warp-uniform
                     const float us = a.unscale[l]; // warp-uniform (layer 0: acc is not read)
+                    cur_m = m;
                     convert(reg, grp, add, cblk, l > 0, us);
                     if (two)
                         convert(reg, c1, add, cblk, l > 0, us);
                     tc::tmem_st_wait();
+                    if (lane == 0 && (e == 0 || e == EPI_WARPS - 1))
+                        stamp2(a, e == 0 ? 5 : 6, m); // this warp's conversion stored
                     tc::tc_fence_before();
                     __syncwarp();
                     if (lane == 0)
@@ -773,7 +779,7 @@ int mlp_tc2_trace(long long *out)
     if (!g_trace2)
         return 1;
     cudaDeviceSynchronize();
-    return cudaMemcpy(out, g_trace2, 4 * 48 * sizeof(long long), cudaMemcpyDeviceToHost) == cudaSuccess ? 0 : 2;
+    return cudaMemcpy(out, g_trace2, 8 * 48 * sizeof(long long), cudaMemcpyDeviceToHost) == cudaSuccess ? 0 : 2;
 }
 
 void launch_mlp_tc2(Ctx &c, int nb, cudaStream_t st)
@@ -830,8 +836,8 @@ void launch_mlp_tc2(Ctx &c, int nb, cudaStream_t st)
     {
         static long long *buf = nullptr;
         if (!buf)
-            check_cuda(cudaMalloc(&buf, 4 * 48 * sizeof(long long)), "trace buffer");
-        cudaMemsetAsync(buf, 0, 4 * 48 * sizeof(long long), st);
+            check_cuda(cudaMalloc(&buf, 8 * 48 * sizeof(long long)), "trace buffer");
+        cudaMemsetAsync(buf, 0, 8 * 48 * sizeof(long long), st);
         a.trace = buf;
         g_trace2 = buf;
     }
