@@ -119,8 +119,8 @@ int swr_render(swr_ctx *ctx, const float *pos_m, int64_t B, uint32_t flags, floa
  * uncaptured call with the same or a larger B has sized the work buffers; the
  * graph's replays then re-read d_pos_m and rewrite the outputs in place. Replays
  * share the context's work buffers, so the caller orders them against other calls
- * on the same context (same stream, or events). Every other entry point
- * synchronises with the host and refuses capture (SWR_EINVAL). */
+ * on the same context (same stream, or events). The other entry points that take
+ * a stream synchronise with the host and refuse a capturing one (SWR_EINVAL). */
 int swr_render_device(swr_ctx *ctx, const float *d_pos_m, int64_t B, uint32_t flags,
                       float *d_spectra, double *d_pooled, double *d_rssi, int32_t *d_aoa_rc,
                       double *d_aoa_ang, void *stream);

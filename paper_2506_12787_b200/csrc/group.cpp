@@ -86,6 +86,16 @@ const Nccl &nccl()
     return n;
 }
 
+// the group / communicator paths use host threads, several devices and NCCL
+// groups: not capturable into a CUDA graph (swr_render_device per context is)
+void refuse_capture(cudaStream_t user)
+{
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    if (cudaStreamIsCapturing(user, &cs) == cudaSuccess && cs != cudaStreamCaptureStatusNone)
+        throw std::invalid_argument("multi-GPU renders cannot be captured into a CUDA graph "
+                                    "(capture swr_render_device on each context instead)");
+}
+
 void api(int rc)
 {
     if (rc == SWR_OK)
@@ -379,6 +389,7 @@ int swr_group_render_device(swr_group *g, const float *d_pos, int64_t B, uint32_
         const bool want_pooled = (flags & SWR_OUT_POOLED) && d_pooled, want_rssi = (flags & SWR_OUT_RSSI) && d_rssi;
         const bool want_aoa = (flags & SWR_OUT_AOA) && (d_aoa_rc || d_aoa_ang);
         cudaStream_t user = (cudaStream_t)stream;
+        refuse_capture(user);
         // everything starts after the work already queued on the caller's stream
         check_cuda(cudaSetDevice(root.device), "cudaSetDevice");
         cudaEvent_t start;
@@ -633,6 +644,7 @@ int swr_render_gather(swr_comm *cm, const float *d_pos, const int64_t *counts, u
         api(swr_get_option(cm->ctx, "chunk", &ch));
         const int64_t chunk = std::max<int64_t>(1, int64_t(ch));
         cudaStream_t user = (cudaStream_t)stream;
+        refuse_capture(user);
         check_cuda(cudaSetDevice(cm->device), "cudaSetDevice");
         const bool spec = flags & SWR_OUT_SPECTRA;
         {
