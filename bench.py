@@ -603,7 +603,7 @@ def main():
                               d_rc[idx].cpu().numpy())
 
     cpu = None
-    if not args.no_cpu_baseline:
+    if not args.no_cpu_baseline and world == 1:  # the contract's CPU leg: rank 0 at N = 1 only
         cores = os.cpu_count()
         cpu = cpu_reference_rate(scene, random_positions(max(cores, 4), seed=99), cores, "blas")
         if cpu is not None:
