@@ -94,6 +94,10 @@ int swr_scene_get_layer(swr_ctx *ctx, int layer, int *rows, int *cols, float *w,
 int swr_scene_get_meta(swr_ctx *ctx, int64_t *iteration, uint64_t *manifest_hash);
 
 /* Options: "mlp_precision" (SWR_MLP_*), "chunk" (positions per device chunk),
+ * "copy_chunk" (swr_render with host spectra: positions per chunk and per raster /
+ * D2H slice, default 256 -- each chunk's copy runs under the next chunk's MLP),
+ * "async_pair_budget" (bytes of bin buffers a chunk may size to the scene's pair
+ * bound without a host read of the pair count; -1 = min(24 GiB, memory / 4)),
  * "rssi_slope" / "rssi_intercept" (affine RSSI calibration, tasks.cpp:60-94; read
  * from the trailer of an RSSI model, load_rssi_model tasks.cpp:139-150; SWR_OUT_RSSI
  * fails with SWR_ERUNTIME while the scene has none, as load_rssi_model does),

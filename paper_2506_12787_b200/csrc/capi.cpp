@@ -672,13 +672,13 @@ static void run_chunk(Ctx &c, const float *d_pos, int nb, bool normalized, bool 
     tm.finish();
 }
 
-constexpr int kCopySlice = 256; // positions per raster launch + D2H slice in swr_render (chunks above 256)
+// positions per raster launch + D2H slice in swr_render: option "copy_chunk" (Ctx::copy_chunk, default 256)
 
 // Raster launches of a chunk in swr_render, each slice's spectra copied out right
 // behind it: 256-position slices, except that the call's LAST chunk ends in halving
 // slices (.., 128, 64, 32, 32), so only ~32 spectra's copy is left exposed after
 // the last raster (a uniform small slice costs launch tails on every slice).
-static std::vector<int> copy_slices(int nb, bool last)
+static std::vector<int> copy_slices(int nb, bool last, int kCopySlice)
 {
     std::vector<int> v;
     int r = nb;
@@ -1169,6 +1169,12 @@ int swr_set_option(swr_ctx *ctx, const char *key, double value)
                 throw std::invalid_argument("chunk must be >= 1");
             c.chunk = int(std::min<double>(value, c.chunk_cap)); // pair offsets stay 32-bit
         }
+        else if (k == "copy_chunk")
+        {
+            if (value < 32)
+                throw std::invalid_argument("copy_chunk must be >= 32");
+            c.copy_chunk = int(std::min<double>(value, c.chunk_cap));
+        }
         else if (k == "rssi_slope")
         {
             c.rssi_slope = value;
@@ -1208,6 +1214,8 @@ int swr_get_option(swr_ctx *ctx, const char *key, double *value)
             *value = c.mlp_precision;
         else if (k == "chunk")
             *value = c.chunk;
+        else if (k == "copy_chunk")
+            *value = c.copy_chunk;
         else if (k == "rssi_slope")
             *value = c.rssi_slope;
         else if (k == "rssi_intercept")
@@ -1288,8 +1296,8 @@ int swr_render(swr_ctx *ctx, const float *pos_m, int64_t B, uint32_t flags, floa
         // 1,024-position batch takes ~4.7 ms at ~56 GB/s -- longer than the raster alone
         // at 10k Gaussians, 4.3 ms -- so copies left to the end would stay exposed)
         int64_t chunk = std::max<int64_t>(1, std::min<int64_t>(B, c.chunk));
-        if ((flags & SWR_OUT_SPECTRA) && spectra && chunk > kCopySlice)
-            chunk = kCopySlice;
+        if ((flags & SWR_OUT_SPECTRA) && spectra && chunk > c.copy_chunk)
+            chunk = c.copy_chunk;
         ensure_work(c, chunk);
         const size_t per = size_t(2) * c.g.H * c.g.W;
         // device staging (kept in the context across calls): positions, two
@@ -1337,7 +1345,7 @@ int swr_render(swr_ctx *ctx, const float *pos_m, int64_t B, uint32_t flags, floa
             };
             run_chunk(c, d_pos + 3 * b0, nb, false, use_mlp, false, want_spec ? d_spec[k] : nullptr, heads, flags,
                       d_pooled + b0, d_rssi + b0, d_rc + 2 * b0, d_ang + 2 * b0, st,
-                      want_spec ? copy_slices(nb, ci + 1 == sizes.size()) : std::vector<int>(),
+                      want_spec ? copy_slices(nb, ci + 1 == sizes.size(), c.copy_chunk) : std::vector<int>(),
                       want_spec ? std::function<void(int, int)>(copy_slice) : std::function<void(int, int)>());
             if (want_spec)
                 check_cuda(cudaEventRecord(freed[k], copy_st), "record");

@@ -3,7 +3,7 @@
 
 #include <cuda_runtime.h>
 
-// Device-side checks of the checked build (libswr_checked.so, build.py --checked):
+// Device-side checks of the checked build (libswr_checked.so, linked by build.py next to libswr.so):
 // an index or invariant that fails prints where and traps the kernel. compute-sanitizer
 // is unavailable on the GPU pool, so these stand in for memcheck / racecheck on the
 // render path (tests/test_checked.py). Compiled out of the product library.
@@ -145,6 +145,7 @@ struct Ctx
     int tile = 16;
     int mlp_precision = 0;
     int chunk = 256;
+    int copy_chunk = 256; // swr_render with host spectra: positions per chunk and per raster / D2H slice
     int chunk_cap = 1 << 30;            // largest chunk whose pair list fits 32-bit offsets (pair_bound)
     int64_t pairs_per_pos_max = 1;      // pair_bound: (tile, primitive) pairs of one position, any residuals
     bool stage_timing = false;
