@@ -708,6 +708,8 @@ static void device_render(Ctx &c, const float *d_pos, int64_t B, uint32_t flags,
                           double *d_rssi, int32_t *d_aoa_rc, double *d_aoa_ang, cudaStream_t st)
 {
     const bool use_mlp = c.has_net && !(flags & SWR_NO_RESIDUALS);
+    if (use_mlp && c.g.n < 1)
+        throw std::invalid_argument("empty gaussian set"); // predict_residuals (deform.cpp:147-148) via render_at
     const bool heads = flags & (SWR_OUT_POOLED | SWR_OUT_RSSI | SWR_OUT_AOA);
     const int64_t chunk = std::max<int64_t>(1, std::min<int64_t>(B, c.chunk));
     ensure_work(c, chunk);
@@ -1311,8 +1313,10 @@ int swr_render(swr_ctx *ctx, const float *pos_m, int64_t B, uint32_t flags, floa
         int32_t *d_rc = S.rc;
         cudaStream_t copy_st = S.copy;
         cudaEvent_t *done = S.done, *freed = S.freed;
-        check_cuda(cudaMemcpyAsync(d_pos, pos_m, sizeof(float) * 3 * B, cudaMemcpyHostToDevice, st), "H2D positions");
         const bool use_mlp = c.has_net && !(flags & SWR_NO_RESIDUALS);
+        if (use_mlp && c.g.n < 1)
+            throw std::invalid_argument("empty gaussian set"); // predict_residuals (deform.cpp:147-148) via render_at
+        check_cuda(cudaMemcpyAsync(d_pos, pos_m, sizeof(float) * 3 * B, cudaMemcpyHostToDevice, st), "H2D positions");
         const bool heads = flags & (SWR_OUT_POOLED | SWR_OUT_RSSI | SWR_OUT_AOA);
         int k = 0;
         // chunk sizes: `chunk` each; with spectra going to the host, the last one is halved,

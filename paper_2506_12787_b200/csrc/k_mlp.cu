@@ -138,6 +138,8 @@ void launch_center_terms(Ctx &c, const float *d_cenc, cudaStream_t st)
 {
     const float *wcen = c.net.wcen;
     const int total = c.g.np * 4 * c.net.wp;
+    if (total == 0)
+        return;
     center_terms_kernel<<<(total + 255) / 256, 256, 0, st>>>(d_cenc, wcen, c.net.cg, c.g.np, c.net.wp,
                                                                c.net.dc, c.net.width);
     c.launches++;
@@ -358,6 +360,8 @@ static void run_mlp(Ctx &c, int nb, cudaStream_t st, unsigned *amax = nullptr)
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, mlp_fp32_kernel<TM, NJ>, 256, smem);
     const long tiles = (long)a.n_gblk * a.n_sblk;
     const long grid = std::min<long>(tiles, (long)dev_sms * std::max(per_sm, 1));
+    if (grid == 0)
+        return;
     mlp_fp32_kernel<TM, NJ><<<(unsigned)grid, 256, smem, st>>>(a);
     c.launches++;
 }

@@ -842,6 +842,8 @@ void launch_mlp_tc2(Ctx &c, int nb, cudaStream_t st)
         g_trace2 = buf;
     }
     const int grid = 2 * std::min(max_clusters, a.ntiles);
+    if (grid == 0)
+        return;
     if (c.mlp_precision == 1)
         mlp_tc2_kernel<true><<<grid, THREADS, SMEM_BYTES, st>>>(a);
     else

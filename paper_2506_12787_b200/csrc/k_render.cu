@@ -181,6 +181,8 @@ __global__ void __launch_bounds__(256) setup_kernel(Grid g, SceneDev sd, const f
 void launch_setup(Ctx &c, int nb, bool with_res, cudaStream_t st)
 {
     dim3 grid((c.g.np / 4 + 255) / 256, nb);
+    if (grid.x == 0) // empty Gaussian set: nothing to set up (the counts are never read)
+        return;
     setup_kernel<<<grid, 256, 0, st>>>(c.g, c.s, c.w.res, c.w.cap_b * c.g.np, c.w.dyn, c.w.rng, c.w.cnt, with_res,
                                        with_res ? c.w.stats + 2 : nullptr, c.gate);
     c.launches++;
@@ -558,7 +560,8 @@ void launch_bin_sort(Ctx &c, int nb, int64_t pairs, int max_seg, cudaStream_t st
 {
     const int tiles = c.g.tiles;
     dim3 ge((c.g.n + 255) / 256, nb);
-    emit_kernel<<<ge, 256, 0, st>>>(c.g, c.w.rng, c.w.poff, c.w.seg, c.w.keys, c.w.vals, c.w.cap_pairs);
+    if (ge.x > 0) // an empty set emits no pairs (the sort still writes empty tile lists)
+        emit_kernel<<<ge, 256, 0, st>>>(c.g, c.w.rng, c.w.poff, c.w.seg, c.w.keys, c.w.vals, c.w.cap_pairs);
     // sort CTAs per position: the chunk count of max_seg -- the longest segment when the
     // host knows it, else an estimate (the CTAs loop over chunks, so a longer segment
     // is still covered, only with fewer CTAs)

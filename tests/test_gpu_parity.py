@@ -365,6 +365,31 @@ def test_errors_follow_reference_types(tmp_path, scene2k):
                                         atten_logit=sc.atten_logit, response=sc.response))
 
 
+def test_empty_gaussian_set_follows_the_reference():
+    """n = 0: render_at's predict_residuals throws invalid_argument("empty gaussian
+    set") (deform.cpp:147-148); rasterize without residuals gives the all-zero
+    spectrum (and its heads: pooled 0, AoA at the first cell, RSSI = intercept)."""
+    import dataclasses
+    base = make_scene(10, seed=1, width=16)
+    base.rssi_cal = (2.0, -50.0)
+    empty = dataclasses.replace(base, center_raw=base.center_raw[:0], cholesky=base.cholesky[:0],
+                                atten_logit=base.atten_logit[:0], response=base.response[:0])
+    pos = random_positions(3, seed=2)
+    ck = swr.Checkpoint.from_scene(empty)
+    with pytest.raises(ValueError, match="empty gaussian set"):
+        swr.render(ck, pos, rssi=True)
+    for sc, kw in ((empty, dict(residuals=False)), (dataclasses.replace(empty, weights=[], biases=[]), {})):
+        out = swr.render(swr.Checkpoint.from_scene(sc), pos, rssi=True, **kw)
+        assert out["spectra"].shape == (3, sc.H, sc.W, 2) and not out["spectra"].any()
+        assert not out["pooled"].any()
+        assert np.all(out["rssi"] == -50.0)
+        port = O.Port(sc)
+        assert not port.rasterize().any()
+        r, c, el, az = port.aoa(np.zeros((sc.H, sc.W, 2), np.float32))
+        assert np.all(out["aoa_rc"] == (r, c))
+        assert np.all(out["aoa_ang"] == (el, az))
+
+
 # ---------------------------------------------------------- tensor-core MLP
 
 def _mlp_errors(ck, port, p01, idx):
