@@ -390,6 +390,33 @@ def test_empty_gaussian_set_follows_the_reference():
         assert np.all(out["aoa_ang"] == (el, az))
 
 
+def test_nonfinite_positions_are_contained(scene2k, ck2k):
+    """NaN / inf / 1e30 TX positions (undefined behaviour in the reference) neither
+    trap nor hang (the checked build runs this too) and leave the finite positions
+    of the batch at their own render's value: identical bits when their chunk holds
+    no bad position, within the FP32-grade bar where the bad neighbour made the
+    chunk re-run its MLP in FP32."""
+    pos = random_positions(40, seed=3)
+    bad = [1, 2, 3, 4, 5]
+    pos[1] = np.nan
+    pos[2, 0] = np.inf
+    pos[3] = -np.inf
+    pos[4] = 1e30
+    pos[5] = -1e30
+    ck = swr.Checkpoint.from_scene(scene2k)
+    ck.set_option("chunk", 16)
+    out = swr.render(ck, pos)
+    assert out["spectra"].shape == (40, scene2k.H, scene2k.W, 2)
+    good = [i for i in range(40) if i not in bad]
+    alone = swr.render(ck, pos[good])
+    for j, i in enumerate(good):
+        a, b = out["spectra"][i], alone["spectra"][j]
+        if i >= 16:                                  # chunks without a bad position: same kernels, same bits
+            assert np.array_equal(a, b), i
+        else:
+            assert np.abs(a - b).max() <= spec_tol(b), i
+
+
 # ---------------------------------------------------------- tensor-core MLP
 
 def _mlp_errors(ck, port, p01, idx):
