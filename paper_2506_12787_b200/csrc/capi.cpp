@@ -1171,6 +1171,10 @@ int swr_set_option(swr_ctx *ctx, const char *key, double value)
                 throw std::invalid_argument("chunk must be >= 1");
             c.chunk = int(std::min<double>(value, c.chunk_cap)); // pair offsets stay 32-bit
         }
+        else if (k == "mlp_max_clusters")
+            c.mlp_max_clusters = int(value);
+        else if (k == "mlp_smem_pad")
+            c.mlp_smem_pad = int(value);
         else if (k == "copy_chunk")
         {
             if (value < 32)

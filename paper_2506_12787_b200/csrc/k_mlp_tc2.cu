@@ -788,8 +788,8 @@ void launch_mlp_tc2(Ctx &c, int nb, cudaStream_t st)
     const int max_clusters = once.get(c.device, [] {
         for (auto k : {mlp_tc2_kernel<true>, mlp_tc2_kernel<false>})
         {
-            check_cuda(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES),
-                       "tc2 mlp smem attribute");
+            check_cuda(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024),
+                       "tc2 mlp smem attribute"); // SMEM_BYTES + the optional pad (mlp_smem_pad)
             check_cuda(cudaFuncSetAttribute(k, cudaFuncAttributePreferredSharedMemoryCarveout,
                                             (int)cudaSharedmemCarveoutMaxShared),
                        "tc2 mlp carveout");
@@ -841,13 +841,15 @@ void launch_mlp_tc2(Ctx &c, int nb, cudaStream_t st)
         a.trace = buf;
         g_trace2 = buf;
     }
-    const int grid = 2 * std::min(max_clusters, a.ntiles);
+    const int cap = c.mlp_max_clusters > 0 ? std::min(c.mlp_max_clusters, max_clusters) : max_clusters;
+    const int grid = 2 * std::min(cap, a.ntiles);
     if (grid == 0)
         return;
+    const int smem = std::min(SMEM_BYTES + std::max(c.mlp_smem_pad, 0), 227 * 1024);
     if (c.mlp_precision == 1)
-        mlp_tc2_kernel<true><<<grid, THREADS, SMEM_BYTES, st>>>(a);
+        mlp_tc2_kernel<true><<<grid, THREADS, smem, st>>>(a);
     else
-        mlp_tc2_kernel<false><<<grid, THREADS, SMEM_BYTES, st>>>(a);
+        mlp_tc2_kernel<false><<<grid, THREADS, smem, st>>>(a);
     c.launches++;
 }
 

@@ -160,6 +160,9 @@ struct Ctx
     const int64_t *gate = nullptr;      // set while launching the FP32 re-run chain: kernels run only if *gate != 0
     size_t mem_total = 0;               // device memory, bytes (async pair-buffer budget)
     int64_t wide_block_rows = int64_t(1) << 21; // width-512 MLP: rows per layer-GEMM block (option "wide_block_rows")
+    // experiment knobs (tools/experiments/round2/partition_exp.py): cap on the tcgen05 MLP's CTA pairs
+    // (0 = as many as fit) and extra dynamic shared memory per MLP CTA (keeps raster CTAs off its SMs)
+    int mlp_max_clusters = 0, mlp_smem_pad = 0;
     int64_t async_pair_budget = -1;     // pair-buffer bytes per chunk for the host-sync-free path (-1: default)
     double stage_ms[6]{};               // accumulated while stage_timing is on (swr_stage_times resolves)
     std::vector<std::array<cudaEvent_t, 7>> stage_pending; // recorded per chunk, read lazily
