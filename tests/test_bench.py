@@ -42,3 +42,35 @@ def test_native_line_carries_the_contract():
     assert 0 < r["frac"] < 1 and r["bound"] == "tensor" and r["kernel"] == "deform MLP (mlp_tc2_kernel)"
     assert d["parity_ok"] is True and d["parity"]["aoa_ok"] is True
     assert d["cpu_baseline"] is None or d["cpu_baseline"]["value"] > 0
+
+
+@pytest.mark.gpu
+@pytest.mark.skipif(not has_ref(), reason="reference build absent")
+def test_parity_check_is_not_vacuous():
+    """bench.parity_check (the post-timing check behind parity_ok) passes the GPU's own
+    outputs and fails each kind of corruption: one cell off by 1e-4 of the peak, the
+    pooled magnitude off by 1e-4 relative, the AoA moved to a non-tied cell."""
+    import numpy as np
+    sys.path.insert(0, ROOT)
+    import bench
+    from paper_2506_12787_b200 import swr
+    from paper_2506_12787_b200.scene import make_scene, random_positions
+    sc = make_scene(1500, seed=4)
+    ck = swr.Checkpoint.from_scene(sc)
+    pos = random_positions(4, seed=8)
+    out = swr.render(ck, pos)
+    idx = np.arange(4)
+    args = (ck, sc, pos, idx)
+    good = bench.parity_check(*args, out["spectra"].copy(), out["pooled"].copy(), out["aoa_rc"].copy())
+    assert good["ok"], good
+    spec = out["spectra"].copy()
+    spec[1, 40, 100, 0] += 1e-4 * max(1.0, float(np.abs(spec[1]).max()))
+    assert not bench.parity_check(*args, spec, out["pooled"], out["aoa_rc"])["ok"]
+    pooled = out["pooled"].copy()
+    pooled[2] *= 1 + 1e-4
+    assert not bench.parity_check(*args, out["spectra"], pooled, out["aoa_rc"])["ok"]
+    rc = out["aoa_rc"].copy()
+    mag = np.hypot(out["spectra"][3][..., 0].astype(np.float64), out["spectra"][3][..., 1])
+    r, c = np.unravel_index(int(np.argmin(mag)), mag.shape)     # the weakest cell: no tie with the peak
+    rc[3] = (r, c)
+    assert not bench.parity_check(*args, out["spectra"], out["pooled"], rc)["ok"]
