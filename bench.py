@@ -210,7 +210,7 @@ def run_reference_arm(args, scene, rank):
         return None
     cores = os.cpu_count()
     rng_pos = __import__("paper_2506_12787_b200.scene", fromlist=["random_positions"]).random_positions
-    per_step = max(cores, 4)
+    per_step = 4 * max(cores, 4)  # ~2-3 s of CPU work per step at 50k Gaussians on 16 cores
     pos = rng_pos(per_step, seed=99)
     res = None
     times = []
