@@ -670,7 +670,7 @@ constexpr int kSweepUnroll = SWR_SWEEP_UNROLL;
 
 // ---------------------------------------------------------------- raster
 //
-// One CTA of 4 warps per (tile, position), 8 CTAs resident per SM. The tile's pair
+// One CTA of 4 warps per (tile, position), 9 CTAs resident per SM. The tile's pair
 // list (ascending primitive index, splat.cpp:251-292) is cut into chunks of 32;
 // warp w takes chunks w, w+4, ... For a chunk, each lane first turns one pair into a
 // record (gathers the pair's dynamic state, shape and box, clips it to the tile:
@@ -679,7 +679,8 @@ constexpr int kSweepUnroll = SWR_SWEEP_UNROLL;
 // by sweep count (bitonic, shuffles) and stores them in that order, so similar
 // records pair up. Each half-warp then evaluates one record at a time: its 16 lanes
 // write the record's row table (d_el, q_c = i00 d_el^2, or +inf where the reference
-// skips the row, splat.cpp:405-408; double-buffered, one __syncwarp per record),
+// skips the row, splat.cpp:405-408, and the row's swizzled accumulator address;
+// single-buffered with SWR_RASTER_SLIM, a __syncwarp before and after the write),
 // map themselves onto the clipped box (magic division: lane -> (row, column)),
 // compute their column's w1 / w2 and sweep rows lr, lr + rpi, ... with a
 // pointer-bounded loop (each lane its own trip count). Each half-warp accumulates
